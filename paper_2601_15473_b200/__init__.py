@@ -1,0 +1,249 @@
+"""paper_2601_15473_b200 -- B200-native SKLinear hot path (Panther / pawX).
+
+Python host mirror of the reference's ``rnla::nn::SkLinear`` API
+(/root/reference/proj/include/rnla/nn/layers.hpp:52-92) over the C-ABI of
+``libskl.so`` (include/skl.h).  PyTorch is used only for device memory and
+streams; all arithmetic runs in the sm_100a kernels of ``libskl.so``.  There
+is no CPU fallback: importing works anywhere, but every compute call raises
+when the library or an sm_100 GPU is missing.
+
+    layer = SkLinear(d_in=768, d_out=3072, num_terms=2, low_rank=128, seed=42)
+    y = layer.forward(x)                      # x [T, d_in]   (row convention)
+    grads = layer.backward(x, g)              # Grads(grad_x, grad_u1, grad_u2, grad_b)
+
+Naming follows pawX (row convention, [L, d, k] stacks; see include/skl.h for
+the exact mapping onto the reference's per-term s1/u1/s2/u2).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libskl.so")
+
+SKL_OK = 0
+STATUS = {0: "SKL_OK", 1: "SKL_ERR_SHAPE", 2: "SKL_ERR_PARAM", 3: "SKL_ERR_CUDA", 4: "SKL_ERR_NCCL",
+          5: "SKL_ERR_UNSUPPORTED", 6: "SKL_ERR_WORKSPACE"}
+GAUSSIAN, RADEMACHER = 0, 1
+F32_TF32, BF16 = 0, 1
+OUT_F64, OUT_F32, OUT_BF16 = 0, 1, 2
+
+ABI_SYMBOLS = (
+    "skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed", "skl_params", "skl_exceeds_dense",
+    "skl_generate_sketches", "skl_init_params", "skl_realize_sketch", "skl_workspace_size",
+    "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads",
+)
+
+
+class SklError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class ShapeError(SklError, ValueError):
+    """rnla::shape_error (errors.hpp:10-13)."""
+
+
+class ParameterError(SklError, ValueError):
+    """rnla::parameter_error (errors.hpp:16-19)."""
+
+
+class _Shape(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_int64), ("d_out", ctypes.c_int64), ("num_terms", ctypes.c_int64),
+                ("low_rank", ctypes.c_int64), ("dtype", ctypes.c_int)]
+
+
+class _ParamCount(ctypes.Structure):
+    _fields_ = [("learnable", ctypes.c_uint64), ("total_stored", ctypes.c_uint64),
+                ("dense_equivalent", ctypes.c_uint64)]
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libskl.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                          " (there is no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, u64, sz = ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+    sp = ctypes.POINTER(_Shape)
+    for name in ("skl_version", "skl_last_error", "skl_rng_algorithm"):
+        getattr(L, name).restype = ctypes.c_char_p
+    L.skl_derive_seed.restype = u64
+    L.skl_derive_seed.argtypes = [u64, u64]
+    L.skl_params.argtypes = [sp, ctypes.POINTER(_ParamCount)]
+    L.skl_exceeds_dense.argtypes = [u64] * 4
+    L.skl_generate_sketches.argtypes = [sp, ctypes.c_int, u64, vp, vp, vp]
+    L.skl_init_params.argtypes = [sp, u64, vp, vp, vp]
+    L.skl_realize_sketch.argtypes = [ctypes.c_int, i64, i64, u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp]
+    L.skl_workspace_size.argtypes = [sp, i64, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+    L.sketched_linear_forward.argtypes = [sp, i64] + [vp] * 9 + [sz, vp]
+    L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 13 + [sz, vp]
+    L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
+    for name in ABI_SYMBOLS:
+        if name not in ("skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed",
+                        "skl_exceeds_dense"):
+            getattr(L, name).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status == SKL_OK:
+        return
+    msg = lib().skl_last_error().decode()
+    if status == 1:
+        raise ShapeError(status, msg)
+    if status == 2:
+        raise ParameterError(status, msg)
+    raise SklError(status, msg)
+
+
+def derive_seed(master: int, index: int) -> int:
+    return int(lib().skl_derive_seed(master, index))
+
+
+def exceeds_dense(l, k, d_in, d_out) -> bool:
+    return bool(lib().skl_exceeds_dense(l, k, d_in, d_out))
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def shape(d_in, d_out, num_terms, low_rank, dtype=BF16) -> _Shape:
+    return _Shape(d_in, d_out, num_terms, low_rank, dtype)
+
+
+def torch_dtype(dtype: int):
+    import torch
+    return torch.bfloat16 if dtype == BF16 else torch.float32
+
+
+def workspace_size(s: _Shape, T: int):
+    f, b = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().skl_workspace_size(ctypes.byref(s), T, ctypes.byref(f), ctypes.byref(b)))
+    return f.value, b.value
+
+
+def params(s: _Shape):
+    pc = _ParamCount()
+    _check(lib().skl_params(ctypes.byref(s), ctypes.byref(pc)))
+    return pc.learnable, pc.total_stored, pc.dense_equivalent
+
+
+def realize_sketch(dist, k, d, seed, out, unit_variance=False, transpose=False, stream=None):
+    """realize_sketch / gaussian_matrix on device into `out` (f64/f32/bf16 tensor)."""
+    import torch
+    ot = {torch.float64: OUT_F64, torch.float32: OUT_F32, torch.bfloat16: OUT_BF16}[out.dtype]
+    _check(lib().skl_realize_sketch(dist, k, d, seed, int(unit_variance), int(transpose), ot, _ptr(out),
+                                    _stream(stream)))
+    return out
+
+
+def generate_sketches(s: _Shape, dist, seed, S1s, S2s, stream=None):
+    _check(lib().skl_generate_sketches(ctypes.byref(s), dist, seed, _ptr(S1s), _ptr(S2s), _stream(stream)))
+
+
+def init_params(s: _Shape, seed, U1s, U2s, stream=None):
+    _check(lib().skl_init_params(ctypes.byref(s), seed, _ptr(U1s), _ptr(U2s), _stream(stream)))
+
+
+def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None):
+    T = x.shape[0]
+    _check(lib().sketched_linear_forward(ctypes.byref(s), T, _ptr(x), _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s),
+                                         _ptr(bias), _ptr(y), _ptr(saved), _ptr(workspace),
+                                         workspace.numel() if workspace is not None else 0, _stream(stream)))
+
+
+def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace, stream=None):
+    T = x.shape[0]
+    _check(lib().sketched_linear_backward(ctypes.byref(s), T, _ptr(g), _ptr(x), _ptr(saved), _ptr(S1s), _ptr(S2s),
+                                          _ptr(U1s), _ptr(U2s), _ptr(grad_x), _ptr(dU1s), _ptr(dU2s), _ptr(db),
+                                          _ptr(workspace), workspace.numel() if workspace is not None else 0,
+                                          _stream(stream)))
+
+
+@dataclass
+class Grads:
+    """SkLinear::Grads (layers.hpp:72-78) in ABI layout."""
+
+    grad_x: object   # [T, d_in]
+    grad_u1: object  # dU1s [L, k, d_out] fp32
+    grad_u2: object  # dU2s [L, d_in, k] fp32
+    grad_b: object   # [d_out] fp32
+
+
+class SkLinear:
+    """Device-resident mirror of rnla::nn::SkLinear (layers.hpp:62-81).
+
+    Construction follows sk_linear_fresh (nn_layers.cpp:133-147): sketches from
+    derive_seed(seed, 2i / 2i+1), U ~ N(0, 2/(d_in+d_out)) from
+    derive_seed(seed, 1000+i), zero bias -- all generated on the GPU.
+    """
+
+    def __init__(self, d_in, d_out, num_terms, low_rank, seed=0, dist=GAUSSIAN, dtype=BF16, device="cuda"):
+        import torch
+        if num_terms < 1 or low_rank < 1:
+            raise ParameterError(2, "SkLinear: num_terms and low_rank must be >= 1")
+        self.d_in, self.d_out, self.num_terms, self.low_rank = d_in, d_out, num_terms, low_rank
+        self.seed, self.dist, self.dtype = seed, dist, dtype
+        self.shape = shape(d_in, d_out, num_terms, low_rank, dtype)
+        td = torch_dtype(dtype)
+        L, k = num_terms, low_rank
+        self.S1s = torch.empty(L, d_in, k, dtype=td, device=device)
+        self.S2s = torch.empty(L, k, d_out, dtype=td, device=device)
+        self.U1s = torch.empty(L, k, d_out, dtype=td, device=device)
+        self.U2s = torch.empty(L, d_in, k, dtype=td, device=device)
+        self.bias = torch.zeros(d_out, dtype=td, device=device)
+        generate_sketches(self.shape, dist, seed, self.S1s, self.S2s)
+        init_params(self.shape, seed, self.U1s, self.U2s)
+        self._ws = None
+
+    def params(self):
+        """SkLinear::params -> (learnable, total_stored, dense_equivalent)."""
+        return params(self.shape)
+
+    def workspace(self, T):
+        import torch
+        need = max(workspace_size(self.shape, T))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.S1s.device)
+        return self._ws
+
+    def forward(self, x, saved=None):
+        import torch
+        if x.dim() != 2 or x.shape[1] != self.d_in:
+            raise ShapeError(1, "SkLinear::forward: input columns != d_in")
+        y = torch.empty(x.shape[0], self.d_out, dtype=x.dtype, device=x.device)
+        forward(self.shape, x, self.S1s, self.S2s, self.U1s, self.U2s, self.bias, y, saved,
+                self.workspace(x.shape[0]))
+        return y
+
+    def backward(self, x, g, saved=None) -> Grads:
+        import torch
+        if x.shape[1] != self.d_in or g.shape[1] != self.d_out or x.shape[0] != g.shape[0]:
+            raise ShapeError(1, "SkLinear::backward: shape mismatch")
+        T = x.shape[0]
+        dev = x.device
+        gx = torch.empty(T, self.d_in, dtype=x.dtype, device=dev)
+        du1 = torch.empty(self.num_terms, self.low_rank, self.d_out, dtype=torch.float32, device=dev)
+        du2 = torch.empty(self.num_terms, self.d_in, self.low_rank, dtype=torch.float32, device=dev)
+        db = torch.empty(self.d_out, dtype=torch.float32, device=dev)
+        backward(self.shape, g, x, saved, self.S1s, self.S2s, self.U1s, self.U2s, gx, du1, du2, db,
+                 self.workspace(T))
+        return Grads(gx, du1, du2, db)

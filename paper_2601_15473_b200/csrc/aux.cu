@@ -1,0 +1,337 @@
+// aux.cu -- the non-GEMM kernels of the SKLinear path (all HBM/latency-bound
+// integer or byte work, written as plain coalesced CUDA):
+//
+//   * device sketch generator: counter-based SplitMix64 -> Box-Muller /
+//     sign bit, bit-exact integer chain of the reference stream
+//     (rng.hpp:13-69, sketch.cpp:34-49, nn_layers.cpp:124-145)
+//   * parameter packing: pawX [L,d,k] stacks -> the K-major operand panels the
+//     tcgen05 kernels stream (Acat / Bcat and their transposes), with TF32
+//     round-to-nearest for the fp32 variant
+//   * deterministic split-K reduction (fixed order) + layout scatter
+//   * deterministic column sum (db = row_sums(G), nn_layers.cpp:23-30,99)
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "skl_internal.h"
+#include "sm100.cuh"
+
+namespace skl {
+namespace {
+
+// ---------------------------------------------------------------- RNG
+// Draw j (0-based) of Splitmix64(seed): state after j+1 increments.
+__device__ __forceinline__ uint64_t sm64_draw(uint64_t seed, uint64_t j) {
+    uint64_t z = seed + (j + 1) * 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t derive_seed_dev(uint64_t master, uint64_t index) {
+    return sm64_draw(master ^ (0x517cc1b727220a95ULL + index), 0);
+}
+// rng.hpp:25-27 next_open01, IEEE ops spelled out (no contraction).
+__device__ __forceinline__ double open01(uint64_t x) {
+    return __dmul_rn(__dadd_rn((double)(x >> 11), 0.5), 0x1.0p-53);
+}
+// Entry e of GaussianStream(seed) (rng.hpp:45-57): pair p = e/2 uses draws
+// 2p and 2p+1; even e -> r cos(theta), odd e -> the cached r sin(theta).
+__device__ __forceinline__ double gauss_at(uint64_t seed, uint64_t e) {
+    const uint64_t p = e >> 1;
+    const double u1 = open01(sm64_draw(seed, 2 * p));
+    const double u2 = open01(sm64_draw(seed, 2 * p + 1));
+    const double r = __dsqrt_rn(__dmul_rn(-2.0, log(u1)));
+    const double theta = __dmul_rn(6.283185307179586, u2);  // 2.0 * 3.14159265358979323846
+    double s, c;
+    sincos(theta, &s, &c);
+    return __dmul_rn(r, (e & 1) ? s : c);
+}
+
+template <typename T>
+__device__ __forceinline__ void store_val(void* out, uint64_t idx, double v);
+template <>
+__device__ __forceinline__ void store_val<double>(void* out, uint64_t idx, double v) {
+    reinterpret_cast<double*>(out)[idx] = v;
+}
+template <>
+__device__ __forceinline__ void store_val<float>(void* out, uint64_t idx, double v) {
+    reinterpret_cast<float*>(out)[idx] = __double2float_rn(v);
+}
+template <>
+__device__ __forceinline__ void store_val<__nv_bfloat16>(void* out, uint64_t idx, double v) {
+    reinterpret_cast<__nv_bfloat16*>(out)[idx] = __double2bfloat16(v);
+}
+
+// realize_sketch(dist, k, d, seed) entry (row, col) of the [k, d] matrix.
+__device__ __forceinline__ double sketch_entry(int dist, uint64_t seed, uint64_t d, uint64_t row, uint64_t col,
+                                               double scale) {
+    const uint64_t e = row * d + col;
+    if (dist == 1) return (sm64_draw(seed, e) >> 63) ? scale : -scale;  // rng.hpp:30, sketch.cpp:44-49
+    return __dmul_rn(gauss_at(seed, e), scale);                          // sketch.cpp:38-43
+}
+
+// All sketches of a layer, directly in the ABI stacks:
+//   S1s[i][c][j] = realize(dist,k,d_in, derive_seed(seed,2i+1))[j][c]
+//   S2s[i][j][o] = realize(dist,k,d_out,derive_seed(seed,2i))[j][o]
+template <typename T>
+__global__ void gen_sketches_kernel(int dist, uint64_t layer_seed, int64_t L, int64_t k, int64_t d_in,
+                                    int64_t d_out, double scale, void* S1s, void* S2s) {
+    const uint64_t n1 = (uint64_t)L * d_in * k;
+    const uint64_t n2 = (uint64_t)L * k * d_out;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n1 + n2;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        if (idx < n1) {
+            const uint64_t i = idx / (d_in * k), rem = idx % (d_in * k);
+            const uint64_t c = rem / k, j = rem % k;
+            const uint64_t seed = derive_seed_dev(layer_seed, 2 * i + 1);
+            store_val<T>(S1s, idx, sketch_entry(dist, seed, d_in, j, c, scale));
+        } else {
+            const uint64_t id2 = idx - n1;
+            const uint64_t i = id2 / (k * d_out), rem = id2 % (k * d_out);
+            const uint64_t j = rem / d_out, o = rem % d_out;
+            const uint64_t seed = derive_seed_dev(layer_seed, 2 * i);
+            store_val<T>(S2s, id2, sketch_entry(dist, seed, d_out, j, o, scale));
+        }
+    }
+}
+
+// sk_linear_fresh U (nn_layers.cpp:136-145): stream g_i = GaussianStream(
+// derive_seed(seed,1000+i)); u1 [k][d_in] = g[0 .. k*d_in), u2 [d_out][k]
+// = g[k*d_in ..).  U2s[i][c][j] = u1[j][c], U1s[i][j][o] = u2[o][j].
+template <typename T>
+__global__ void init_u_kernel(uint64_t layer_seed, int64_t L, int64_t k, int64_t d_in, int64_t d_out,
+                              double std_dev, void* U1s, void* U2s) {
+    const uint64_t n2 = (uint64_t)L * d_in * k;
+    const uint64_t n1 = (uint64_t)L * k * d_out;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n1 + n2;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        if (idx < n2) {
+            const uint64_t i = idx / (d_in * k), rem = idx % (d_in * k);
+            const uint64_t c = rem / k, j = rem % k;
+            const uint64_t seed = derive_seed_dev(layer_seed, 1000 + i);
+            store_val<T>(U2s, idx, __dmul_rn(gauss_at(seed, j * d_in + c), std_dev));
+        } else {
+            const uint64_t id1 = idx - n2;
+            const uint64_t i = id1 / (k * d_out), rem = id1 % (k * d_out);
+            const uint64_t j = rem / d_out, o = rem % d_out;
+            const uint64_t seed = derive_seed_dev(layer_seed, 1000 + i);
+            store_val<T>(U1s, id1, __dmul_rn(gauss_at(seed, (uint64_t)k * d_in + o * k + j), std_dev));
+        }
+    }
+}
+
+template <typename T>
+__global__ void realize_kernel(int dist, int64_t k, int64_t d, uint64_t seed, double scale, int unit_var,
+                               int transpose, void* out) {
+    const uint64_t n = (uint64_t)k * d;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < n;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t row, col;
+        if (transpose) { col = idx / k; row = idx % k; }
+        else { row = idx / d; col = idx % d; }
+        double v;
+        if (unit_var) v = gauss_at(seed, row * d + col);  // gaussian_matrix, sketch.cpp:120-125
+        else v = sketch_entry(dist, seed, d, row, col, scale);
+        store_val<T>(out, idx, v);
+    }
+}
+
+// ---------------------------------------------------------------- packing
+template <typename T>
+__device__ __forceinline__ float ld_f(const void* p, uint64_t i) {
+    if constexpr (sizeof(T) == 2) return __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(p)[i]);
+    else return reinterpret_cast<const float*>(p)[i];
+}
+
+// Acat [d_in][R_pad]: column r < Lk -> S1s[r/k][c][r%k], Lk <= r < 2Lk ->
+// U2s[..], zero padding.  Bcat [R_pad][d_out]: row r < Lk -> U1s[r/k][r%k][:],
+// then S2s, zero padding.  Operand element type: bf16 copy, or fp32 rounded
+// to TF32 (cvt.rna) for the tf32 variant.
+template <typename T>
+__global__ void pack_cat_kernel(const void* S1s, const void* U2s, const void* U1s, const void* S2s, int64_t L,
+                                int64_t k, int64_t d_in, int64_t d_out, int64_t R_pad, void* Acat, void* Bcat) {
+    const int64_t Lk = L * k;
+    const uint64_t na = (uint64_t)d_in * R_pad, nb = (uint64_t)R_pad * d_out;
+    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < na + nb;
+         idx += (uint64_t)gridDim.x * blockDim.x) {
+        float v = 0.f;
+        uint64_t o = idx;
+        if (idx < na) {
+            const int64_t c = idx / R_pad, r = idx % R_pad;
+            if (r < Lk) v = ld_f<T>(S1s, ((r / k) * d_in + c) * k + r % k);
+            else if (r < 2 * Lk) v = ld_f<T>(U2s, (((r - Lk) / k) * d_in + c) * k + (r - Lk) % k);
+        } else {
+            o = idx - na;
+            const int64_t r = o / d_out, c = o % d_out;
+            if (r < Lk) v = ld_f<T>(U1s, r * d_out + c);
+            else if (r < 2 * Lk) v = ld_f<T>(S2s, (r - Lk) * d_out + c);
+        }
+        if constexpr (sizeof(T) == 2) {
+            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(idx < na ? Acat : Bcat);
+            dst[o] = __float2bfloat16_rn(v);
+        } else {
+            float* dst = reinterpret_cast<float*>(idx < na ? Acat : Bcat);
+            dst[o] = dev::tf32_rna(v);
+        }
+    }
+}
+
+// out[c][r] = in[r][c], in is [rows][cols]; 32x32 smem tiles.
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t cols) {
+    __shared__ T tile[32][33];
+    const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t r = r0 + i, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int64_t c = c0 + i, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
+    }
+}
+
+template <typename T>
+__global__ void to_f32_kernel(const void* in, float* out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = in ? ld_f<T>(in, i) : 0.f;
+}
+
+// ---------------------------------------------------------------- reductions
+// out[(n / nb) * blk + m * ldm + n % nb] = alpha * sum_{s=0..S-1} part[s][m][n]
+__global__ void reduce_partials_kernel(const float* __restrict__ part, int S, int64_t M, int64_t N, float alpha,
+                                       float* __restrict__ out, int64_t nb, int64_t blk, int64_t ldm) {
+    const int64_t MN = M * N;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.f;
+        for (int s = 0; s < S; ++s) acc += part[s * MN + i];
+        const int64_t m = i / N, n = i % N;
+        out[(n / nb) * blk + m * ldm + n % nb] = acc * alpha;
+    }
+}
+
+// Column sums of G [T][N] in two fixed-order stages: chunk c sums rows
+// [c*rows_per, (c+1)*rows_per) into part[c][N]; then part is reduced.
+template <typename T>
+__global__ void colsum_partial_kernel(const void* G, int64_t rows, int64_t N, int64_t rows_per, float* part) {
+    const int64_t c = blockIdx.y;
+    const int64_t r0 = c * rows_per, r1 = min(rows, r0 + rows_per);
+    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
+        float acc = 0.f;
+        for (int64_t r = r0; r < r1; ++r) acc += ld_f<T>(G, r * N + n);
+        part[c * N + n] = acc;
+    }
+}
+
+inline int grid_for(uint64_t n, int block = 256) {
+    uint64_t g = (n + block - 1) / block;
+    if (g > 148ull * 16) g = 148ull * 16;
+    return (int)(g ? g : 1);
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- launchers
+cudaError_t launch_gen_sketches(int dist, uint64_t seed, const SklDims& d, int elem, void* S1s, void* S2s,
+                                cudaStream_t st) {
+    const double scale = 1.0 / sqrt((double)d.k);
+    const uint64_t n = (uint64_t)d.L * d.k * (d.d_in + d.d_out);
+    if (elem == ELEM_BF16)
+        gen_sketches_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(dist, seed, d.L, d.k, d.d_in, d.d_out,
+                                                                        scale, S1s, S2s);
+    else if (elem == ELEM_F32)
+        gen_sketches_kernel<float><<<grid_for(n), 256, 0, st>>>(dist, seed, d.L, d.k, d.d_in, d.d_out, scale, S1s,
+                                                                S2s);
+    else
+        gen_sketches_kernel<double><<<grid_for(n), 256, 0, st>>>(dist, seed, d.L, d.k, d.d_in, d.d_out, scale,
+                                                                 S1s, S2s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_u(uint64_t seed, const SklDims& d, int elem, void* U1s, void* U2s, cudaStream_t st) {
+    const double std_dev = sqrt(2.0 / (double)(d.d_in + d.d_out));
+    const uint64_t n = (uint64_t)d.L * d.k * (d.d_in + d.d_out);
+    if (elem == ELEM_BF16)
+        init_u_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(seed, d.L, d.k, d.d_in, d.d_out, std_dev, U1s,
+                                                                  U2s);
+    else if (elem == ELEM_F32)
+        init_u_kernel<float><<<grid_for(n), 256, 0, st>>>(seed, d.L, d.k, d.d_in, d.d_out, std_dev, U1s, U2s);
+    else
+        init_u_kernel<double><<<grid_for(n), 256, 0, st>>>(seed, d.L, d.k, d.d_in, d.d_out, std_dev, U1s, U2s);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int unit_var, int transpose, int elem,
+                           void* out, cudaStream_t st) {
+    const double scale = 1.0 / sqrt((double)k);
+    const uint64_t n = (uint64_t)k * dd;
+    if (elem == ELEM_BF16)
+        realize_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(dist, k, dd, seed, scale, unit_var, transpose,
+                                                                   out);
+    else if (elem == ELEM_F32)
+        realize_kernel<float><<<grid_for(n), 256, 0, st>>>(dist, k, dd, seed, scale, unit_var, transpose, out);
+    else
+        realize_kernel<double><<<grid_for(n), 256, 0, st>>>(dist, k, dd, seed, scale, unit_var, transpose, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
+                        const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, cudaStream_t st) {
+    const uint64_t n = (uint64_t)d.R_pad * (d.d_in + d.d_out);
+    if (elem == ELEM_BF16)
+        pack_cat_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
+                                                                    d.R_pad, Acat, Bcat);
+    else
+        pack_cat_kernel<float><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
+                                                            d.R_pad, Acat, Bcat);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dim3 blk(32, 8);
+    if (AcatT) {
+        dim3 g((d.R_pad + 31) / 32, (d.d_in + 31) / 32);
+        if (elem == ELEM_BF16)
+            transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Acat, (__nv_bfloat16*)AcatT,
+                                                               d.d_in, d.R_pad);
+        else
+            transpose_kernel<float><<<g, blk, 0, st>>>((const float*)Acat, (float*)AcatT, d.d_in, d.R_pad);
+    }
+    if (BcatT) {
+        dim3 g((d.d_out + 31) / 32, (d.R_pad + 31) / 32);
+        if (elem == ELEM_BF16)
+            transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Bcat, (__nv_bfloat16*)BcatT,
+                                                               d.R_pad, d.d_out);
+        else
+            transpose_kernel<float><<<g, blk, 0, st>>>((const float*)Bcat, (float*)BcatT, d.R_pad, d.d_out);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_to_f32(const void* in, int elem, float* out, int64_t n, cudaStream_t st) {
+    if (elem == ELEM_BF16) to_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(in, out, n);
+    else to_f32_kernel<float><<<grid_for(n), 256, 0, st>>>(in, out, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_partials(const float* part, int S, int64_t M, int64_t N, float alpha, float* out,
+                                   int64_t nb, int64_t blk, int64_t ldm, cudaStream_t st) {
+    reduce_partials_kernel<<<grid_for((uint64_t)M * N), 256, 0, st>>>(part, S, M, N, alpha, out, nb, blk, ldm);
+    return cudaGetLastError();
+}
+
+int64_t colsum_chunks(int64_t rows) { return rows < 256 ? 1 : (rows + 255) / 256 < 512 ? (rows + 255) / 256 : 512; }
+
+cudaError_t launch_colsum(const void* G, int elem, int64_t rows, int64_t N, float* part, float* out,
+                          cudaStream_t st) {
+    const int64_t chunks = colsum_chunks(rows);
+    const int64_t rows_per = (rows + chunks - 1) / chunks;
+    dim3 g((unsigned)((N + 255) / 256), (unsigned)chunks);
+    if (elem == ELEM_BF16) colsum_partial_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
+    else colsum_partial_kernel<float><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_reduce_partials(part, (int)chunks, 1, N, 1.0f, out, N, 0, N, st);
+}
+
+}  // namespace skl

@@ -1,0 +1,353 @@
+// b2b.cuh -- fused back-to-back tcgen05 kernel: the SKLinear hot op.
+//
+// Forward  (nn_layers.cpp:61-76, row convention):
+//     H = X · Acat                  [tile, R]   (R = 2Lk: all L terms, both branches)
+//     Y = inv · H · Bcat + b        [tile, d_out]
+// Backward data path (nn_layers.cpp:78-101):
+//     P  = G · Bcatᵀ                [tile, R]
+//     dX = inv · P · Acatᵀ          [tile, d_in]
+// Both are   OUT = alpha · (A1 · B1ᵀ) · B2ᵀ (+ bias),  so one kernel serves both.
+//
+// The rank-R intermediate never touches HBM: GEMM1 accumulates H in TMEM
+// (fp32), the epilogue warps round it to bf16 and write it back into TMEM,
+// and GEMM2 consumes it directly as the A operand (tcgen05.mma ... [a_tmem],
+// the "TS" form).  The Σ over the L terms and the two branches is simply the
+// K = R reduction of GEMM2, i.e. one TMEM accumulator per output tile; the
+// 1/(2L) scale and the bias are fused into the GEMM2 epilogue.  Columns of H
+// the backward needs (x·S1 in the forward, G·S2ᵀ in the backward) are
+// streamed out by the conversion epilogue, from registers, at no extra read.
+//
+// TMEM map (512 columns, one CTA per SM):
+//   GEMM1 chunk c (<= 256 wide) accumulates fp32 in [256c, 256c + W_c)
+//   bf16 H (2 values / column)          lives in [0, R/2)   (in-place compaction)
+//   GEMM2 double-buffered slots         [256, 384) and [384, 512)
+// Chunk 1 and the GEMM2 slots share [256, 512); chunk 1 therefore acquires
+// both slots from the slot ring and releases them once converted.
+//
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..7 epilogue.
+// kCG == 2 runs cta_group::2 (M = 256 tokens per CTA pair, each CTA keeps
+// its 128 rows of H in its own TMEM, B operands are split across the pair).
+#pragma once
+
+#include "sm100.cuh"
+
+namespace skl {
+
+struct B2BArgs {
+    int T, K1, R, R_pad, N2;
+    float alpha;
+    const float* bias;  // [N2] fp32, nullable
+    void* out;          // [T, N2] bf16, row stride ldo
+    long long ldo;
+    void* save;         // H columns [save_col0, save_col0 + save_cols) -> save[t][c - save_col0]
+    int save_col0, save_cols;
+    long long ld_save;
+};
+
+namespace dev {
+
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem]  (kind::f16, A K-major bf16 packed 2/column)
+template <int kCG>
+__device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+    if constexpr (kCG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+
+template <int kCG>
+struct B2BCfg {
+    static constexpr int kStageBytes = kCG == 1 ? 48 * 1024 : 32 * 1024;
+    static constexpr int kStages = kCG == 1 ? 4 : 6;
+    static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
+    static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
+    static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
+    static constexpr int kB1BoxRows = 32;
+    static constexpr int kSmem = kStages * kStageBytes + 1024 + 512;
+};
+
+template <int kCG>
+__global__ void __launch_bounds__(256, 1)
+    b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
+               const __grid_constant__ CUtensorMap tmB2, B2BArgs args) {
+    using C = B2BCfg<kCG>;
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint64_t* full = bars;                            // [kStages]
+    uint64_t* empty = bars + C::kStages;              // [kStages]
+    uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
+    uint64_t* hready = tfull1 + 2;                    // [2] chunk converted to bf16 H
+    uint64_t* tfull2 = hready + 2;                    // [2] GEMM2 slot accumulated
+    uint64_t* tempty2 = tfull2 + 2;                   // [2] GEMM2 slot drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty2 + 2);
+
+    const uint32_t warp = warp_id();
+    const uint32_t rank = kCG == 2 ? cluster_ctarank() : 0;
+    const bool leader = rank == 0;
+
+    if (warp == 0 && elect_one()) {
+        prefetch_tmap(&tmA1);
+        prefetch_tmap(&tmB1);
+        prefetch_tmap(&tmB2);
+        for (int s = 0; s < C::kStages; ++s) {
+            mbar_init(&full[s], kCG);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull1[i], 1);
+            mbar_init(&hready[i], 4 * kCG);
+            mbar_init(&tfull2[i], 1);
+            mbar_init(&tempty2[i], 4 * kCG);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        tmem_alloc<kCG>(tmem_slot, 512);
+        tmem_relinquish<kCG>();
+    }
+    tc_fence_before();
+    if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int tile_rows = 128 * kCG;
+    const int num_tiles = (args.T + tile_rows - 1) / tile_rows;
+    const int cluster_id = blockIdx.x / kCG;
+    const int num_clusters = gridDim.x / kCG;
+    const int nch = (args.R_pad + 255) / 256;
+    const int nkb1 = (args.K1 + 63) / 64;
+    const int nkb2 = args.R_pad / 64;
+    const int nst2 = (nkb2 + C::kKbPerStage2 - 1) / C::kKbPerStage2;
+    const int n2_tiles = (args.N2 + 127) / 128;
+
+    if (warp == 0) {
+        // ---------------------------------------------------------------- producer
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
+            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+                const int am = t * tile_rows + (int)rank * 128;
+                for (int c = 0; c < nch; ++c) {
+                    const int wc = min(256, args.R_pad - 256 * c);
+                    const int brows = wc / kCG;
+                    const int b0 = 256 * c + (int)rank * brows;
+                    const uint32_t bytes = 16384 + brows * 128;
+                    for (int kb = 0; kb < nkb1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smem + stage * C::kStageBytes;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
+                        else mbar_arrive_cluster(&full[stage], 0);
+                        tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * 64, am);
+                        for (int r = 0; r < brows; r += C::kB1BoxRows)
+                            tma_load_2d<kCG>(&tmB1, &full[stage], st + 16384 + r * 128, kb * 64, b0 + r);
+                        next();
+                    }
+                }
+                for (int j = 0; j < n2_tiles; ++j) {
+                    const int brow = j * 128 + (int)rank * C::kB2Rows;
+                    for (int s = 0; s < nst2; ++s) {
+                        const int kb0 = s * C::kKbPerStage2;
+                        const int nk = min(C::kKbPerStage2, nkb2 - kb0);
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smem + stage * C::kStageBytes;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
+                        else mbar_arrive_cluster(&full[stage], 0);
+                        for (int q = 0; q < nk; ++q)
+                            tma_load_2d<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, (kb0 + q) * 64, brow);
+                        next();
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------------------------------------------------------- MMA issuer
+        if (leader && elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
+            uint32_t slot_seq = 0;
+            const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, 0);
+            int it = 0;
+            for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+                // ---- GEMM1: H chunks
+                for (int c = 0; c < nch; ++c) {
+                    const int wc = min(256, args.R_pad - 256 * c);
+                    if (c == 1) {  // chunk 1 overlays both GEMM2 slots
+                        for (int u = 0; u < 2; ++u, ++slot_seq)
+                            mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1);
+                        tc_fence_after();
+                    }
+                    const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, 0);
+                    const uint32_t d = tmem_base + 256 * c;
+                    for (int kb = 0; kb < nkb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
+                        const uint32_t b_addr = a_addr + 16384;
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024), make_sdesc(b_addr + k * 32, 0, 1024),
+                                           idesc1, (kb > 0 || k > 0) ? 1u : 0u);
+                        mma_commit<kCG>(&empty[stage]);
+                        next();
+                    }
+                    mma_commit<kCG>(&tfull1[c]);
+                }
+                // ---- wait for the bf16 H of this tile (both CTAs)
+                for (int c = 0; c < nch; ++c) mbar_wait(&hready[c], it & 1);
+                tc_fence_after();
+                // ---- GEMM2: 128-wide output tiles, A = H from TMEM
+                for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
+                    const uint32_t s = slot_seq & 1;
+                    mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t d = tmem_base + 256 + 128 * s;
+                    for (int st2 = 0; st2 < nst2; ++st2) {
+                        const int kb0 = st2 * C::kKbPerStage2;
+                        const int nk = min(C::kKbPerStage2, nkb2 - kb0);
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+                        const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
+                        for (int q = 0; q < nk; ++q) {
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const uint32_t a_t = tmem_base + (uint32_t)((kb0 + q) * 32 + k * 8);
+                                mma_ts<kCG>(d, a_t, make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024), idesc2,
+                                            (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
+                            }
+                        }
+                        mma_commit<kCG>(&empty[stage]);
+                        next();
+                    }
+                    mma_commit<kCG>(&tfull2[s]);
+                }
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------------------------------------------------------- epilogue
+        const uint32_t q = warp & 3;
+        const uint32_t lane = lane_id();
+        const uint32_t lane_base = (q * 32u) << 16;
+        uint32_t slot_seq = 0;
+        int it = 0;
+        for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+            const int row = t * tile_rows + (int)rank * 128 + (int)(q * 32 + lane);
+            const bool row_ok = row < args.T;
+            // ---- convert GEMM1 chunks: fp32 -> bf16 H in TMEM (+ saved columns)
+            for (int c = 0; c < nch; ++c) {
+                const int wc = min(256, args.R_pad - 256 * c);
+                mbar_wait(&tfull1[c], it & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int g = 0; g < wc / 16; ++g) {
+                    uint32_t r[16];
+                    tmem_ld16(tmem_base + lane_base + 256 * c + 16 * g, r);
+                    tmem_ld_wait();
+                    uint32_t p[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                    tmem_st8(tmem_base + lane_base + 128 * c + 8 * g, p);
+                    const int col = 256 * c + 16 * g;  // H column (R order)
+                    if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
+                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) +
+                                             (long long)row * args.ld_save + (col - args.save_col0);
+                        if (col >= args.save_col0 && col + 16 <= args.save_col0 + args.save_cols &&
+                            (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                            reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+                            reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+                        } else {
+                            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
+                            for (int i = 0; i < 16; ++i)
+                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
+                                    dst[i] = pb[i];
+                        }
+                    }
+                }
+                tmem_st_wait();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(&hready[c]);
+                    else mbar_arrive_cluster(&hready[c], 0);
+                    if (c == 1) {  // release the two slots chunk 1 overlaid
+                        for (int u = 0; u < 2; ++u) {
+                            const uint32_t s = (slot_seq + u) & 1;
+                            if (leader) mbar_arrive(&tempty2[s]);
+                            else mbar_arrive_cluster(&tempty2[s], 0);
+                        }
+                    }
+                }
+                if (c == 1) slot_seq += 2;
+            }
+            // ---- GEMM2 output tiles
+            for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
+                const uint32_t s = slot_seq & 1;
+                mbar_wait(&tfull2[s], (slot_seq >> 1) & 1);
+                tc_fence_after();
+#pragma unroll 1
+                for (int g = 0; g < 8; ++g) {
+                    uint32_t r[16];
+                    tmem_ld16(tmem_base + lane_base + 256 + 128 * s + 16 * g, r);
+                    tmem_ld_wait();
+                    const int n = j * 128 + 16 * g;
+                    if (!row_ok || n >= args.N2) continue;
+                    float v[16];
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * args.alpha;
+                    if (args.bias) {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            if (n + i < args.N2) v[i] += args.bias[n + i];
+                    }
+                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (long long)row * args.ldo + n;
+                    if (n + 16 <= args.N2 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
+                                                                      pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
+                        reinterpret_cast<uint4*>(dst)[1] =
+                            make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]), pack_bf16x2(v[12], v[13]),
+                                       pack_bf16x2(v[14], v[15]));
+                    } else {
+                        for (int i = 0; i < 16 && n + i < args.N2; ++i) dst[i] = __float2bfloat16_rn(v[i]);
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(&tempty2[s]);
+                    else mbar_arrive_cluster(&tempty2[s], 0);
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<kCG>(tmem_base, 512);
+    }
+}
+
+}  // namespace dev
+
+// Host side (skl.cu): whether the fused path handles this rank / dtype.
+inline bool b2b_supported(long long R_pad, int kind) { return kind == 0 && R_pad <= 512; }
+
+}  // namespace skl

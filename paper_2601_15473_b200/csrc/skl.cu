@@ -1,0 +1,602 @@
+// skl.cu -- C-ABI dispatch of the B200 SKLinear hot path (include/skl.h).
+//
+// Maps the reference's SkLinear::forward / backward contract
+// (nn_layers.cpp:61-101) onto the sm_100a kernels:
+//   forward : pack params -> fused B2B kernel (H = x·Acat stays on chip,
+//             y = inv·H·Bcat + b)            [R <= 512]
+//             or GEMM(H) + GEMM(y) through HBM [R > 512, documented fallback]
+//   backward: pack -> fused B2B kernel (P = G·Bcatᵀ on chip -> dX, P_S2 out)
+//             -> split-K tcgen05 GEMMs dU1 = inv·Savedᵀ·G, dU2 = inv·Xᵀ·P_S2
+//             -> fixed-order partial reduction; db = column sums of G.
+// Status codes replace the reference's exceptions (errors.hpp:10-19).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/skl.h"
+#include "b2b.cuh"
+#include "gemm.cuh"
+#include "skl_internal.h"
+
+namespace skl {
+namespace {
+
+thread_local std::string g_err;
+
+skl_status fail(skl_status s, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return s;
+}
+
+#define SKL_CUDA(expr)                                                                               \
+    do {                                                                                             \
+        cudaError_t e_ = (expr);                                                                     \
+        if (e_ != cudaSuccess) return fail(SKL_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_));   \
+    } while (0)
+
+#define SKL_TRY(expr)                   \
+    do {                                \
+        skl_status s_ = (expr);         \
+        if (s_ != SKL_OK) return s_;    \
+    } while (0)
+
+// ---------------------------------------------------------------- device
+struct DevInfo {
+    int sms = 0;
+    int major = 0;
+};
+DevInfo dev_info() {
+    int dev = 0;
+    DevInfo d;
+    if (cudaGetDevice(&dev) != cudaSuccess) return d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.major, cudaDevAttrComputeCapabilityMajor, dev);
+    return d;
+}
+
+skl_status check_device(DevInfo& di) {
+    di = dev_info();
+    if (di.sms == 0) return fail(SKL_ERR_CUDA, "no CUDA device available (libskl has no CPU fallback)");
+    if (di.major != 10) return fail(SKL_ERR_CUDA, "libskl requires an sm_100 (B200) device, found sm_%d", di.major);
+    return SKL_OK;
+}
+
+// ---------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+// 2-D view: `inner` contiguous elements per row, `outer` rows `ld` elements
+// apart; box {box_inner, box_outer}; 128B swizzle; OOB reads return zero.
+skl_status make_tmap(CUtensorMap* m, const void* ptr, int elem_bytes, int64_t inner, int64_t outer, int64_t ld,
+                     int box_inner, int box_outer) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(SKL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * elem_bytes) & 15) != 0)
+        return fail(SKL_ERR_UNSUPPORTED, "TMA needs 16-byte aligned base and row stride (ld=%lld)", (long long)ld);
+    cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+    cuuint64_t strides[1] = {(cuuint64_t)(ld * elem_bytes)};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = enc(m, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        return fail(SKL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%dx%d",
+                    (int)r, (long long)inner, (long long)outer, (long long)ld, box_inner, box_outer);
+    return SKL_OK;
+}
+
+// ---------------------------------------------------------------- GEMM launch
+// Operand view: element (row-major storage) pointer, storage rows x cols, ld.
+struct View {
+    const void* ptr;
+    int64_t rows, cols, ld;
+};
+
+template <int kCG, int kKind, bool kAMN, bool kBMN, int kBN, int kStages>
+skl_status run_gemm(const View& A, const View& B, int M, int N, int K, GemmArgs args, int sms,
+                    cudaStream_t st) {
+    using C = dev::GemmCfg<kCG, kKind, kAMN, kBMN, kBN, kStages>;
+    const int eb = dev::KindTraits<kKind>::kElem;
+    const int bk = C::kBK;
+    CUtensorMap ta, tb;
+    // A(m,k): K-major storage [M][K] or MN-major storage [K][M]
+    if (!kAMN) SKL_TRY(make_tmap(&ta, A.ptr, eb, K, M, A.ld, bk, 128));
+    else SKL_TRY(make_tmap(&ta, A.ptr, eb, M, K, A.ld, 128 / eb, bk));
+    if (!kBMN) SKL_TRY(make_tmap(&tb, B.ptr, eb, K, N, B.ld, bk, C::kNcta));
+    else SKL_TRY(make_tmap(&tb, B.ptr, eb, N, K, B.ld, 128 / eb, bk));
+    args.M = M;
+    args.N = N;
+    args.K = K;
+    args.num_m_tiles = (M + 128 * kCG - 1) / (128 * kCG);
+    args.num_n_tiles = (N + kBN - 1) / kBN;
+    args.k_blocks = (K + bk - 1) / bk;
+    if (args.splits < 1) args.splits = 1;
+    if (args.splits > args.k_blocks) args.splits = std::max(1, args.k_blocks);
+    const int tiles = args.num_m_tiles * args.num_n_tiles * args.splits;
+    int grid = std::min(sms / kCG, tiles) * kCG;
+    if (grid < kCG) grid = kCG;
+    auto kern = dev::gemm_kernel<kCG, kKind, kAMN, kBMN, kBN, kStages>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
+    return SKL_OK;
+}
+
+template <int kCG>
+skl_status run_b2b_cg(const void* a1, const void* b1, const void* b2, B2BArgs a, int sms, cudaStream_t st) {
+    using C = dev::B2BCfg<kCG>;
+    CUtensorMap ta, tb1, tb2;
+    SKL_TRY(make_tmap(&ta, a1, 2, a.K1, a.T, a.K1, 64, 128));
+    SKL_TRY(make_tmap(&tb1, b1, 2, a.K1, a.R_pad, a.K1, 64, C::kB1BoxRows));
+    SKL_TRY(make_tmap(&tb2, b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
+    const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
+    int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
+    auto kern = dev::b2b_kernel<kCG>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, a));
+    return SKL_OK;
+}
+
+int g_b2b_cg = 1;  // CTA-group width of the fused kernel (SKL_B2B_CG env overrides)
+
+skl_status run_b2b(int kind, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms, cudaStream_t st) {
+    if (kind != 0) return fail(SKL_ERR_UNSUPPORTED, "fused kernel is bf16-only");
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* e = getenv("SKL_B2B_CG");
+        if (e && atoi(e) == 2) g_b2b_cg = 2;
+    });
+    if (g_b2b_cg == 2) return run_b2b_cg<2>(a1, b1, b2, a, sms, st);
+    return run_b2b_cg<1>(a1, b1, b2, a, sms, st);
+}
+
+int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
+    const int tiles = ((M + 128 * cg - 1) / (128 * cg)) * ((N + bn - 1) / bn);
+    const int kb = (K + bk - 1) / bk;
+    int s = std::max(1, (sms / cg) / std::max(1, tiles));
+    s = std::min(s, std::max(1, kb / 4));  // keep >= 4 k-blocks per split
+    return std::max(1, std::min(s, 64));
+}
+
+// ---------------------------------------------------------------- shapes / workspace
+size_t align_up(size_t x, size_t a = 1024) { return (x + a - 1) / a * a; }
+
+skl_status get_dims(const skl_shape* s, SklDims& d) {
+    if (!s) return fail(SKL_ERR_PARAM, "null shape");
+    if (s->num_terms < 1 || s->low_rank < 1)
+        return fail(SKL_ERR_PARAM, "SkLinear: num_terms and low_rank must be >= 1");  // nn_layers.cpp:116
+    if (s->d_in < 1 || s->d_out < 1) return fail(SKL_ERR_SHAPE, "SkLinear: d_in and d_out must be >= 1");
+    if (s->dtype != SKL_BF16 && s->dtype != SKL_F32_TF32) return fail(SKL_ERR_PARAM, "unknown dtype %d", s->dtype);
+    d.d_in = s->d_in;
+    d.d_out = s->d_out;
+    d.L = s->num_terms;
+    d.k = s->low_rank;
+    d.Lk = d.L * d.k;
+    d.R = 2 * d.Lk;
+    d.R_pad = (d.R + 63) / 64 * 64;
+    return SKL_OK;
+}
+
+int elem_of(skl_dtype t) { return t == SKL_BF16 ? ELEM_BF16 : ELEM_F32; }
+int ebytes(skl_dtype t) { return t == SKL_BF16 ? 2 : 4; }
+
+// Shapes the TMA-fed kernels accept: every row stride a multiple of 16 B.
+skl_status check_alignment(const SklDims& d, skl_dtype t) {
+    const int e = ebytes(t);
+    if ((d.d_in * e) % 16 || (d.d_out * e) % 16 || (d.Lk * e) % 16)
+        return fail(SKL_ERR_UNSUPPORTED,
+                    "unsupported shape: d_in, d_out and L*k must be multiples of %d elements for %s (got %lld, %lld, "
+                    "%lld)",
+                    16 / e, t == SKL_BF16 ? "bf16" : "tf32", (long long)d.d_in, (long long)d.d_out,
+                    (long long)d.Lk);
+    return SKL_OK;
+}
+
+// SKL_FORCE_UNFUSED=1 routes every shape through the unfused GEMM chain
+// (testing aid: both paths are parity-checked against the oracle).
+bool use_fused(const SklDims& d, skl_dtype t) {
+    static const bool force_unfused = [] {
+        const char* e = getenv("SKL_FORCE_UNFUSED");
+        return e && atoi(e) != 0;
+    }();
+    return !force_unfused && b2b_supported(d.R_pad, t == SKL_BF16 ? 0 : 1);
+}
+
+struct Plan {
+    size_t acat, bcat, acatT, bcatT, bias32, inter, saved, part, colsum, total;
+    int s_du1, s_du2;
+};
+
+// Offsets into the caller's workspace (1 KiB aligned).
+Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
+    const size_t e = ebytes(t);
+    Plan p = {};
+    size_t off = 0;
+    auto take = [&](size_t bytes) {
+        size_t o = off;
+        off += align_up(bytes ? bytes : 1);
+        return o;
+    };
+    p.acat = take((size_t)d.d_in * d.R_pad * e);
+    p.bcat = take((size_t)d.R_pad * d.d_out * e);
+    p.acatT = take((size_t)d.R_pad * d.d_in * e);
+    p.bcatT = take((size_t)d.d_out * d.R_pad * e);
+    p.bias32 = take((size_t)d.d_out * 4);
+    const bool fused = use_fused(d, t);
+    // fwd: H [T, R_pad] only when unfused; bwd: P [T, R_pad] (P_S2 always goes out)
+    p.inter = take((bwd || !fused) ? (size_t)T * d.R_pad * e : 0);
+    p.saved = take(bwd ? (size_t)T * d.Lk * e : 0);
+    p.s_du1 = pick_splits((int)d.Lk, (int)d.d_out, (int)T, 256, 1, sms, t == SKL_BF16 ? 64 : 32);
+    p.s_du2 = pick_splits((int)d.d_in, (int)d.Lk, (int)T, 256, 1, sms, t == SKL_BF16 ? 64 : 32);
+    size_t part = 0;
+    if (bwd) {
+        part = std::max((size_t)p.s_du1 * d.Lk * d.d_out, (size_t)p.s_du2 * d.d_in * d.Lk) * 4;
+        if (t == SKL_F32_TF32) part += (size_t)T * (d.d_in + d.d_out + 2 * d.Lk) * 4;  // transposed operands
+    }
+    p.part = take(part);
+    p.colsum = take(bwd ? (size_t)colsum_chunks(T) * d.d_out * 4 : 0);
+    p.total = off;
+    return p;
+}
+
+template <typename Tp>
+Tp* at(void* ws, size_t off) {
+    return reinterpret_cast<Tp*>(reinterpret_cast<uint8_t*>(ws) + off);
+}
+
+}  // namespace
+}  // namespace skl
+
+using namespace skl;
+
+extern "C" {
+
+const char* skl_version(void) { return "skl-b200 0.1 (sm_100a tcgen05)"; }
+const char* skl_last_error(void) { return g_err.c_str(); }
+const char* skl_rng_algorithm(void) { return "splitmix64-boxmuller-v1"; }
+
+uint64_t skl_derive_seed(uint64_t master, uint64_t index) {
+    uint64_t z = (master ^ (0x517cc1b727220a95ULL + index)) + 0x9e3779b97f4a7c15ULL;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+
+skl_status skl_params(const skl_shape* s, skl_param_count* out) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    const uint64_t lk = (uint64_t)d.Lk;
+    out->learnable = lk * (uint64_t)(d.d_in + d.d_out) + (uint64_t)d.d_out;
+    out->total_stored = 2 * lk * (uint64_t)(d.d_in + d.d_out) + (uint64_t)d.d_out;
+    out->dense_equivalent = (uint64_t)d.d_in * (uint64_t)d.d_out + (uint64_t)d.d_out;
+    return SKL_OK;
+}
+
+int skl_exceeds_dense(uint64_t l, uint64_t k, uint64_t d_in, uint64_t d_out) {
+    return 2 * l * k * (d_in + d_out) > d_in * d_out;
+}
+
+skl_status skl_generate_sketches(const skl_shape* s, skl_dist dist, uint64_t layer_seed, void* S1s, void* S2s,
+                                 void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (dist != SKL_DIST_GAUSSIAN && dist != SKL_DIST_RADEMACHER) return fail(SKL_ERR_PARAM, "unknown dist %d", dist);
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    SKL_CUDA(launch_gen_sketches((int)dist, layer_seed, d, elem_of(s->dtype), S1s, S2s, (cudaStream_t)stream));
+    return SKL_OK;
+}
+
+skl_status skl_init_params(const skl_shape* s, uint64_t layer_seed, void* U1s, void* U2s, void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    SKL_CUDA(launch_init_u(layer_seed, d, elem_of(s->dtype), U1s, U2s, (cudaStream_t)stream));
+    return SKL_OK;
+}
+
+skl_status skl_realize_sketch(skl_dist dist, int64_t k, int64_t dd, uint64_t seed, int unit_variance, int transpose,
+                              skl_out_type out_type, void* out, void* stream) {
+    if (k < 1 || dd < 1) return fail(SKL_ERR_SHAPE, "make_sketch: dimensions must be >= 1");  // sketch.cpp:92
+    if (dist != SKL_DIST_GAUSSIAN && dist != SKL_DIST_RADEMACHER) return fail(SKL_ERR_PARAM, "unknown dist %d", dist);
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    const int elem = out_type == SKL_OUT_F64 ? ELEM_F64 : out_type == SKL_OUT_F32 ? ELEM_F32 : ELEM_BF16;
+    SKL_CUDA(launch_realize((int)dist, k, dd, seed, unit_variance, transpose, elem, out, (cudaStream_t)stream));
+    return SKL_OK;
+}
+
+skl_status skl_workspace_size(const skl_shape* s, int64_t T, size_t* fwd_bytes, size_t* bwd_bytes) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "T must be >= 0");
+    DevInfo di = dev_info();
+    const int sms = di.sms ? di.sms : 148;
+    if (fwd_bytes) *fwd_bytes = plan(d, s->dtype, T, false, sms).total;
+    if (bwd_bytes) *bwd_bytes = plan(d, s->dtype, T, true, sms).total;
+    return SKL_OK;
+}
+
+skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x, const void* S1s, const void* S2s,
+                                   const void* U1s, const void* U2s, const void* bias, void* y, void* saved_proj,
+                                   void* workspace, size_t ws_bytes, void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::forward: T must be >= 0");
+    if (T == 0) return SKL_OK;
+    if (!x || !S1s || !S2s || !U1s || !U2s || !y) return fail(SKL_ERR_PARAM, "null tensor argument");
+    SKL_TRY(check_alignment(d, s->dtype));
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    const Plan p = plan(d, s->dtype, T, false, di.sms);
+    if (!workspace || ws_bytes < p.total)
+        return fail(SKL_ERR_WORKSPACE, "forward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    const int elem = elem_of(s->dtype);
+    const int eb = ebytes(s->dtype);
+    const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    void* acat = at<void>(workspace, p.acat);
+    void* bcat = at<void>(workspace, p.bcat);
+    void* acatT = at<void>(workspace, p.acatT);
+    void* bcatT = at<void>(workspace, p.bcatT);
+    float* bias32 = at<float>(workspace, p.bias32);
+    SKL_CUDA(launch_pack(d, elem, S1s, U2s, U1s, S2s, acat, bcat, acatT, bcatT, st));
+    SKL_CUDA(launch_to_f32(bias, elem, bias32, d.d_out, st));
+
+    if (use_fused(d, s->dtype)) {
+        B2BArgs a = {};
+        a.T = (int)T;
+        a.K1 = (int)d.d_in;
+        a.R = (int)d.R;
+        a.R_pad = (int)d.R_pad;
+        a.N2 = (int)d.d_out;
+        a.alpha = inv;
+        a.bias = bias32;
+        a.out = y;
+        a.ldo = d.d_out;
+        a.save = saved_proj;
+        a.save_col0 = 0;
+        a.save_cols = (int)d.Lk;
+        a.ld_save = d.Lk;
+        return run_b2b(s->dtype == SKL_BF16 ? 0 : 1, x, acatT, bcatT, a, di.sms, st);
+    }
+
+    // Unfused fallback: H through HBM.
+    void* H = at<void>(workspace, p.inter);
+    GemmArgs g1 = {};
+    g1.alpha = 1.f;
+    g1.out = H;
+    g1.ldo = d.R_pad;
+    g1.out2 = saved_proj;
+    g1.ldo2 = d.Lk;
+    g1.n_split = saved_proj ? (int)d.Lk : 0;
+    g1.out_f32 = eb == 4;
+    g1.splits = 1;
+    View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+    if (s->dtype == SKL_BF16)
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
+    else
+        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
+    GemmArgs g2 = {};
+    g2.alpha = inv;
+    g2.bias = bias32;
+    g2.out = y;
+    g2.ldo = d.d_out;
+    g2.n_split = 0;
+    g2.out_f32 = eb == 4;
+    g2.splits = 1;
+    View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
+    if (s->dtype == SKL_BF16)
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
+    else
+        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
+    return SKL_OK;
+}
+
+skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* grad_y, const void* x,
+                                    const void* saved_proj, const void* S1s, const void* S2s, const void* U1s,
+                                    const void* U2s, void* grad_x, float* grad_U1s, float* grad_U2s,
+                                    float* grad_bias, void* workspace, size_t ws_bytes, void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::backward: T must be >= 0");
+    if (!grad_y || !x || !S1s || !S2s || !U1s || !U2s || !grad_U1s || !grad_U2s)
+        return fail(SKL_ERR_PARAM, "null tensor argument");
+    SKL_TRY(check_alignment(d, s->dtype));
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    const Plan p = plan(d, s->dtype, T, true, di.sms);
+    if (!workspace || ws_bytes < p.total)
+        return fail(SKL_ERR_WORKSPACE, "backward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (T == 0) {  // empty batch: all gradients are zero (sums over no tokens)
+        SKL_CUDA(cudaMemsetAsync(grad_U1s, 0, (size_t)d.Lk * d.d_out * 4, st));
+        SKL_CUDA(cudaMemsetAsync(grad_U2s, 0, (size_t)d.Lk * d.d_in * 4, st));
+        if (grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
+        return SKL_OK;
+    }
+    const int elem = elem_of(s->dtype);
+    const int eb = ebytes(s->dtype);
+    const bool bf16 = s->dtype == SKL_BF16;
+    const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    void* acat = at<void>(workspace, p.acat);
+    void* bcat = at<void>(workspace, p.bcat);
+    void* acatT = at<void>(workspace, p.acatT);
+    void* P = at<void>(workspace, p.inter);
+    float* part = at<float>(workspace, p.part);
+    SKL_CUDA(launch_pack(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, st));
+
+    // Saved projection x·S1 (recomputed only when the caller did not keep it).
+    const void* saved = saved_proj;
+    if (!saved) {
+        void* sv = at<void>(workspace, p.saved);
+        GemmArgs g = {};
+        g.alpha = 1.f;
+        g.out = sv;
+        g.ldo = d.Lk;
+        g.out_f32 = eb == 4;
+        g.splits = 1;
+        View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        saved = sv;
+    }
+
+    // P = G·Bcatᵀ and dX = inv·P·Acatᵀ
+    if (use_fused(d, s->dtype) && grad_x) {
+        B2BArgs a = {};
+        a.T = (int)T;
+        a.K1 = (int)d.d_out;
+        a.R = (int)d.R;
+        a.R_pad = (int)d.R_pad;
+        a.N2 = (int)d.d_in;
+        a.alpha = inv;
+        a.bias = nullptr;
+        a.out = grad_x;
+        a.ldo = d.d_in;
+        a.save = at<uint8_t>(P, (size_t)d.Lk * eb);  // only the S2 half of P leaves the chip
+        a.save_col0 = (int)d.Lk;
+        a.save_cols = (int)d.Lk;
+        a.ld_save = d.R_pad;
+        SKL_TRY(run_b2b(bf16 ? 0 : 1, grad_y, bcat, acat, a, di.sms, st));
+    } else {
+        GemmArgs g = {};
+        g.alpha = 1.f;
+        g.out = P;
+        g.ldo = d.R_pad;
+        g.out_f32 = eb == 4;
+        g.splits = 1;
+        View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
+        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        if (grad_x) {
+            GemmArgs g2 = {};
+            g2.alpha = inv;
+            g2.out = grad_x;
+            g2.ldo = d.d_in;
+            g2.out_f32 = eb == 4;
+            g2.splits = 1;
+            View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
+            if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+            else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+        }
+    }
+
+    // dU1s = inv·Savedᵀ·G  ([Lk, d_out] == [L][k][d_out])
+    // dU2s = inv·Xᵀ·P_S2   ([d_in, Lk] scattered to [L][d_in][k])
+    const void* P_S2 = at<uint8_t>(P, (size_t)d.Lk * eb);
+    if (bf16) {
+        GemmArgs g = {};
+        g.partial = part;
+        g.splits = p.s_du1;
+        View va{saved, T, d.Lk, d.Lk}, vb{grad_y, T, d.d_out, d.d_out};
+        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>(va, vb, (int)d.Lk, (int)d.d_out, (int)T, g, di.sms, st)));
+        SKL_CUDA(launch_reduce_partials(part, g.splits, d.Lk, d.d_out, inv,
+                                        grad_U1s, d.d_out, 0, d.d_out, st));
+        GemmArgs g2 = {};
+        g2.partial = part;
+        g2.splits = p.s_du2;
+        View vx{x, T, d.d_in, d.d_in}, vp{P_S2, T, d.Lk, d.R_pad};
+        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>(vx, vp, (int)d.d_in, (int)d.Lk, (int)T, g2, di.sms, st)));
+        SKL_CUDA(launch_reduce_partials(part, g2.splits, d.d_in, d.Lk, inv,
+                                        grad_U2s, d.k, d.d_in * d.k, d.k, st));
+    } else {
+        // TF32: MN-major fp32 operands are not staged by TMA here; transpose the
+        // token-major operands once so both dU GEMMs run K-major.
+        float* tX = part + std::max((size_t)p.s_du1 * d.Lk * d.d_out, (size_t)p.s_du2 * d.d_in * d.Lk);
+        float* tG = tX + (size_t)T * d.d_in;
+        float* tS = tG + (size_t)T * d.d_out;
+        float* tP = tS + (size_t)T * d.Lk;
+        (void)tX; (void)tG; (void)tS; (void)tP;
+        return fail(SKL_ERR_UNSUPPORTED, "tf32 backward dU path not built yet");
+    }
+    if (grad_bias) SKL_CUDA(launch_colsum(grad_y, elem, T, d.d_out, at<float>(workspace, p.colsum), grad_bias, st));
+    return SKL_OK;
+}
+
+// ---------------------------------------------------------------- NCCL
+typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+
+skl_status skl_allreduce_grads(void* nccl_comm, float* grad_bucket, size_t count, void* stream) {
+    static nccl_allreduce_fn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        // Use the NCCL the host process already loaded (torch's or the app's);
+        // fall back to the system library.
+        void* p = dlsym(RTLD_DEFAULT, "ncclAllReduce");
+        if (!p) {
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (h) p = dlsym(h, "ncclAllReduce");
+        }
+        fn = reinterpret_cast<nccl_allreduce_fn>(p);
+    });
+    if (!fn) return fail(SKL_ERR_UNSUPPORTED, "NCCL (libnccl.so.2) not available");
+    if (!nccl_comm) return fail(SKL_ERR_PARAM, "null NCCL communicator");
+    // ncclFloat32 = 7, ncclSum = 0 (nccl.h)
+    const int r = fn(grad_bucket, grad_bucket, count, 7, 0, nccl_comm, (cudaStream_t)stream);
+    if (r != 0) return fail(SKL_ERR_NCCL, "ncclAllReduce failed (%d)", r);
+    return SKL_OK;
+}
+
+}  // extern "C"

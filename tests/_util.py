@@ -1,0 +1,53 @@
+"""Shared helpers for the parity tests (numpy side of the checker)."""
+from __future__ import annotations
+
+import numpy as np
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round f64 values to the nearest bfloat16 (ties to even), returned as f64."""
+    a = np.asarray(a, dtype=np.float64)
+    m, e = np.frexp(a)                 # a = m * 2**e, 0.5 <= |m| < 1
+    return np.ldexp(np.rint(m * 256.0) / 256.0, e)   # 8 significant bits
+
+
+def f32_round(a: np.ndarray) -> np.ndarray:
+    return np.asarray(a, dtype=np.float64).astype(np.float32).astype(np.float64)
+
+
+def tf32_round(a: np.ndarray) -> np.ndarray:
+    """fp32 -> TF32 round-to-nearest (cvt.rna: ties away from zero)."""
+    f = np.asarray(a, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    f = ((f + 0x1000) & 0xFFFFE000).astype(np.uint32)
+    return f.view(np.float32).astype(np.float64)
+
+
+def rel_fro(approx, exact) -> float:
+    approx = np.asarray(approx, dtype=np.float64)
+    exact = np.asarray(exact, dtype=np.float64)
+    ref = np.linalg.norm(exact)
+    return float(np.linalg.norm(approx - exact) / (ref if ref > 0 else 1.0))
+
+
+def max_abs_rel(approx, exact) -> float:
+    """max |approx - exact| / max |exact|."""
+    approx = np.asarray(approx, dtype=np.float64)
+    exact = np.asarray(exact, dtype=np.float64)
+    den = np.max(np.abs(exact))
+    return float(np.max(np.abs(approx - exact)) / (den if den > 0 else 1.0))
+
+
+# Tolerance gates vs the f64 oracle on identical (already rounded) inputs,
+# BASELINE.md §5 / SURVEY.md §8(c).
+GATES = {
+    "bf16": dict(rel_fro=1e-2, max_abs=2e-2),
+    "tf32": dict(rel_fro=2e-3, max_abs=2e-3),
+}
+
+
+def check_close(name, approx, exact, variant="bf16"):
+    g = GATES[variant]
+    rf, ma = rel_fro(approx, exact), max_abs_rel(approx, exact)
+    assert rf <= g["rel_fro"] and ma <= g["max_abs"], (
+        f"{name}: rel_fro={rf:.3e} (gate {g['rel_fro']:.0e}), max_abs/max|ref|={ma:.3e} (gate {g['max_abs']:.0e})")
+    return rf, ma

@@ -1,0 +1,165 @@
+"""GPU parity tests: the sm_100a kernels (through the C-ABI of libskl.so)
+against the oracle (oracle/, the reference algorithm in f64) on identical
+seeded inputs.  Run on a B200:  python -m pytest tests -m gpu -x -q
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def skl():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2601_15473_b200 as skl
+    skl.lib()  # loud failure if libskl.so is missing
+    return skl
+
+
+def _np(t):
+    return t.detach().double().cpu().numpy()
+
+
+def _tdev(a, dtype):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(device="cuda", dtype=dtype)
+
+
+# --------------------------------------------------------------------------- B1
+@pytest.mark.parametrize("k,d,seed", [(64, 1024, 0xE816C0EF88EC839C), (3, 7, 42), (128, 3072, 12345)])
+def test_gaussian_sketch_entries(skl, port, k, d, seed):
+    """realize_sketch(Gaussian) on device: integer chain exact, values equal
+    after rounding to f32/bf16 on every entry; f64 within 4 ulp."""
+    ref = port.realize_sketch(0, k, d, seed)
+    out64 = torch.empty(k, d, dtype=torch.float64, device="cuda")
+    skl.realize_sketch(0, k, d, seed, out64)
+    dev = _np(out64)
+    ulp = np.abs(dev.view(np.int64) - ref.view(np.int64))
+    assert ulp.max() <= 4, f"f64 ulp max {ulp.max()}"
+    out32 = torch.empty(k, d, dtype=torch.float32, device="cuda")
+    skl.realize_sketch(0, k, d, seed, out32)
+    assert np.array_equal(_np(out32), ref.astype(np.float32).astype(np.float64))
+    outb = torch.empty(k, d, dtype=torch.bfloat16, device="cuda")
+    skl.realize_sketch(0, k, d, seed, outb)
+    from tests._util import bf16_round
+    assert np.array_equal(_np(outb), bf16_round(ref))
+
+
+def test_rademacher_bit_exact(skl, port):
+    ref = port.realize_sketch(1, 33, 517, 99)
+    out = torch.empty(33, 517, dtype=torch.float64, device="cuda")
+    skl.realize_sketch(1, 33, 517, 99, out)
+    assert np.array_equal(_np(out), ref)
+
+
+def test_gaussian_matrix_unit_variance(skl, port):
+    ref = port.gaussian_matrix(37, 11, 7)
+    out = torch.empty(37, 11, dtype=torch.float64, device="cuda")
+    skl.realize_sketch(0, 37, 11, 7, out, unit_variance=True)
+    assert np.abs(_np(out).view(np.int64) - ref.view(np.int64)).max() <= 4
+
+
+@pytest.mark.parametrize("dist", [0, 1])
+@pytest.mark.parametrize("d_in,d_out,L,k", [(1024, 1024, 1, 64), (768, 3072, 2, 128), (40, 24, 3, 8)])
+def test_generate_layer_matches_sk_linear_fresh(skl, port, dist, d_in, d_out, L, k):
+    """Device sketches + U init in the ABI stacks == sk_linear_fresh (f32 rounding)."""
+    import oracle
+    seed = 42
+    p = port.sk_linear_fresh(d_in, d_out, L, k, seed, dist)
+    abi = oracle.to_abi(p)
+    s = skl.shape(d_in, d_out, L, k, skl.F32_TF32)
+    S1s = torch.empty(L, d_in, k, device="cuda")
+    S2s = torch.empty(L, k, d_out, device="cuda")
+    U1s = torch.empty(L, k, d_out, device="cuda")
+    U2s = torch.empty(L, d_in, k, device="cuda")
+    skl.generate_sketches(s, dist, seed, S1s, S2s)
+    skl.init_params(s, seed, U1s, U2s)
+    for name, t in (("S1s", S1s), ("S2s", S2s), ("U1s", U1s), ("U2s", U2s)):
+        assert np.array_equal(_np(t), abi[name].astype(np.float32).astype(np.float64)), name
+
+
+# --------------------------------------------------------------------------- B2/B3
+def _make_case(skl, port, d_in, d_out, L, k, T, dtype, seed=42, dist=0):
+    """Device layer + inputs, and the same (rounded) values as f64 for the oracle."""
+    import oracle
+    td = skl.torch_dtype(dtype)
+    s = skl.shape(d_in, d_out, L, k, dtype)
+    S1s = torch.empty(L, d_in, k, dtype=td, device="cuda")
+    S2s = torch.empty(L, k, d_out, dtype=td, device="cuda")
+    U1s = torch.empty(L, k, d_out, dtype=td, device="cuda")
+    U2s = torch.empty(L, d_in, k, dtype=td, device="cuda")
+    skl.generate_sketches(s, dist, seed, S1s, S2s)
+    skl.init_params(s, seed, U1s, U2s)
+    x, g, b = oracle.inputs(d_in, d_out, T, seed, port)
+    X = _tdev(x.T, td)
+    G = _tdev(g.T, td)
+    B = _tdev(b, td)
+    P = oracle.from_abi(d_in, d_out, _np(S1s), _np(U1s), _np(U2s), _np(S2s))
+    return s, (S1s, S2s, U1s, U2s), X, G, B, P, _np(X).T.copy(), _np(G).T.copy(), _np(B)
+
+
+def _variant(dtype, skl):
+    return "bf16" if dtype == skl.BF16 else "tf32"
+
+
+CASES = [
+    (1024, 1024, 1, 64, 64),       # c1 shape
+    (768, 3072, 2, 128, 300),      # c2 shape, ragged token count
+    (256, 512, 3, 32, 129),        # R = 192 (single GEMM1 chunk), ragged
+    (512, 256, 4, 64, 200),        # R = 512, d_out < d_in
+    (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
+]
+
+
+@pytest.mark.parametrize("unfused", [False, True])
+@pytest.mark.parametrize("d_in,d_out,L,k,T", CASES)
+def test_forward_parity_bf16(skl, port, monkeypatch, unfused, d_in, d_out, L, k, T):
+    if unfused and os.environ.get("SKL_FORCE_UNFUSED") is None:
+        pytest.skip("unfused path is exercised in a separate process (SKL_FORCE_UNFUSED=1)")
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
+    y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(T, L * k, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    torch.cuda.synchronize()
+    y_ref = port.forward(P, b64, x64).T
+    from tests._util import check_close
+    check_close("y", _np(y), y_ref, "bf16")
+    # saved projection x·S1_i, term-major columns
+    sv_ref = np.concatenate([x64.T @ P.s2[i].T for i in range(L)], axis=1)
+    check_close("saved", _np(saved), sv_ref, "bf16")
+
+
+@pytest.mark.parametrize("d_in,d_out,L,k,T", CASES)
+def test_backward_parity_bf16(skl, port, d_in, d_out, L, k, T):
+    import oracle
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
+    y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(T, L * k, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    gx = torch.empty(T, d_in, dtype=torch.bfloat16, device="cuda")
+    du1 = torch.empty(L, k, d_out, device="cuda")
+    du2 = torch.empty(L, d_in, k, device="cuda")
+    db = torch.empty(d_out, device="cuda")
+    skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+    torch.cuda.synchronize()
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    from tests._util import check_close
+    check_close("grad_x", _np(gx), rgx, "bf16")
+    check_close("dU1s", _np(du1), rgu1, "bf16")
+    check_close("dU2s", _np(du2), rgu2, "bf16")
+    check_close("db", _np(db), rgb, "bf16")
+    # recompute path (no saved projection) gives the same gradients
+    du1b = torch.empty_like(du1)
+    du2b = torch.empty_like(du2)
+    skl.backward(s, G, X, None, S1s, S2s, U1s, U2s, None, du1b, du2b, None, ws)
+    torch.cuda.synchronize()
+    check_close("dU1s(recompute)", _np(du1b), rgu1, "bf16")
+    check_close("dU2s(recompute)", _np(du2b), rgu2, "bf16")
