@@ -86,7 +86,7 @@ def lib() -> ctypes.CDLL:
     L.skl_realize_sketch.argtypes = [ctypes.c_int, i64, i64, u64, ctypes.c_int, ctypes.c_int, ctypes.c_int, vp, vp]
     L.skl_workspace_size.argtypes = [sp, i64, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     L.sketched_linear_forward.argtypes = [sp, i64] + [vp] * 9 + [sz, vp]
-    L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 13 + [sz, vp]
+    L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 12 + [sz, vp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
     for name in ABI_SYMBOLS:
         if name not in ("skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed",

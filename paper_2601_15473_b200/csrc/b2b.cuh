@@ -246,6 +246,7 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t lane = lane_id();
         const uint32_t lane_base = (q * 32u) << 16;
         uint32_t slot_seq = 0;
+        uint32_t tf_par0 = 0, tf_par1 = 0;
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             const int row = t * tile_rows + (int)rank * 128 + (int)(q * 32 + lane);
@@ -299,7 +300,10 @@ __global__ void __launch_bounds__(256, 1)
             // ---- GEMM2 output tiles
             for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                 const uint32_t s = slot_seq & 1;
-                mbar_wait(&tfull2[s], (slot_seq >> 1) & 1);
+                // tfull2[s] completes once per GEMM2 job on slot s (chunk-1
+                // acquisitions never commit it), so count its phases per slot.
+                mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
+                if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
                 tc_fence_after();
 #pragma unroll 1
                 for (int g = 0; g < 8; ++g) {
