@@ -1,0 +1,337 @@
+#!/usr/bin/env python3
+"""bench.py -- SKLinear fwd+bwd tokens/s on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1, one rank per GPU)
+
+A step is one SKLinear forward + backward (dX, dU1s, dU2s, db) over one batch
+of synthetic tokens, through the C-ABI of libskl.so:
+  workload c2 (BASELINE.json configs[1], the BERT-base FFN shape):
+    d_in=768, d_out=3072, L=2, k=128, 32768 tokens per GPU, bf16.
+Multi-GPU: token sharding (weak scaling, 32768 tokens per GPU); forward needs
+no communication; the backward all-reduces the fp32 gradient bucket
+(dU1s | dU2s | db) with NCCL.  Rank 0 prints one JSON line.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/librnla_ref.so: the unmodified reference sources, timed by the
+reference's bench::time_op) on all host threads, over a bounded token slice of
+the same workload per step; rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "SKLinear fwd+bwd tokens/s and % roofline at 1/2/4/8 B200 vs host-CPU reference"
+D_IN, D_OUT, L, K_RANK, T_GPU = 768, 3072, 2, 128, 32768
+SEED = 42
+WORKLOAD = (f"c2: SKLinear fwd+bwd d_in={D_IN} d_out={D_OUT} L={L} k={K_RANK}, "
+            f"{T_GPU} tokens per GPU (BERT-base FFN shape)")
+CPU_SAMPLE_T = 1024  # tokens per reference CPU step (bounded sample of the same workload)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json, burst)"
+    return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def flops_per_token(d_in=D_IN, d_out=D_OUT, l=L, k=K_RANK):
+    R, D = 2 * l * k, d_in + d_out
+    return {"fwd": 2 * R * D, "bwd": 3 * R * D, "b2b": 2 * R * D,
+            "dU1": 2 * l * k * d_out, "dU2": 2 * l * k * d_in}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+            time.sleep(0.3)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        loaded = [s for s in sm if s > 0.5 * (max(sm) if sm else 1)] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+def cpu_baseline_reference(t_sample=CPU_SAMPLE_T, trials=3, warmup=1):
+    """Reference CPU SkLinear fwd+bwd (oracle/_ref) on all host cores, bounded token slice."""
+    import oracle
+    threads = os.cpu_count() or 1
+    if oracle.available("reference"):
+        o = oracle.Oracle("reference")
+        mean_ms, std_ms = o.time_fwd_bwd(D_IN, D_OUT, L, K_RANK, t_sample, SEED, threads, trials, warmup)
+        kind, cores = "reference", threads
+    else:  # scalar C restatement of the reference (oracle/skl_oracle.c)
+        o = oracle.Oracle("port")
+        t_sample = min(t_sample, 256)
+        p = o.sk_linear_fresh(D_IN, D_OUT, L, K_RANK, SEED)
+        x, g, b = oracle.inputs(D_IN, D_OUT, t_sample, SEED, o)
+        ts = []
+        for i in range(warmup + trials):
+            t0 = time.perf_counter()
+            o.forward(p, b, x)
+            o.backward(p, x, g)
+            if i >= warmup:
+                ts.append((time.perf_counter() - t0) * 1e3)
+        mean_ms, kind, cores = statistics.mean(ts), "port", 1
+    return {"value": t_sample / (mean_ms / 1e3), "unit": "tokens/s", "cores": cores, "kind": kind,
+            "sample": f"c2 shape, {t_sample}-token slice, fwd+bwd f64, mean of {trials} after {warmup} warm-up "
+                      f"(bench::time_op), {mean_ms:.1f} ms/step"}
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    cb = cpu_baseline_reference(CPU_SAMPLE_T, trials=max(1, args.steps), warmup=max(0, args.warmup))
+    v = cb["value"]
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": CPU_SAMPLE_T / v * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD + f" (reference CPU arm: {CPU_SAMPLE_T}-token slices)",
+                       "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
+                       "tokens_per_step": CPU_SAMPLE_T, "parallelism": "host OpenMP"},
+            "impl": "reference", "cpu_baseline": cb,
+            "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2601_15473_b200 as skl
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+    stream = torch.cuda.current_stream()
+
+    s = skl.shape(D_IN, D_OUT, L, K_RANK, skl.BF16)
+    bf = torch.bfloat16
+    # Replicated parameters: every rank regenerates the same sketches / U from the seed.
+    S1s = torch.empty(L, D_IN, K_RANK, dtype=bf, device=dev)
+    S2s = torch.empty(L, K_RANK, D_OUT, dtype=bf, device=dev)
+    U1s = torch.empty(L, K_RANK, D_OUT, dtype=bf, device=dev)
+    U2s = torch.empty(L, D_IN, K_RANK, dtype=bf, device=dev)
+    skl.generate_sketches(s, skl.GAUSSIAN, SEED, S1s, S2s)
+    skl.init_params(s, SEED, U1s, U2s)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1000 + rank)
+    bias = (torch.randn(D_OUT, device=dev, generator=gen) * 0.1).to(bf)
+    T = T_GPU
+    X = torch.randn(T, D_IN, device=dev, generator=gen).to(bf)
+    G = torch.randn(T, D_OUT, device=dev, generator=gen).to(bf)
+    Y = torch.empty(T, D_OUT, dtype=bf, device=dev)
+    saved = torch.empty(T, L * K_RANK, dtype=bf, device=dev)
+    GX = torch.empty(T, D_IN, dtype=bf, device=dev)
+    n1, n2 = L * K_RANK * D_OUT, L * D_IN * K_RANK
+    bucket = torch.empty(n1 + n2 + D_OUT, dtype=torch.float32, device=dev)  # dU1s | dU2s | db
+    dU1s = bucket[:n1].view(L, K_RANK, D_OUT)
+    dU2s = bucket[n1:n1 + n2].view(L, D_IN, K_RANK)
+    db = bucket[n1 + n2:]
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device=dev)
+
+    def step(x=X, g=G):
+        skl.forward(s, x, S1s, S2s, U1s, U2s, bias, Y, saved, ws)
+        skl.backward(s, g, x, saved, S1s, S2s, U1s, U2s, GX, dU1s, dU2s, db, ws)
+        if world > 1:
+            dist.all_reduce(bucket)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+
+    # ---------------- timed region: device-resident inputs (X, G > L2 each step)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = skl.launch_count()
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = skl.launch_count() - launches0
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    clocks = clk.summary()
+    value = world * T / (ms / 1e3)
+
+    # ---------------- per-kernel device times (CUDA events on the launch stream)
+    skl.profile_enable(True)
+    skl.profile_collect()
+    barrier()
+    for _ in range(args.steps):
+        step()
+    barrier()
+    prof = skl.profile_collect()
+    skl.profile_enable(False)
+    per_kernel = {k: {"launches": n, "avg_ms": t / n, "share": None} for k, (n, t) in prof.items()}
+    tot = sum(t for (_, t) in prof.values()) or 1.0
+    for k, (n, t) in prof.items():
+        per_kernel[k]["share"] = t / tot
+    dom = max(prof.items(), key=lambda kv: kv[1][1])[0] if prof else None
+    fpt = flops_per_token()
+    alg_flops = {"b2b_fwd": fpt["b2b"] * T, "b2b_bwd": fpt["b2b"] * T, "gemm_dU1": fpt["dU1"] * T,
+                 "gemm_dU2": fpt["dU2"] * T}
+    peak_tf, peak_bw, peak_src = peaks()
+    roof = None
+    if dom in alg_flops:
+        avg_ms = per_kernel[dom]["avg_ms"]
+        achieved = alg_flops[dom] / (avg_ms / 1e3) / 1e12
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "traffic.json")
+        if os.path.exists(tp):
+            with open(tp) as f:
+                traffic = json.load(f).get(dom)
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+                "frac": achieved / peak_tf, "traffic": traffic, "kernel": dom,
+                "kernel_ms": avg_ms, "peak_source": peak_src}
+    step_flops = (fpt["fwd"] + fpt["bwd"]) * T
+    step_roof = step_flops / (ms / 1e3) / 1e12
+
+    # ---------------- end to end: host buffers through the public API
+    Xh = X.cpu().pin_memory()
+    Gh = G.cpu().pin_memory()
+    Xd = torch.empty_like(X)
+    Gd = torch.empty_like(G)
+    out_h = torch.empty(bucket.numel(), dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        Xd.copy_(Xh, non_blocking=True)
+        Gd.copy_(Gh, non_blocking=True)
+        step(Xd, Gd)
+        out_h.copy_(bucket, non_blocking=True)
+    barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for _ in range(args.steps):
+        Xd.copy_(Xh, non_blocking=True)
+        Gd.copy_(Gh, non_blocking=True)
+        step(Xd, Gd)
+        out_h.copy_(bucket, non_blocking=True)
+    f1.record(stream)
+    barrier()
+    ms_e2e = max_over_ranks(f0.elapsed_time(f1) / args.steps)
+    e2e = {"value": world * T / (ms_e2e / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": Xh.numel() * 2 + Gh.numel() * 2, "d2h_bytes_per_step": out_h.numel() * 4,
+           "ms_per_step": ms_e2e, "path": "pinned host X,G -> sketched_linear_forward/backward -> grads to host"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_baseline_reference()
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "tokens/s", "cores": None, "kind": None, "sample": f"failed: {e}"}
+
+    if world > 1:
+        dist.barrier()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded Gaussian activations; sketches/U from the reference seed chain)",
+            "config": {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
+                       "tokens_per_gpu": T, "global_tokens": world * T,
+                       "parallelism": f"dp{world} (token sharding, NCCL all-reduce of dU1s|dU2s|db)",
+                       "l2": "inputs larger than L2 (X 50 MB + G 201 MB read, Y 201 MB written per step)"},
+            "roofline": roof,
+            "step_tflops": step_roof, "step_roofline_frac": step_roof / peak_tf,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+            "kernels": per_kernel,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

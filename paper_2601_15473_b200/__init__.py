@@ -33,7 +33,8 @@ OUT_F64, OUT_F32, OUT_BF16 = 0, 1, 2
 ABI_SYMBOLS = (
     "skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed", "skl_params", "skl_exceeds_dense",
     "skl_generate_sketches", "skl_init_params", "skl_realize_sketch", "skl_workspace_size",
-    "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads",
+    "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads", "skl_launch_count",
+    "skl_profile_enable", "skl_profile_collect",
 )
 
 
@@ -59,6 +60,26 @@ class _Shape(ctypes.Structure):
 class _ParamCount(ctypes.Structure):
     _fields_ = [("learnable", ctypes.c_uint64), ("total_stored", ctypes.c_uint64),
                 ("dense_equivalent", ctypes.c_uint64)]
+
+
+class _ProfEntry(ctypes.Structure):
+    _fields_ = [("name", ctypes.c_char * 48), ("launches", ctypes.c_uint64), ("total_ms", ctypes.c_double)]
+
+
+def launch_count() -> int:
+    """Kernels launched by libskl in this process (native counter)."""
+    return int(lib().skl_launch_count())
+
+
+def profile_enable(on: bool = True):
+    _check(lib().skl_profile_enable(int(on)))
+
+
+def profile_collect(max_entries: int = 64):
+    """-> {kernel name: (launches, total device ms)} since the last collect."""
+    buf = (_ProfEntry * max_entries)()
+    n = lib().skl_profile_collect(buf, max_entries)
+    return {buf[i].name.decode(): (int(buf[i].launches), float(buf[i].total_ms)) for i in range(n)}
 
 
 _lib = None
@@ -88,9 +109,14 @@ def lib() -> ctypes.CDLL:
     L.sketched_linear_forward.argtypes = [sp, i64] + [vp] * 9 + [sz, vp]
     L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 12 + [sz, vp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
+    L.skl_launch_count.restype = u64
+    L.skl_profile_enable.argtypes = [ctypes.c_int]
+    L.skl_profile_enable.restype = ctypes.c_int
+    L.skl_profile_collect.argtypes = [ctypes.POINTER(_ProfEntry), ctypes.c_int]
+    L.skl_profile_collect.restype = ctypes.c_int
     for name in ABI_SYMBOLS:
         if name not in ("skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed",
-                        "skl_exceeds_dense"):
+                        "skl_exceeds_dense", "skl_launch_count"):
             getattr(L, name).restype = ctypes.c_int
     _lib = L
     return L

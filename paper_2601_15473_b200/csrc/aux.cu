@@ -15,6 +15,7 @@
 #include <cstdint>
 
 #include "skl_internal.h"
+#include "prof.h"
 #include "sm100.cuh"
 
 namespace skl {
@@ -204,6 +205,21 @@ __global__ void to_f32_kernel(const void* in, float* out, int64_t n) {
 __global__ void reduce_partials_kernel(const float* __restrict__ part, int S, int64_t M, int64_t N, float alpha,
                                        float* __restrict__ out, int64_t nb, int64_t blk, int64_t ldm) {
     const int64_t MN = M * N;
+    if ((N & 3) == 0 && (nb & 3) == 0 && (ldm & 3) == 0 && (blk & 3) == 0) {
+        // 4 consecutive n per thread (never straddle an nb block)
+        for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < MN;
+             i += (int64_t)gridDim.x * blockDim.x * 4) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s = 0; s < S; ++s) {
+                const float4 v = __ldg(reinterpret_cast<const float4*>(part + s * MN + i));
+                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+            }
+            const int64_t m = i / N, n = i % N;
+            *reinterpret_cast<float4*>(out + (n / nb) * blk + m * ldm + n % nb) =
+                make_float4(acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha);
+        }
+        return;
+    }
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
         float acc = 0.f;
         for (int s = 0; s < S; ++s) acc += part[s * MN + i];
@@ -214,15 +230,51 @@ __global__ void reduce_partials_kernel(const float* __restrict__ part, int S, in
 
 // Column sums of G [T][N] in two fixed-order stages: chunk c sums rows
 // [c*rows_per, (c+1)*rows_per) into part[c][N]; then part is reduced.
+// Each thread owns 8 consecutive columns (one 16-B load per row for bf16,
+// two for fp32), rows in ascending order: fixed summation order.
+// Block = 8 warps x 32 lanes over 256 columns: lane owns 8 columns, warp w
+// takes rows r0+w, r0+w+8, ...; the 8 warp partials are then added in warp
+// order through shared memory (fixed order -> deterministic).
 template <typename T>
-__global__ void colsum_partial_kernel(const void* G, int64_t rows, int64_t N, int64_t rows_per, float* part) {
+__global__ void __launch_bounds__(256) colsum_partial_kernel(const void* G, int64_t rows, int64_t N,
+                                                             int64_t rows_per, float* part) {
+    __shared__ float sh[8][256];
     const int64_t c = blockIdx.y;
     const int64_t r0 = c * rows_per, r1 = min(rows, r0 + rows_per);
-    for (int64_t n = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; n < N; n += (int64_t)gridDim.x * blockDim.x) {
-        float acc = 0.f;
-        for (int64_t r = r0; r < r1; ++r) acc += ld_f<T>(G, r * N + n);
-        part[c * N + n] = acc;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t n0 = blockIdx.x * 256 + lane * 8;
+    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (n0 + 8 <= N && (N & 7) == 0) {
+#pragma unroll 4
+        for (int64_t r = r0 + w; r < r1; r += 8) {
+            if constexpr (sizeof(T) == 2) {
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(G) + r * N + n0));
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const float2 f = __bfloat1622float2(h[i]);
+                    acc[2 * i] += f.x;
+                    acc[2 * i + 1] += f.y;
+                }
+            } else {
+                const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + r * N + n0);
+                const float4 a = __ldg(p), b = __ldg(p + 1);
+                acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
+                acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
+            }
+        }
+    } else if (n0 < N) {
+        for (int64_t r = r0 + w; r < r1; r += 8)
+            for (int i = 0; i < 8 && n0 + i < N; ++i) acc[i] += ld_f<T>(G, r * N + n0 + i);
     }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) sh[w][lane * 8 + i] = acc[i];
+    __syncthreads();
+    const int64_t col = blockIdx.x * 256 + threadIdx.x;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s += sh[i][threadIdx.x];
+    if (col < N) part[c * N + col] = s;
 }
 
 inline int grid_for(uint64_t n, int block = 256) {
@@ -236,6 +288,7 @@ inline int grid_for(uint64_t n, int block = 256) {
 // ---------------------------------------------------------------- launchers
 cudaError_t launch_gen_sketches(int dist, uint64_t seed, const SklDims& d, int elem, void* S1s, void* S2s,
                                 cudaStream_t st) {
+    ProfScope ps_("gen_sketches", st);
     const double scale = 1.0 / sqrt((double)d.k);
     const uint64_t n = (uint64_t)d.L * d.k * (d.d_in + d.d_out);
     if (elem == ELEM_BF16)
@@ -251,6 +304,7 @@ cudaError_t launch_gen_sketches(int dist, uint64_t seed, const SklDims& d, int e
 }
 
 cudaError_t launch_init_u(uint64_t seed, const SklDims& d, int elem, void* U1s, void* U2s, cudaStream_t st) {
+    ProfScope ps_("init_u", st);
     const double std_dev = sqrt(2.0 / (double)(d.d_in + d.d_out));
     const uint64_t n = (uint64_t)d.L * d.k * (d.d_in + d.d_out);
     if (elem == ELEM_BF16)
@@ -265,6 +319,7 @@ cudaError_t launch_init_u(uint64_t seed, const SklDims& d, int elem, void* U1s, 
 
 cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int unit_var, int transpose, int elem,
                            void* out, cudaStream_t st) {
+    ProfScope ps_("realize", st);
     const double scale = 1.0 / sqrt((double)k);
     const uint64_t n = (uint64_t)k * dd;
     if (elem == ELEM_BF16)
@@ -280,16 +335,20 @@ cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int u
 cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
                         const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, cudaStream_t st) {
     const uint64_t n = (uint64_t)d.R_pad * (d.d_in + d.d_out);
+    {
+    ProfScope ps_("pack", st);
     if (elem == ELEM_BF16)
         pack_cat_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
                                                                     d.R_pad, Acat, Bcat);
     else
         pack_cat_kernel<float><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
                                                             d.R_pad, Acat, Bcat);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     dim3 blk(32, 8);
     if (AcatT) {
+        ProfScope ps_("transpose", st);
         dim3 g((d.R_pad + 31) / 32, (d.d_in + 31) / 32);
         if (elem == ELEM_BF16)
             transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Acat, (__nv_bfloat16*)AcatT,
@@ -298,6 +357,7 @@ cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void*
             transpose_kernel<float><<<g, blk, 0, st>>>((const float*)Acat, (float*)AcatT, d.d_in, d.R_pad);
     }
     if (BcatT) {
+        ProfScope ps_("transpose", st);
         dim3 g((d.d_out + 31) / 32, (d.R_pad + 31) / 32);
         if (elem == ELEM_BF16)
             transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Bcat, (__nv_bfloat16*)BcatT,
@@ -309,6 +369,7 @@ cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void*
 }
 
 cudaError_t launch_to_f32(const void* in, int elem, float* out, int64_t n, cudaStream_t st) {
+    ProfScope ps_("bias_f32", st);
     if (elem == ELEM_BF16) to_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(in, out, n);
     else to_f32_kernel<float><<<grid_for(n), 256, 0, st>>>(in, out, n);
     return cudaGetLastError();
@@ -316,6 +377,7 @@ cudaError_t launch_to_f32(const void* in, int elem, float* out, int64_t n, cudaS
 
 cudaError_t launch_reduce_partials(const float* part, int S, int64_t M, int64_t N, float alpha, float* out,
                                    int64_t nb, int64_t blk, int64_t ldm, cudaStream_t st) {
+    ProfScope ps_("reduce", st);
     reduce_partials_kernel<<<grid_for((uint64_t)M * N), 256, 0, st>>>(part, S, M, N, alpha, out, nb, blk, ldm);
     return cudaGetLastError();
 }
@@ -327,8 +389,10 @@ cudaError_t launch_colsum(const void* G, int elem, int64_t rows, int64_t N, floa
     const int64_t chunks = colsum_chunks(rows);
     const int64_t rows_per = (rows + chunks - 1) / chunks;
     dim3 g((unsigned)((N + 255) / 256), (unsigned)chunks);
+    ProfScope* ps_ = new ProfScope("colsum", st);
     if (elem == ELEM_BF16) colsum_partial_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
     else colsum_partial_kernel<float><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
+    delete ps_;
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return launch_reduce_partials(part, (int)chunks, 1, N, 1.0f, out, N, 0, N, st);

@@ -41,6 +41,7 @@ struct B2BArgs {
     long long ldo;
     void* save;         // H columns [save_col0, save_col0 + save_cols) -> save[t][c - save_col0]
     int save_col0, save_cols;
+    int dbg;            // perf-bisection switches (SKL_B2B_DEBUG): 1 skip GEMM2 epilogue math/stores, 4 skip GEMM2 MMAs
     long long ld_save;
 };
 
@@ -77,18 +78,21 @@ struct B2BCfg {
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 + 512;
+    static constexpr int kSmem = kStages * kStageBytes + 2 * 16384 + 1024 /*bias*/ + 1024 /*align*/ + 256;
+    static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
 template <int kCG>
 __global__ void __launch_bounds__(256, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
-               const __grid_constant__ CUtensorMap tmB2, B2BArgs args) {
+               const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
     using C = B2BCfg<kCG>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::kStages * C::kStageBytes);
+    uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 2 x 16 KB output staging
+    float* bias_s = reinterpret_cast<float*>(stage_out + 2 * 16384);  // 2 slots x 128 bias values
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * 16384 + 1024);
     uint64_t* full = bars;                            // [kStages]
     uint64_t* empty = bars + C::kStages;              // [kStages]
     uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
@@ -105,6 +109,7 @@ __global__ void __launch_bounds__(256, 1)
         prefetch_tmap(&tmA1);
         prefetch_tmap(&tmB1);
         prefetch_tmap(&tmB2);
+        prefetch_tmap(&tmY);
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], kCG);
             mbar_init(&empty[s], 1);
@@ -226,6 +231,7 @@ __global__ void __launch_bounds__(256, 1)
                         tc_fence_after();
                         const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int q = 0; q < nk; ++q) {
+                            if (args.dbg & 4) break;  // perf bisection: skip GEMM2 MMAs
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const uint32_t a_t = tmem_base + (uint32_t)((kb0 + q) * 32 + k * 8);
@@ -247,6 +253,8 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t lane_base = (q * 32u) << 16;
         uint32_t slot_seq = 0;
         uint32_t tf_par0 = 0, tf_par1 = 0;
+        uint32_t sbuf = 0;                       // output staging buffer toggle
+        const bool issuer = (q == 0 && lane == 0);  // issues / waits the bulk stores
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             const int row = t * tile_rows + (int)rank * 128 + (int)(q * 32 + lane);
@@ -257,10 +265,15 @@ __global__ void __launch_bounds__(256, 1)
                 mbar_wait(&tfull1[c], it & 1);
                 tc_fence_after();
 #pragma unroll 1
-                for (int g = 0; g < wc / 16; ++g) {
-                    uint32_t r[16];
-                    tmem_ld16(tmem_base + lane_base + 256 * c + 16 * g, r);
-                    tmem_ld_wait();
+                for (int g2 = 0; g2 < wc / 32; ++g2) {
+                  uint32_t rr[2][16];
+                  tmem_ld16(tmem_base + lane_base + 256 * c + 32 * g2, rr[0]);
+                  tmem_ld16(tmem_base + lane_base + 256 * c + 32 * g2 + 16, rr[1]);
+                  tmem_ld_wait();
+#pragma unroll
+                  for (int hh = 0; hh < 2; ++hh) {
+                    const int g = 2 * g2 + hh;
+                    const uint32_t (&r)[16] = rr[hh];
                     uint32_t p[8];
 #pragma unroll
                     for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
@@ -280,6 +293,7 @@ __global__ void __launch_bounds__(256, 1)
                                     dst[i] = pb[i];
                         }
                     }
+                  }
                 }
                 tmem_st_wait();
                 tc_fence_before();
@@ -300,45 +314,74 @@ __global__ void __launch_bounds__(256, 1)
             // ---- GEMM2 output tiles
             for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                 const uint32_t s = slot_seq & 1;
+                const uint32_t srow = q * 32 + lane;
+                // The tile's 128 bias values go through shared memory: with
+                // ~226 KB of smem in use L1 is tiny, so per-thread global bias
+                // loads would each pay L2 latency inside the epilogue.
+                const int bcol = j * 128 + (int)srow;
+                const float bval = (args.bias != nullptr && bcol < args.N2) ? __ldg(args.bias + bcol) : 0.f;
                 // tfull2[s] completes once per GEMM2 job on slot s (chunk-1
                 // acquisitions never commit it), so count its phases per slot.
                 mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
                 if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
                 tc_fence_after();
-#pragma unroll 1
-                for (int g = 0; g < 8; ++g) {
-                    uint32_t r[16];
-                    tmem_ld16(tmem_base + lane_base + 256 + 128 * s + 16 * g, r);
-                    tmem_ld_wait();
-                    const int n = j * 128 + 16 * g;
-                    if (!row_ok || n >= args.N2) continue;
-                    float v[16];
-#pragma unroll
-                    for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]) * args.alpha;
-                    if (args.bias) {
-#pragma unroll
-                        for (int i = 0; i < 16; ++i)
-                            if (n + i < args.N2) v[i] += args.bias[n + i];
+                bias_s[s * 128 + srow] = bval;  // published by the named barrier below
+                // Two 64-column halves per tile: TMEM -> alpha*acc + b -> bf16 ->
+                // 128B-swizzled smem staging buffer -> one TMA bulk store each
+                // (coalesced, clipped at T / N2 by the tensor map).
+                if (args.dbg & 1) {  // perf bisection: release the slot without reading it
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (leader) mbar_arrive(&tempty2[s]);
+                        else mbar_arrive_cluster(&tempty2[s], 0);
                     }
-                    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.out) + (long long)row * args.ldo + n;
-                    if (n + 16 <= args.N2 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                        reinterpret_cast<uint4*>(dst)[0] = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                                                      pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-                        reinterpret_cast<uint4*>(dst)[1] =
-                            make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]), pack_bf16x2(v[12], v[13]),
-                                       pack_bf16x2(v[14], v[15]));
-                    } else {
-                        for (int i = 0; i < 16 && n + i < args.N2; ++i) dst[i] = __float2bfloat16_rn(v[i]);
-                    }
+                    continue;
                 }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) {
-                    if (leader) mbar_arrive(&tempty2[s]);
-                    else mbar_arrive_cluster(&tempty2[s], 0);
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    uint32_t ra[32], rb[32];
+                    tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * h, ra);
+                    tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * h + 32, rb);
+                    tmem_ld_wait();
+                    if (h == 1) {  // every TMEM read of this slot has completed
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (leader) mbar_arrive(&tempty2[s]);
+                            else mbar_arrive_cluster(&tempty2[s], 0);
+                        }
+                    }
+                    const int n0 = j * 128 + 64 * h;
+                    uint8_t* buf = stage_out + sbuf * 16384;
+                    if (issuer) bulk_wait_read<1>();  // the store that used `buf` has read it
+                    named_bar_sync(1, 128);
+                    const uint32_t row_addr = smem_u32(buf) + srow * 128;
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float4* bp = reinterpret_cast<const float4*>(bias_s + s * 128 + 64 * h + 8 * c);
+                        const float4 b0 = bp[0], b1 = bp[1];
+                        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                        const uint32_t* src = (c < 4) ? ra : rb;
+                        const int o = (c & 3) * 8;
+                        uint32_t w[4];
+#pragma unroll
+                        for (int i = 0; i < 4; ++i)
+                            w[i] = pack_bf16x2(fmaf(__uint_as_float(src[o + 2 * i]), args.alpha, bv[2 * i]),
+                                               fmaf(__uint_as_float(src[o + 2 * i + 1]), args.alpha, bv[2 * i + 1]));
+                        st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1, 128);
+                    if (issuer) {
+                        tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
+                        bulk_commit();
+                    }
+                    sbuf ^= 1;
                 }
             }
         }
+        if (issuer) bulk_wait<0>();
     }
 
     tc_fence_before();

@@ -241,11 +241,10 @@ __global__ void __launch_bounds__(256, 1)
                     }
                     continue;
                 }
+                float bv[16];
+                load_bias16(args.bias, n, args.N, bv);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    v[j] *= args.alpha;
-                    if (args.bias && n + j < args.N) v[j] += args.bias[n + j];
-                }
+                for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], args.alpha, bv[j]);
                 const int nvalid = min(16, args.N - n);
                 for (int w = 0; w < 2; ++w) {
                     void* obase = w == 0 ? args.out : args.out2;

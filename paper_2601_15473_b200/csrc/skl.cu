@@ -25,6 +25,7 @@
 #include "../../include/skl.h"
 #include "b2b.cuh"
 #include "gemm.cuh"
+#include "prof.h"
 #include "skl_internal.h"
 
 namespace skl {
@@ -122,7 +123,7 @@ struct View {
 };
 
 template <int kCG, int kKind, bool kAMN, bool kBMN, int kBN, int kStages>
-skl_status run_gemm(const View& A, const View& B, int M, int N, int K, GemmArgs args, int sms,
+skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N, int K, GemmArgs args, int sms,
                     cudaStream_t st) {
     using C = dev::GemmCfg<kCG, kKind, kAMN, kBMN, kBN, kStages>;
     const int eb = dev::KindTraits<kKind>::kElem;
@@ -162,17 +163,21 @@ skl_status run_gemm(const View& A, const View& B, int M, int N, int K, GemmArgs 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
+    ProfScope ps_(name, st);
     SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
     return SKL_OK;
 }
 
 template <int kCG>
-skl_status run_b2b_cg(const void* a1, const void* b1, const void* b2, B2BArgs a, int sms, cudaStream_t st) {
+skl_status run_b2b_cg(const char* name, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms,
+                      cudaStream_t st) {
     using C = dev::B2BCfg<kCG>;
     CUtensorMap ta, tb1, tb2;
     SKL_TRY(make_tmap(&ta, a1, 2, a.K1, a.T, a.K1, 64, 128));
     SKL_TRY(make_tmap(&tb1, b1, 2, a.K1, a.R_pad, a.K1, 64, C::kB1BoxRows));
     SKL_TRY(make_tmap(&tb2, b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
+    CUtensorMap ty;
+    SKL_TRY(make_tmap(&ty, a.out, 2, a.N2, a.T, a.ldo, 64, 128));
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
     auto kern = dev::b2b_kernel<kCG>;
@@ -193,21 +198,28 @@ skl_status run_b2b_cg(const void* a1, const void* b1, const void* b2, B2BArgs a,
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, a));
+    ProfScope ps_(name, st);
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, ty, a));
     return SKL_OK;
 }
 
 int g_b2b_cg = 1;  // CTA-group width of the fused kernel (SKL_B2B_CG env overrides)
 
-skl_status run_b2b(int kind, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms, cudaStream_t st) {
+skl_status run_b2b(const char* name, int kind, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms,
+                   cudaStream_t st) {
     if (kind != 0) return fail(SKL_ERR_UNSUPPORTED, "fused kernel is bf16-only");
     static std::once_flag once;
     std::call_once(once, [] {
         const char* e = getenv("SKL_B2B_CG");
         if (e && atoi(e) == 2) g_b2b_cg = 2;
     });
-    if (g_b2b_cg == 2) return run_b2b_cg<2>(a1, b1, b2, a, sms, st);
-    return run_b2b_cg<1>(a1, b1, b2, a, sms, st);
+    static const int dbg = [] {
+        const char* e = getenv("SKL_B2B_DEBUG");
+        return e ? atoi(e) : 0;
+    }();
+    a.dbg = dbg;
+    if (g_b2b_cg == 2) return run_b2b_cg<2>(name, a1, b1, b2, a, sms, st);
+    return run_b2b_cg<1>(name, a1, b1, b2, a, sms, st);
 }
 
 int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
@@ -419,7 +431,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
         a.save_col0 = 0;
         a.save_cols = (int)d.Lk;
         a.ld_save = d.Lk;
-        return run_b2b(s->dtype == SKL_BF16 ? 0 : 1, x, acatT, bcatT, a, di.sms, st);
+        return run_b2b("b2b_fwd", s->dtype == SKL_BF16 ? 0 : 1, x, acatT, bcatT, a, di.sms, st);
     }
 
     // Unfused fallback: H through HBM.
@@ -435,9 +447,9 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g1.splits = 1;
     View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
     if (s->dtype == SKL_BF16)
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
     else
-        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
+        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
     GemmArgs g2 = {};
     g2.alpha = inv;
     g2.bias = bias32;
@@ -448,9 +460,9 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g2.splits = 1;
     View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
     if (s->dtype == SKL_BF16)
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
     else
-        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
+        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
     return SKL_OK;
 }
 
@@ -498,8 +510,8 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         g.out_f32 = eb == 4;
         g.splits = 1;
         View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
-        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
-        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
         saved = sv;
     }
 
@@ -519,7 +531,7 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         a.save_col0 = (int)d.Lk;
         a.save_cols = (int)d.Lk;
         a.ld_save = d.R_pad;
-        SKL_TRY(run_b2b(bf16 ? 0 : 1, grad_y, bcat, acat, a, di.sms, st));
+        SKL_TRY(run_b2b("b2b_bwd", bf16 ? 0 : 1, grad_y, bcat, acat, a, di.sms, st));
     } else {
         GemmArgs g = {};
         g.alpha = 1.f;
@@ -528,8 +540,8 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         g.out_f32 = eb == 4;
         g.splits = 1;
         View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
-        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
-        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
         if (grad_x) {
             GemmArgs g2 = {};
             g2.alpha = inv;
@@ -538,8 +550,8 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
             g2.out_f32 = eb == 4;
             g2.splits = 1;
             View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
-            if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>(vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
-            else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>(vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+            if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+            else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
         }
     }
 
@@ -551,14 +563,14 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         g.partial = part;
         g.splits = p.s_du1;
         View va{saved, T, d.Lk, d.Lk}, vb{grad_y, T, d.d_out, d.d_out};
-        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>(va, vb, (int)d.Lk, (int)d.d_out, (int)T, g, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>("gemm_dU1", va, vb, (int)d.Lk, (int)d.d_out, (int)T, g, di.sms, st)));
         SKL_CUDA(launch_reduce_partials(part, g.splits, d.Lk, d.d_out, inv,
                                         grad_U1s, d.d_out, 0, d.d_out, st));
         GemmArgs g2 = {};
         g2.partial = part;
         g2.splits = p.s_du2;
         View vx{x, T, d.d_in, d.d_in}, vp{P_S2, T, d.Lk, d.R_pad};
-        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>(vx, vp, (int)d.d_in, (int)d.Lk, (int)T, g2, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>("gemm_dU2", vx, vp, (int)d.d_in, (int)d.Lk, (int)T, g2, di.sms, st)));
         SKL_CUDA(launch_reduce_partials(part, g2.splits, d.d_in, d.Lk, inv,
                                         grad_U2s, d.k, d.d_in * d.k, d.k, st));
     } else {
@@ -574,6 +586,16 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     if (grad_bias) SKL_CUDA(launch_colsum(grad_y, elem, T, d.d_out, at<float>(workspace, p.colsum), grad_bias, st));
     return SKL_OK;
 }
+
+// ---------------------------------------------------------------- tracing
+uint64_t skl_launch_count(void) { return skl::prof_launches(); }
+
+skl_status skl_profile_enable(int on) {
+    skl::prof_set_enabled(on != 0);
+    return SKL_OK;
+}
+
+int skl_profile_collect(skl_profile_entry* out, int max_entries) { return skl::prof_collect(out, max_entries); }
 
 // ---------------------------------------------------------------- NCCL
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);
