@@ -1,0 +1,98 @@
+"""CPU tests of the C-ABI boundary (include/skl.h <-> libskl.so): the library
+loads, exports exactly what the header declares, its host-side logic matches
+the reference contracts, and without a GPU every compute entry point fails
+loudly (no CPU fallback)."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import subprocess
+
+import pytest
+
+import paper_2601_15473_b200 as skl
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "skl.h")
+
+
+def declared_functions():
+    src = open(HEADER).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*([a-z_0-9]+)\s*\(", src, flags=re.M)))
+
+
+def test_header_declares_the_path():
+    fns = declared_functions()
+    for f in ("sketched_linear_forward", "sketched_linear_backward", "skl_generate_sketches", "skl_init_params",
+              "skl_workspace_size", "skl_allreduce_grads", "skl_last_error", "skl_derive_seed"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol():
+    lib = skl.lib()
+    out = subprocess.run(["nm", "-D", "--defined-only", skl.LIB_PATH], capture_output=True, text=True).stdout
+    exported = {line.split()[-1] for line in out.splitlines() if " T " in line}
+    for f in declared_functions():
+        assert f in exported, f
+        assert getattr(lib, f) is not None
+    assert set(skl.ABI_SYMBOLS) <= set(declared_functions())
+
+
+def test_library_targets_sm100a_only():
+    out = subprocess.run(["cuobjdump", "--list-elf", skl.LIB_PATH], capture_output=True, text=True).stdout
+    archs = set(re.findall(r"sm_(\d+a?)", out))
+    assert archs == {"100a"}, archs
+
+
+def test_host_contracts(port):
+    assert skl.lib().skl_rng_algorithm().decode() == "splitmix64-boxmuller-v1"  # rng.hpp:10
+    for m, i in ((42, 0), (42, 1000), (0, 7), (2**64 - 1, 3)):
+        assert skl.derive_seed(m, i) == port.derive_seed(m, i)
+    s = skl.shape(8192, 8192, 1, 16)
+    learn, stored, dense = skl.params(s)
+    assert stored - 8192 == 524288 and dense - 8192 == 67108864 and learn == 16 * 16384 + 8192
+    assert skl.exceeds_dense(2, 64, 256, 256) and not skl.exceeds_dense(1, 64, 256, 256)
+
+
+def test_parameter_and_shape_errors():
+    with pytest.raises(skl.ParameterError):
+        skl.params(skl.shape(8, 8, 0, 4))          # nn_layers.cpp:116
+    with pytest.raises(skl.ParameterError):
+        skl.workspace_size(skl.shape(8, 8, 2, 0), 16)
+    with pytest.raises(skl.ShapeError):
+        skl.workspace_size(skl.shape(8, 8, 1, 4), -1)
+    with pytest.raises(skl.ShapeError):
+        skl.params(skl.shape(0, 8, 1, 4))
+
+
+def test_workspace_plan_is_monotone_in_tokens():
+    s = skl.shape(768, 3072, 2, 128)
+    f1, b1 = skl.workspace_size(s, 1024)
+    f2, b2 = skl.workspace_size(s, 32768)
+    assert 0 < f1 <= f2 and 0 < b1 <= b2
+    assert b2 >= 32768 * 512 * 2  # backward keeps P [T, R] (bf16)
+
+
+def test_compute_fails_loudly_without_gpu():
+    """No CPU fallback: compute entry points report SKL_ERR_CUDA on a GPU-less host."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    s = skl.shape(64, 64, 1, 16)
+    lib = skl.lib()
+    rc = lib.skl_generate_sketches(ctypes.byref(s), 0, 1, None, None, None)
+    assert rc == 3 and b"no CUDA device" in lib.skl_last_error()
+    rc = lib.sketched_linear_forward(ctypes.byref(s), 16, *([ctypes.c_void_p(16)] * 9), 1 << 30, None)
+    assert rc == 3
+
+
+def test_unsupported_alignment_is_reported():
+    """Row strides that TMA cannot address are rejected, not silently mishandled."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("reaches the device check first on CPU only")
+    s = skl.shape(6, 8, 2, 3)  # reference test shape: d_in*2 bytes not 16-B aligned
+    rc = skl.lib().sketched_linear_forward(ctypes.byref(s), 4, *([ctypes.c_void_p(16)] * 9), 1 << 30, None)
+    assert rc == 5 and b"multiples of" in skl.lib().skl_last_error()
