@@ -1,0 +1,326 @@
+// du.cuh -- the fused parameter-gradient kernel of the SKLinear backward.
+//
+//   dU1s = inv · Savedᵀ · G      [L·k, d_out]          Saved = x·S1 (from the forward)
+//   dU2s = inv · Xᵀ · P_S2       [d_in, L·k] -> [L][d_in][k]   P_S2 = G·S2ᵀ (from b2b_bwd)
+//   db   = Σ_t G[t, :]                                  (nn_layers.cpp:99, unscaled)
+//
+// Reference: SkLinear::backward grad_u1 / grad_u2 / grad_b (nn_layers.cpp:88-99).
+// All three are reductions over the T tokens.  One persistent launch covers
+// both GEMMs as a grouped problem list, split along T (split-K) so every SM
+// has work; the column sums of G ride along on the G tiles already staged in
+// shared memory for dU1 (warp 3 sums them while the tensor core consumes the
+// same stage), so G is read from HBM once for dU1 and db together.
+//
+// Reduction is deterministic and in-kernel: every (tile, split) unit writes
+// its fp32 partial to the workspace; the last unit of a tile to finish (an
+// atomic ticket per tile) sums the partials in split order 0..S-1, applies
+// alpha and the output layout, and resets the ticket.  No extra launches.
+//
+// Operands are token-major in HBM, so both A and B are MN-major UMMA tiles
+// (128B-swizzled TMA boxes of [64 tokens x 64 features]).
+#pragma once
+
+#include "sm100.cuh"
+
+namespace skl {
+
+struct DuProblem {
+    int M, N;             // output is M x N
+    int m_tiles, n_tiles;  // 128 x 256 tiles
+    int tile0;            // first global tile index of this problem
+    int colsum;           // 1: also sum the B operand over K (db)
+    float alpha;
+    float* out;           // out[(n / nb) * blk + m * ldm + n % nb]
+    long long nb, blk, ldm;
+    float* db;            // [N] when colsum
+};
+
+struct DuArgs {
+    int k_blocks, splits, num_tiles;
+    DuProblem p[2];
+    float* part;     // [num_tiles][splits][128][256]
+    float* cpart;    // [p0.n_tiles][splits][256]
+    int* tickets;    // [num_tiles], zero on entry, left zero on exit
+    int coop;        // 1: cooperative launch (all units co-resident) -> split-parallel reduction
+};
+
+namespace dev {
+
+constexpr int kDuBM = 128, kDuBN = 256, kDuBK = 64, kDuStages = 4;
+constexpr int kDuABytes = kDuBM * 128;   // 2 blocks of [64 rows x 128 B]
+constexpr int kDuBBytes = kDuBN * 128;   // 4 blocks of [64 rows x 128 B]
+constexpr int kDuStageBytes = kDuABytes + kDuBBytes;
+constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 4096;
+
+__global__ void __launch_bounds__(256, 1)
+    du_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
+              const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1, DuArgs args) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + kDuStages * kDuABytes;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kDuStages * kDuStageBytes);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + kDuStages;
+    uint64_t* tfull = bars + 2 * kDuStages;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* ticket_s = reinterpret_cast<int*>(tmem_slot + 1);
+    float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [4][256]
+
+    const uint32_t warp = warp_id();
+    const uint32_t lane = lane_id();
+
+    if (warp == 0 && elect_one()) {
+        prefetch_tmap(&tmA0);
+        prefetch_tmap(&tmB0);
+        prefetch_tmap(&tmA1);
+        prefetch_tmap(&tmB1);
+        for (int s = 0; s < kDuStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 5);  // MMA commit + 4 colsum warps (or 4 extra commits)
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 2) {
+        tmem_alloc<1>(tmem_slot, 512);
+        tmem_relinquish<1>();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    const int units = args.num_tiles * args.splits;
+    struct Unit {
+        int p, mt, nt, tile, split, kb0, kb1;
+        bool colsum;
+    };
+    auto decode = [&](int u) {
+        Unit x;
+        x.split = u / args.num_tiles;
+        x.tile = u % args.num_tiles;
+        x.p = x.tile >= args.p[1].tile0 && args.p[1].m_tiles > 0 ? 1 : 0;
+        const int lt = x.tile - args.p[x.p].tile0;
+        x.mt = lt % args.p[x.p].m_tiles;
+        x.nt = lt / args.p[x.p].m_tiles;
+        x.kb0 = (int)(((long long)x.split * args.k_blocks) / args.splits);
+        x.kb1 = (int)(((long long)(x.split + 1) * args.k_blocks) / args.splits);
+        x.colsum = args.p[x.p].colsum && x.mt == 0;
+        return x;
+    };
+
+    if (warp == 0) {
+        // ------------------------------------------------------------ producer
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+                const Unit x = decode(u);
+                const CUtensorMap* ma = x.p ? &tmA1 : &tmA0;
+                const CUtensorMap* mb = x.p ? &tmB1 : &tmB0;
+                const int m0 = x.mt * kDuBM, n0 = x.nt * kDuBN;
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    uint8_t* a_dst = sA + stage * kDuABytes;
+                    uint8_t* b_dst = sB + stage * kDuBBytes;
+                    const int k0 = kb * kDuBK;
+                    mbar_arrive_expect_tx(&full[stage], kDuStageBytes);
+                    tma_load_2d<1>(ma, &full[stage], a_dst, m0, k0);
+                    tma_load_2d<1>(ma, &full[stage], a_dst + 64 * 128, m0 + 64, k0);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) tma_load_2d<1>(mb, &full[stage], b_dst + j * 64 * 128, n0 + 64 * j, k0);
+                    if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------------------------------------ MMA issuer
+        if (elect_one()) {
+            constexpr uint32_t idesc = make_idesc(0, kDuBM, kDuBN, 1, 1);
+            int stage = 0;
+            uint32_t phase = 0;
+            int iter = 0;
+            for (int u = blockIdx.x; u < units; u += gridDim.x, ++iter) {
+                const Unit x = decode(u);
+                const int acc = iter & 1;
+                mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * kDuBN;
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = smem_u32(sA + stage * kDuABytes);
+                    const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        mma_ss<1, 0>(d_tmem, make_sdesc(a_addr + k * 16 * 128, 64 * 128, 1024),
+                                     make_sdesc(b_addr + k * 16 * 128, 64 * 128, 1024), idesc,
+                                     (kb > x.kb0 || k > 0) ? 1u : 0u);
+                    mma_commit<1>(&empty[stage]);
+                    if (!x.colsum)  // stand in for the 4 colsum warps
+                        for (int i = 0; i < 4; ++i) mma_commit<1>(&empty[stage]);
+                    if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+                }
+                mma_commit<1>(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------------------------------------------------------ epilogue warps (colsum + partials + reduce)
+        const uint32_t q = warp & 3;
+        const int t = (int)(q * 32 + lane);  // 0..127
+        int stage = 0;
+        uint32_t phase = 0;
+        int iter = 0;
+        for (int u = blockIdx.x; u < units; u += gridDim.x, ++iter) {
+            const Unit x = decode(u);
+            const DuProblem& P = args.p[x.p];
+            const int m0 = x.mt * kDuBM, n0 = x.nt * kDuBN;
+            if (x.colsum) {
+                // ---- column sums of the staged G tiles while the tensor core
+                // consumes them: thread -> one 16-B chunk (8 columns) of one of the
+                // four 64-column blocks, 16 of the 64 token rows of each stage.
+                const int chunk = t & 31, blk = chunk >> 3, ch = chunk & 7, r0 = (t >> 5) * 16;
+                float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes) + blk * 64 * 128;
+#pragma unroll
+                    for (int r = r0; r < r0 + 16; ++r) {
+                        uint32_t w[4];
+                        asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+                                     : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                                     : "r"(b_addr + r * 128 + ((uint32_t)(ch ^ (r & 7)) << 4)));
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+                            cs[2 * i] += f.x;
+                            cs[2 * i + 1] += f.y;
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[stage]);
+                    if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+                }
+                // combine the four row groups in order -> cpart[nt][split][256]
+#pragma unroll
+                for (int i = 0; i < 8; ++i) csum_s[(t >> 5) * 256 + chunk * 8 + i] = cs[i];
+                named_bar_sync(2, 128);
+                for (int c = t; c < kDuBN; c += 128)
+                    __stcg(args.cpart + ((long long)x.nt * args.splits + x.split) * kDuBN + c,
+                           csum_s[c] + csum_s[256 + c] + csum_s[512 + c] + csum_s[768 + c]);
+                named_bar_sync(2, 128);
+            } else {
+                // the MMA issuer arrives for us on non-colsum units; keep the ring position
+                for (int kb = x.kb0; kb < x.kb1; ++kb)
+                    if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+            }
+            // ---- accumulator -> fp32 partial [tile][split][128][256]
+            const int acc = iter & 1;
+            mbar_wait(&tfull[acc], (iter >> 1) & 1);
+            tc_fence_after();
+            {
+                float* prow = args.part + (((long long)x.tile * args.splits + x.split) * kDuBM + t) * kDuBN;
+                const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
+#pragma unroll 1
+                for (int c = 0; c < kDuBN; c += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + c, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        __stcg(reinterpret_cast<float4*>(prow + c + i),
+                               make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                           __uint_as_float(v[i + 3])));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+
+            // ---- deterministic split reduction (sum in split order 0..S-1)
+            __threadfence();
+            named_bar_sync(2, 128);
+            int* tk = args.tickets + x.tile;
+            int row_lo, row_hi, col_lo, col_hi;
+            if (args.coop) {
+                // all units are co-resident (cooperative launch): wait for the S
+                // partials, then unit `split` reduces its 1/S slice of the tile.
+                if (t == 0) {
+                    atomicAdd(tk, 1);
+                    while (ld_acquire_gpu(tk) < args.splits) __nanosleep(64);
+                }
+                named_bar_sync(2, 128);
+                row_lo = x.split * kDuBM / args.splits;
+                row_hi = (x.split + 1) * kDuBM / args.splits;
+                col_lo = x.split * kDuBN / args.splits;
+                col_hi = (x.split + 1) * kDuBN / args.splits;
+            } else {
+                if (t == 0) *ticket_s = atomicAdd(tk, 1);
+                named_bar_sync(2, 128);
+                const bool last = *ticket_s == args.splits - 1;
+                named_bar_sync(2, 128);
+                row_lo = 0; row_hi = last ? kDuBM : 0;
+                col_lo = 0; col_hi = last ? kDuBN : 0;
+            }
+            __threadfence();
+            const float* pbase = args.part + (long long)x.tile * args.splits * kDuBM * kDuBN;
+            const bool vec = (P.nb & 3) == 0 && (P.ldm & 3) == 0 && (P.blk & 3) == 0 &&
+                             (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
+            for (int f = t; f < (row_hi - row_lo) * (kDuBN / 4); f += 128) {
+                const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
+                const int m = m0 + r, n = n0 + c;
+                if (m >= P.M || n >= P.N) continue;
+                float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int sp = 0; sp < args.splits; ++sp) {
+                    const float4 v = __ldcg(reinterpret_cast<const float4*>(pbase + ((long long)sp * kDuBM + r) * kDuBN + c));
+                    sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+                }
+                const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
+                if (vec && n + 4 <= P.N) {
+                    *reinterpret_cast<float4*>(P.out + (n / P.nb) * P.blk + (long long)m * P.ldm + n % P.nb) =
+                        make_float4(o[0], o[1], o[2], o[3]);
+                } else {
+                    for (int i = 0; i < 4 && n + i < P.N; ++i) {
+                        const long long nn = n + i;
+                        P.out[(nn / P.nb) * P.blk + (long long)m * P.ldm + nn % P.nb] = o[i];
+                    }
+                }
+            }
+            if (x.colsum) {
+                for (int c = col_lo + t; c < col_hi; c += 128) {
+                    const int n = n0 + c;
+                    if (n >= P.N) continue;
+                    float sum = 0.f;
+                    for (int sp = 0; sp < args.splits; ++sp)
+                        sum += __ldcg(args.cpart + ((long long)x.nt * args.splits + sp) * kDuBN + c);
+                    P.db[n] = sum;
+                }
+            }
+            // ---- ticket release: the last of the S units to get here resets it
+            named_bar_sync(2, 128);
+            if (t == 0) {
+                if (args.coop) {
+                    if (atomicAdd(tk, 1) == 2 * args.splits - 1) atomicExch(tk, 0);
+                } else if (*ticket_s == args.splits - 1) {
+                    atomicExch(tk, 0);
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem_base, 512);
+    }
+}
+
+}  // namespace dev
+}  // namespace skl

@@ -24,6 +24,7 @@
 
 #include "../../include/skl.h"
 #include "b2b.cuh"
+#include "du.cuh"
 #include "gemm.cuh"
 #include "prof.h"
 #include "skl_internal.h"
@@ -276,8 +277,26 @@ bool use_fused(const SklDims& d, skl_dtype t) {
 
 struct Plan {
     size_t acat, bcat, acatT, bcatT, bias32, inter, saved, part, colsum, total;
+    size_t du_part, du_cpart, du_tickets;
     int s_du1, s_du2;
 };
+
+// Tiling of the fused dU kernel (du.cuh): problem 0 = dU1 [Lk, d_out],
+// problem 1 = dU2 [d_in, Lk]; 128 x 256 tiles; T split so ~one unit per SM.
+struct DuShape {
+    int m0, n0t, m1, n1t, tiles, splits, kb;
+};
+DuShape du_shape(const SklDims& d, int64_t T, int sms) {
+    DuShape s;
+    s.m0 = (int)((d.Lk + 127) / 128);
+    s.n0t = (int)((d.d_out + 255) / 256);
+    s.m1 = (int)((d.d_in + 127) / 128);
+    s.n1t = (int)((d.Lk + 255) / 256);
+    s.tiles = s.m0 * s.n0t + s.m1 * s.n1t;
+    s.kb = (int)std::max<int64_t>(1, (T + 63) / 64);
+    s.splits = std::max(1, std::min(sms / s.tiles, std::max(1, s.kb / 2)));
+    return s;
+}
 
 // Offsets into the caller's workspace (1 KiB aligned).
 Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
@@ -304,6 +323,10 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     if (bwd) {
         part = std::max((size_t)p.s_du1 * d.Lk * d.d_out, (size_t)p.s_du2 * d.d_in * d.Lk) * 4;
         if (t == SKL_F32_TF32) part += (size_t)T * (d.d_in + d.d_out + 2 * d.Lk) * 4;  // transposed operands
+        const DuShape u = du_shape(d, T, sms);
+        p.du_part = take((size_t)u.tiles * u.splits * 128 * 256 * 4);
+        p.du_cpart = take((size_t)u.n0t * u.splits * 256 * 4);
+        p.du_tickets = take((size_t)u.tiles * 4);
     }
     p.part = take(part);
     p.colsum = take(bwd ? (size_t)colsum_chunks(T) * d.d_out * 4 : 0);
@@ -558,6 +581,53 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     // dU1s = inv·Savedᵀ·G  ([Lk, d_out] == [L][k][d_out])
     // dU2s = inv·Xᵀ·P_S2   ([d_in, Lk] scattered to [L][d_in][k])
     const void* P_S2 = at<uint8_t>(P, (size_t)d.Lk * eb);
+    static const bool legacy_du = [] {
+        const char* e = getenv("SKL_DU_LEGACY");
+        return e && atoi(e) != 0;
+    }();
+    if (bf16 && !legacy_du) {
+        // fused dU1 + dU2 (+ db) with in-kernel deterministic split reduction
+        const DuShape u = du_shape(d, T, di.sms);
+        DuArgs a = {};
+        a.k_blocks = u.kb;
+        a.splits = u.splits;
+        a.num_tiles = u.tiles;
+        a.p[0] = DuProblem{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
+                           (long long)d.d_out, 0, (long long)d.d_out, grad_bias};
+        a.p[1] = DuProblem{(int)d.d_in, (int)d.Lk, u.m1, u.n1t, u.m0 * u.n0t, 0, inv, grad_U2s,
+                           (long long)d.k, (long long)(d.d_in * d.k), (long long)d.k, nullptr};
+        a.part = at<float>(workspace, p.du_part);
+        a.cpart = at<float>(workspace, p.du_cpart);
+        a.tickets = at<int>(workspace, p.du_tickets);
+        CUtensorMap ta0, tb0, ta1, tb1;
+        SKL_TRY(make_tmap(&ta0, saved, 2, d.Lk, T, d.Lk, 64, 64));
+        SKL_TRY(make_tmap(&tb0, grad_y, 2, d.d_out, T, d.d_out, 64, 64));
+        SKL_TRY(make_tmap(&ta1, x, 2, d.d_in, T, d.d_in, 64, 64));
+        SKL_TRY(make_tmap(&tb1, P_S2, 2, d.Lk, T, d.R_pad, 64, 64));
+        SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
+        static bool attr_set = false;
+        if (!attr_set) {
+            SKL_CUDA(cudaFuncSetAttribute(dev::du_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
+            attr_set = true;
+        }
+        const int units = u.tiles * u.splits;
+        // One unit per SM and all units co-resident -> cooperative launch, and
+        // the S units of a tile reduce its partials in parallel (1/S each).
+        a.coop = units <= di.sms ? 1 : 0;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(a.coop ? units : std::min(di.sms, units));
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = dev::kDuSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = a.coop;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ProfScope ps_("du_fused", st);
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a));
+        return SKL_OK;
+    }
     if (bf16) {
         GemmArgs g = {};
         g.partial = part;
