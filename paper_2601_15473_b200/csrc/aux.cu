@@ -12,6 +12,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "skl_internal.h"
@@ -329,6 +330,80 @@ cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int u
         realize_kernel<float><<<grid_for(n), 256, 0, st>>>(dist, k, dd, seed, scale, unit_var, transpose, out);
     else
         realize_kernel<double><<<grid_for(n), 256, 0, st>>>(dist, k, dd, seed, scale, unit_var, transpose, out);
+    return cudaGetLastError();
+}
+
+// One launch packs both operand panels in every requested layout: each block
+// moves a 32x32 tile (coalesced read of the contiguous stack dimension,
+// coalesced write of the natural layout, smem transpose for the other), and
+// block 0 also converts the bias to fp32.
+template <typename T>
+__global__ void __launch_bounds__(256) pack_tiles_kernel(const void* S1s, const void* U2s, const void* U1s,
+                                                         const void* S2s, int64_t L, int64_t k, int64_t d_in,
+                                                         int64_t d_out, int64_t R_pad, void* Acat, void* Bcat,
+                                                         void* AcatT, void* BcatT, const void* bias, float* bias32) {
+    __shared__ float tile[32][33];
+    const int64_t Lk = L * k;
+    const int64_t ta_r = R_pad / 32, ta_c = (d_in + 31) / 32;
+    const int64_t tb_c = (d_out + 31) / 32;
+    const int64_t nA = ta_r * ta_c, nB = ta_r * tb_c;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    if (bias32 && blockIdx.x == 0)
+        for (int64_t i = threadIdx.x; i < d_out; i += blockDim.x) bias32[i] = bias ? ld_f<T>(bias, i) : 0.f;
+    for (int64_t b = blockIdx.x; b < nA + nB; b += gridDim.x) {
+        const bool isA = b < nA;
+        int64_t row0, col0, rows, cols;  // natural layout: A = [d_in][R_pad], B = [R_pad][d_out]
+        if (isA) { row0 = (b / ta_r) * 32; col0 = (b % ta_r) * 32; rows = d_in; cols = R_pad; }
+        else { const int64_t bb = b - nA; row0 = (bb / tb_c) * 32; col0 = (bb % tb_c) * 32; rows = R_pad; cols = d_out; }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = row0 + ty + 8 * i, c = col0 + tx;
+            float v = 0.f;
+            if (r < rows && c < cols) {
+                if (isA) {  // (c_in = r, rank = c)
+                    if (c < Lk) v = ld_f<T>(S1s, ((c / k) * d_in + r) * k + c % k);
+                    else if (c < 2 * Lk) v = ld_f<T>(U2s, (((c - Lk) / k) * d_in + r) * k + (c - Lk) % k);
+                } else {    // (rank = r, c_out = c)
+                    if (r < Lk) v = ld_f<T>(U1s, r * d_out + c);
+                    else if (r < 2 * Lk) v = ld_f<T>(S2s, (r - Lk) * d_out + c);
+                }
+            }
+            if constexpr (sizeof(T) == 4) v = dev::tf32_rna(v);
+            tile[ty + 8 * i][tx] = v;
+            void* nat = isA ? Acat : Bcat;
+            if (nat && r < rows && c < cols) {
+                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(nat)[r * cols + c] = __float2bfloat16_rn(v);
+                else reinterpret_cast<float*>(nat)[r * cols + c] = v;
+            }
+        }
+        void* tr = isA ? AcatT : BcatT;
+        if (!tr) continue;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t c = col0 + ty + 8 * i, r = row0 + tx;  // transposed: [cols][rows]
+            if (r < rows && c < cols) {
+                const float v = tile[tx][ty + 8 * i];
+                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(tr)[c * rows + r] = __float2bfloat16_rn(v);
+                else reinterpret_cast<float*>(tr)[c * rows + r] = v;
+            }
+        }
+    }
+}
+
+cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
+                         const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, const void* bias,
+                         float* bias32, cudaStream_t st) {
+    ProfScope ps_("pack", st);
+    const int64_t tiles = (d.R_pad / 32) * ((d.d_in + 31) / 32 + (d.d_out + 31) / 32);
+    const int grid = (int)std::min<int64_t>(tiles, 148 * 8);
+    if (elem == ELEM_BF16)
+        pack_tiles_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out, d.R_pad,
+                                                               Acat, Bcat, AcatT, BcatT, bias, bias32);
+    else
+        pack_tiles_kernel<float><<<grid, 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out, d.R_pad, Acat,
+                                                       Bcat, AcatT, BcatT, bias, bias32);
     return cudaGetLastError();
 }
 

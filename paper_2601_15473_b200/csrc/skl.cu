@@ -436,8 +436,9 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     void* acatT = at<void>(workspace, p.acatT);
     void* bcatT = at<void>(workspace, p.bcatT);
     float* bias32 = at<float>(workspace, p.bias32);
-    SKL_CUDA(launch_pack(d, elem, S1s, U2s, U1s, S2s, acat, bcat, acatT, bcatT, st));
-    SKL_CUDA(launch_to_f32(bias, elem, bias32, d.d_out, st));
+    SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, bcatT, bias, bias32, st));
+    (void)acat;
+    (void)bcat;
 
     if (use_fused(d, s->dtype)) {
         B2BArgs a = {};
@@ -520,7 +521,8 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     void* acatT = at<void>(workspace, p.acatT);
     void* P = at<void>(workspace, p.inter);
     float* part = at<float>(workspace, p.part);
-    SKL_CUDA(launch_pack(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, st));
+    SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, nullptr,
+                          nullptr, st));
 
     // Saved projection x·S1 (recomputed only when the caller did not keep it).
     const void* saved = saved_proj;
