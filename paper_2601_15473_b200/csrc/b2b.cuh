@@ -41,6 +41,8 @@ struct B2BArgs {
     long long ldo;
     void* save;         // H columns [save_col0, save_col0 + save_cols) -> save[t][c - save_col0]
     int save_col0, save_cols;
+    int Lk, k, dS;      // direct modes: L*k, k, and the term row stride of the [L*d][k] views
+    int bias_bf16;      // bias pointer holds bf16 (direct modes skip the fp32 copy)
     int dbg;            // perf-bisection switches (SKL_B2B_DEBUG): 1 skip GEMM2 epilogue math/stores, 4 skip GEMM2 MMAs
     long long ld_save;
 };
@@ -82,10 +84,17 @@ struct B2BCfg {
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
-template <int kCG>
+// kMode 0: B1 / B2 are packed K-major panels (any k).
+// kMode 1: forward straight from the ABI stacks (k % 64 == 0): B1 = S1s|U2s
+//          viewed as [L*d_in][k] (MN-major tiles), B2 = U1s|S2s viewed as
+//          [L*k][d_out] (MN-major tiles).  No packing pass.
+// kMode 2: backward straight from the stacks: B1 = U1s|S2s [L*k][d_out]
+//          (K-major), B2 = S1s|U2s [L*d_in][k] (K-major, per-term row offset).
+template <int kCG, int kMode>
 __global__ void __launch_bounds__(256, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
-               const __grid_constant__ CUtensorMap tmB2, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
+               const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
+               const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
     using C = B2BCfg<kCG>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -109,6 +118,10 @@ __global__ void __launch_bounds__(256, 1)
         prefetch_tmap(&tmA1);
         prefetch_tmap(&tmB1);
         prefetch_tmap(&tmB2);
+        if constexpr (kMode != 0) {
+            prefetch_tmap(&tmB1b);
+            prefetch_tmap(&tmB2b);
+        }
         prefetch_tmap(&tmY);
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], kCG);
@@ -160,8 +173,23 @@ __global__ void __launch_bounds__(256, 1)
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
                         tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * 64, am);
-                        for (int r = 0; r < brows; r += C::kB1BoxRows)
-                            tma_load_2d<kCG>(&tmB1, &full[stage], st + 16384 + r * 128, kb * 64, b0 + r);
+                        if constexpr (kMode == 0) {
+                            for (int r = 0; r < brows; r += C::kB1BoxRows)
+                                tma_load_2d<kCG>(&tmB1, &full[stage], st + 16384 + r * 128, kb * 64, b0 + r);
+                        } else if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
+                            for (int r = 0; r < brows; r += C::kB1BoxRows) {
+                                const int rg = b0 + r;
+                                tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], st + 16384 + r * 128, kb * 64,
+                                                 rg < args.Lk ? rg : rg - args.Lk);
+                            }
+                        } else {  // MN-major [64 d_in rows x 64 rank cols] blocks of S1s | U2s
+                            for (int jb = 0; jb < brows / 64; ++jb) {
+                                const int rg = b0 + 64 * jb;
+                                const int rr = rg < args.Lk ? rg : rg - args.Lk;
+                                tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], st + 16384 + jb * 8192,
+                                                 rr % args.k, (rr / args.k) * args.dS + kb * 64);
+                            }
+                        }
                         next();
                     }
                 }
@@ -174,8 +202,21 @@ __global__ void __launch_bounds__(256, 1)
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
                         else mbar_arrive_cluster(&full[stage], 0);
-                        for (int q = 0; q < nk; ++q)
-                            tma_load_2d<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, (kb0 + q) * 64, brow);
+                        for (int q = 0; q < nk; ++q) {
+                            const int r0 = (kb0 + q) * 64;  // rank index of this k-block
+                            if constexpr (kMode == 0) {
+                                tma_load_2d<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, r0, brow);
+                            } else if constexpr (kMode == 1) {  // MN-major rows of [U1s ; S2s]
+                                const CUtensorMap* m = r0 < args.Lk ? &tmB2 : &tmB2b;
+                                const int rr = r0 < args.Lk ? r0 : r0 - args.Lk;
+                                for (int jb = 0; jb < C::kB2Rows / 64; ++jb)
+                                    tma_load_2d<kCG>(m, &full[stage], st + q * C::kB2KbBytes + jb * 8192, brow + 64 * jb, rr);
+                            } else {  // K-major [d_in rows x 64 rank cols] of S1s | U2s, term row offset
+                                const int rr = r0 < args.Lk ? r0 : r0 - args.Lk;
+                                tma_load_2d<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st + q * C::kB2KbBytes,
+                                                 rr % args.k, (rr / args.k) * args.dS + brow);
+                            }
+                        }
                         next();
                     }
                 }
@@ -188,7 +229,7 @@ __global__ void __launch_bounds__(256, 1)
             uint32_t phase = 0;
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             uint32_t slot_seq = 0;
-            const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, 0);
+            const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
             int it = 0;
             for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
                 // ---- GEMM1: H chunks
@@ -199,7 +240,7 @@ __global__ void __launch_bounds__(256, 1)
                             mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1);
                         tc_fence_after();
                     }
-                    const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, 0);
+                    const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
                     const uint32_t d = tmem_base + 256 * c;
                     for (int kb = 0; kb < nkb1; ++kb) {
                         mbar_wait(&full[stage], phase);
@@ -208,7 +249,9 @@ __global__ void __launch_bounds__(256, 1)
                         const uint32_t b_addr = a_addr + 16384;
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
-                            mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024), make_sdesc(b_addr + k * 32, 0, 1024),
+                            mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024),
+                                           kMode == 1 ? make_sdesc(b_addr + k * 2048, 8192, 1024)
+                                                      : make_sdesc(b_addr + k * 32, 0, 1024),
                                            idesc1, (kb > 0 || k > 0) ? 1u : 0u);
                         mma_commit<kCG>(&empty[stage]);
                         next();
@@ -235,8 +278,10 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const uint32_t a_t = tmem_base + (uint32_t)((kb0 + q) * 32 + k * 8);
-                                mma_ts<kCG>(d, a_t, make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024), idesc2,
-                                            (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
+                                const uint64_t bdesc = kMode == 1
+                                    ? make_sdesc(b_addr + q * C::kB2KbBytes + k * 2048, 8192, 1024)
+                                    : make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024);
+                                mma_ts<kCG>(d, a_t, bdesc, idesc2, (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
                             }
                         }
                         mma_commit<kCG>(&empty[stage]);
@@ -319,7 +364,10 @@ __global__ void __launch_bounds__(256, 1)
                 // ~226 KB of smem in use L1 is tiny, so per-thread global bias
                 // loads would each pay L2 latency inside the epilogue.
                 const int bcol = j * 128 + (int)srow;
-                const float bval = (args.bias != nullptr && bcol < args.N2) ? __ldg(args.bias + bcol) : 0.f;
+                float bval = 0.f;
+                if (args.bias != nullptr && bcol < args.N2)
+                    bval = args.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[bcol])
+                                          : __ldg(args.bias + bcol);
                 // tfull2[s] completes once per GEMM2 job on slot s (chunk-1
                 // acquisitions never commit it), so count its phases per slot.
                 mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
@@ -353,6 +401,7 @@ __global__ void __launch_bounds__(256, 1)
                         }
                     }
                     const int n0 = j * 128 + 64 * h;
+                    if (args.dbg & 16) continue;  // perf bisection: TMEM reads only
                     uint8_t* buf = stage_out + sbuf * 16384;
                     if (issuer) bulk_wait_read<1>();  // the store that used `buf` has read it
                     named_bar_sync(1, 128);
@@ -373,7 +422,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(1, 128);
-                    if (issuer) {
+                    if (issuer && !(args.dbg & 8)) {
                         tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
                         bulk_commit();
                     }

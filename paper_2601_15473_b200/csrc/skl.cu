@@ -169,19 +169,42 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     return SKL_OK;
 }
 
-template <int kCG>
-skl_status run_b2b_cg(const char* name, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms,
-                      cudaStream_t st) {
+// Operand sources of the fused kernel.  kMode 0: b1 / b2 are packed panels.
+// kMode 1 (forward, direct): b1 = S1s, b1b = U2s ([L*d_in][k] views),
+//                            b2 = U1s, b2b = S2s ([L*k][d_out] views).
+// kMode 2 (backward, direct): b1 = U1s, b1b = S2s ([L*k][d_out] views),
+//                             b2 = S1s, b2b = U2s ([L*d_in][k] views).
+struct B2BSrc {
+    const void *a1, *b1, *b1b, *b2, *b2b;
+};
+
+template <int kCG, int kMode>
+skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     using C = dev::B2BCfg<kCG>;
-    CUtensorMap ta, tb1, tb2;
-    SKL_TRY(make_tmap(&ta, a1, 2, a.K1, a.T, a.K1, 64, 128));
-    SKL_TRY(make_tmap(&tb1, b1, 2, a.K1, a.R_pad, a.K1, 64, C::kB1BoxRows));
-    SKL_TRY(make_tmap(&tb2, b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
-    CUtensorMap ty;
+    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty;
+    SKL_TRY(make_tmap(&ta, src.a1, 2, a.K1, a.T, a.K1, 64, 128));
+    if constexpr (kMode == 0) {
+        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.R_pad, a.K1, 64, C::kB1BoxRows));
+        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
+        tb1b = tb1;
+        tb2b = tb2;
+    } else if constexpr (kMode == 1) {
+        const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
+        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.k, srows, a.k, 64, 64));
+        SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.k, srows, a.k, 64, 64));
+        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.N2, a.Lk, a.N2, 64, 64));
+        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.N2, a.Lk, a.N2, 64, 64));
+    } else {
+        const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
+        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.Lk, a.K1, 64, C::kB1BoxRows));
+        SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.K1, a.Lk, a.K1, 64, C::kB1BoxRows));
+        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.k, srows, a.k, 64, C::kB2Rows));
+        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.k, srows, a.k, 64, C::kB2Rows));
+    }
     SKL_TRY(make_tmap(&ty, a.out, 2, a.N2, a.T, a.ldo, 64, 128));
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
-    auto kern = dev::b2b_kernel<kCG>;
+    auto kern = dev::b2b_kernel<kCG, kMode>;
     static bool attr_set = false;
     if (!attr_set) {
         SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -200,27 +223,44 @@ skl_status run_b2b_cg(const char* name, const void* a1, const void* b1, const vo
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ProfScope ps_(name, st);
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, ty, a));
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, a));
     return SKL_OK;
 }
 
-int g_b2b_cg = 1;  // CTA-group width of the fused kernel (SKL_B2B_CG env overrides)
+int g_b2b_cg = 2;       // CTA-group width of the fused kernel (SKL_B2B_CG=1 forces single-CTA MMAs)
+int g_b2b_direct = 1;   // read the ABI stacks directly when k % 64 == 0 (SKL_B2B_PACKED=1 disables)
 
-skl_status run_b2b(const char* name, int kind, const void* a1, const void* b1, const void* b2, B2BArgs a, int sms,
-                   cudaStream_t st) {
+skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     if (kind != 0) return fail(SKL_ERR_UNSUPPORTED, "fused kernel is bf16-only");
-    static std::once_flag once;
-    std::call_once(once, [] {
-        const char* e = getenv("SKL_B2B_CG");
-        if (e && atoi(e) == 2) g_b2b_cg = 2;
-    });
     static const int dbg = [] {
         const char* e = getenv("SKL_B2B_DEBUG");
         return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
-    if (g_b2b_cg == 2) return run_b2b_cg<2>(name, a1, b1, b2, a, sms, st);
-    return run_b2b_cg<1>(name, a1, b1, b2, a, sms, st);
+    if (g_b2b_cg == 2) {
+        if (mode == 1) return run_b2b_cg<2, 1>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0>(name, src, a, sms, st);
+    }
+    if (mode == 1) return run_b2b_cg<1, 1>(name, src, a, sms, st);
+    if (mode == 2) return run_b2b_cg<1, 2>(name, src, a, sms, st);
+    return run_b2b_cg<1, 0>(name, src, a, sms, st);
+}
+
+void read_b2b_env() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* e = getenv("SKL_B2B_CG");
+        if (e && atoi(e) == 1) g_b2b_cg = 1;
+        e = getenv("SKL_B2B_PACKED");
+        if (e && atoi(e) != 0) g_b2b_direct = 0;
+    });
+}
+
+// Direct (pack-free) operand streaming needs 64-wide rank blocks inside one term.
+bool direct_ok(const SklDims& d, skl_dtype t) {
+    read_b2b_env();
+    return g_b2b_direct && t == SKL_BF16 && d.k % 64 == 0 && d.R_pad == d.R;
 }
 
 int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
@@ -436,11 +476,13 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     void* acatT = at<void>(workspace, p.acatT);
     void* bcatT = at<void>(workspace, p.bcatT);
     float* bias32 = at<float>(workspace, p.bias32);
-    SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, bcatT, bias, bias32, st));
     (void)acat;
     (void)bcat;
+    const bool fused = use_fused(d, s->dtype);
+    const bool direct = fused && direct_ok(d, s->dtype);
+    if (!direct) SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, bcatT, bias, bias32, st));
 
-    if (use_fused(d, s->dtype)) {
+    if (fused) {
         B2BArgs a = {};
         a.T = (int)T;
         a.K1 = (int)d.d_in;
@@ -448,14 +490,20 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
         a.R_pad = (int)d.R_pad;
         a.N2 = (int)d.d_out;
         a.alpha = inv;
-        a.bias = bias32;
+        a.bias = direct ? reinterpret_cast<const float*>(bias) : bias32;
+        a.bias_bf16 = direct ? 1 : 0;
         a.out = y;
         a.ldo = d.d_out;
         a.save = saved_proj;
         a.save_col0 = 0;
         a.save_cols = (int)d.Lk;
         a.ld_save = d.Lk;
-        return run_b2b("b2b_fwd", s->dtype == SKL_BF16 ? 0 : 1, x, acatT, bcatT, a, di.sms, st);
+        a.Lk = (int)d.Lk;
+        a.k = (int)d.k;
+        a.dS = (int)d.d_in;
+        if (direct) return run_b2b("b2b_fwd", 0, 1, B2BSrc{x, S1s, U2s, U1s, S2s}, a, di.sms, st);
+        return run_b2b("b2b_fwd", s->dtype == SKL_BF16 ? 0 : 1, 0, B2BSrc{x, acatT, nullptr, bcatT, nullptr}, a,
+                       di.sms, st);
     }
 
     // Unfused fallback: H through HBM.
@@ -521,8 +569,10 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     void* acatT = at<void>(workspace, p.acatT);
     void* P = at<void>(workspace, p.inter);
     float* part = at<float>(workspace, p.part);
-    SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, nullptr,
-                          nullptr, st));
+    const bool bwd_direct = use_fused(d, s->dtype) && grad_x != nullptr && direct_ok(d, s->dtype);
+    if (!bwd_direct || !saved_proj)
+        SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, nullptr,
+                              nullptr, st));
 
     // Saved projection x·S1 (recomputed only when the caller did not keep it).
     const void* saved = saved_proj;
@@ -556,7 +606,13 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         a.save_col0 = (int)d.Lk;
         a.save_cols = (int)d.Lk;
         a.ld_save = d.R_pad;
-        SKL_TRY(run_b2b("b2b_bwd", bf16 ? 0 : 1, grad_y, bcat, acat, a, di.sms, st));
+        a.Lk = (int)d.Lk;
+        a.k = (int)d.k;
+        a.dS = (int)d.d_in;
+        if (bwd_direct)
+            SKL_TRY(run_b2b("b2b_bwd", 0, 2, B2BSrc{grad_y, U1s, S2s, S1s, U2s}, a, di.sms, st));
+        else
+            SKL_TRY(run_b2b("b2b_bwd", bf16 ? 0 : 1, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
     } else {
         GemmArgs g = {};
         g.alpha = 1.f;
