@@ -24,7 +24,8 @@
 // Chunk 1 and the GEMM2 slots share [256, 512); chunk 1 therefore acquires
 // both slots from the slot ring and releases them once converted.
 //
-// Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..7 epilogue.
+// Warp roles: 0 TMA producer, 1 MMA issuer, 2 TMEM allocator, 4..11 epilogue
+// (two warpgroups splitting the columns of every tile).
 // kCG == 2 runs cta_group::2 (M = 256 tokens per CTA pair, each CTA keeps
 // its 128 rows of H in its own TMEM, B operands are split across the pair).
 #pragma once
@@ -72,15 +73,40 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-template <int kCG>
+// Per-CTA cycle accounting for perf analysis (SKL_B2B_DEBUG bit 32):
+// [0] MMA waits on GEMM1 stages, [1] on GEMM2 stages, [2] on TMEM slots,
+// [3] on bf16-H readiness, [4] MMA loop total, [5] producer waits (GEMM1),
+// [6] producer waits (GEMM2), [7] producer total.
+__device__ unsigned long long g_b2b_prof[296][8];
+// Epilogue (warp 4 lane 0): [0] waits on GEMM2 accumulators, [1] bulk-store
+// buffer reuse, [2]/[3] epilogue named barriers, [4] waits on GEMM1 chunks,
+// [5] epilogue total.
+__device__ unsigned long long g_b2b_eprof[296][8];
+#define SKL_TIMED(slot, call)                                                  \
+    do {                                                                       \
+        if (args.dbg & 32) {                                                   \
+            const long long t0_ = clock64();                                   \
+            call;                                                              \
+            prof[slot] += (unsigned long long)(clock64() - t0_);               \
+        } else {                                                               \
+            call;                                                              \
+        }                                                                      \
+    } while (0)
+
+template <int kCG, int kMode>
 struct B2BCfg {
     static constexpr int kStageBytes = kCG == 1 ? 48 * 1024 : 32 * 1024;
-    static constexpr int kStages = kCG == 1 ? 4 : 6;
+    // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
+    // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
+    static constexpr int kBiasTabBytes = kMode == 1 ? 32 * 1024 : 0;
+    static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
+    static constexpr int kStages = (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0);
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
-    static constexpr int kSmem = kStages * kStageBytes + 2 * 16384 + 1024 /*bias*/ + 1024 /*align*/ + 256;
+    static constexpr int kSmem =
+        kStages * kStageBytes + 2 * 16384 + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 256;
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -91,17 +117,18 @@ struct B2BCfg {
 // kMode 2: backward straight from the stacks: B1 = U1s|S2s [L*k][d_out]
 //          (K-major), B2 = S1s|U2s [L*d_in][k] (K-major, per-term row offset).
 template <int kCG, int kMode>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
-    using C = B2BCfg<kCG>;
+    using C = B2BCfg<kCG, kMode>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
     uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 2 x 16 KB output staging
     float* bias_s = reinterpret_cast<float*>(stage_out + 2 * 16384);  // 2 slots x 128 bias values
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * 16384 + 1024);
+    float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * 16384 + 1024);  // kMode 1: bias[N2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * 16384 + 1024 + C::kBiasTabBytes);
     uint64_t* full = bars;                            // [kStages]
     uint64_t* empty = bars + C::kStages;              // [kStages]
     uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
@@ -129,9 +156,9 @@ __global__ void __launch_bounds__(256, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&tfull1[i], 1);
-            mbar_init(&hready[i], 4 * kCG);
+            mbar_init(&hready[i], 8 * kCG);   // 8 epilogue warps per CTA
             mbar_init(&tfull2[i], 1);
-            mbar_init(&tempty2[i], 4 * kCG);
+            mbar_init(&tempty2[i], 8 * kCG);
         }
         fence_barrier_init();
     }
@@ -159,6 +186,8 @@ __global__ void __launch_bounds__(256, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const long long tp0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             for (int t = cluster_id; t < num_tiles; t += num_clusters) {
                 const int am = t * tile_rows + (int)rank * 128;
@@ -168,7 +197,7 @@ __global__ void __launch_bounds__(256, 1)
                     const int b0 = 256 * c + (int)rank * brows;
                     const uint32_t bytes = 16384 + brows * 128;
                     for (int kb = 0; kb < nkb1; ++kb) {
-                        mbar_wait(&empty[stage], phase ^ 1);
+                        SKL_TIMED(5, mbar_wait(&empty[stage], phase ^ 1));
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
@@ -198,7 +227,7 @@ __global__ void __launch_bounds__(256, 1)
                     for (int s = 0; s < nst2; ++s) {
                         const int kb0 = s * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
-                        mbar_wait(&empty[stage], phase ^ 1);
+                        SKL_TIMED(6, mbar_wait(&empty[stage], phase ^ 1));
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
                         else mbar_arrive_cluster(&full[stage], 0);
@@ -221,12 +250,18 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
             }
+            if (args.dbg & 32) {
+                prof[7] = (unsigned long long)(clock64() - tp0);
+                for (int i = 5; i < 8; ++i) g_b2b_prof[blockIdx.x][i] = prof[i];
+            }
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer
         if (leader && elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            const long long tm0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             uint32_t slot_seq = 0;
             const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
@@ -237,13 +272,13 @@ __global__ void __launch_bounds__(256, 1)
                     const int wc = min(256, args.R_pad - 256 * c);
                     if (c == 1) {  // chunk 1 overlays both GEMM2 slots
                         for (int u = 0; u < 2; ++u, ++slot_seq)
-                            mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1);
+                            SKL_TIMED(2, mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1));
                         tc_fence_after();
                     }
                     const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
                     const uint32_t d = tmem_base + 256 * c;
                     for (int kb = 0; kb < nkb1; ++kb) {
-                        mbar_wait(&full[stage], phase);
+                        SKL_TIMED(0, mbar_wait(&full[stage], phase));
                         tc_fence_after();
                         const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
                         const uint32_t b_addr = a_addr + 16384;
@@ -259,18 +294,18 @@ __global__ void __launch_bounds__(256, 1)
                     mma_commit<kCG>(&tfull1[c]);
                 }
                 // ---- wait for the bf16 H of this tile (both CTAs)
-                for (int c = 0; c < nch; ++c) mbar_wait(&hready[c], it & 1);
+                for (int c = 0; c < nch; ++c) SKL_TIMED(3, mbar_wait(&hready[c], it & 1));
                 tc_fence_after();
                 // ---- GEMM2: 128-wide output tiles, A = H from TMEM
                 for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                     const uint32_t s = slot_seq & 1;
-                    mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1);
+                    SKL_TIMED(2, mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1));
                     tc_fence_after();
                     const uint32_t d = tmem_base + 256 + 128 * s;
                     for (int st2 = 0; st2 < nst2; ++st2) {
                         const int kb0 = st2 * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
-                        mbar_wait(&full[stage], phase);
+                        SKL_TIMED(1, mbar_wait(&full[stage], phase));
                         tc_fence_after();
                         const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int q = 0; q < nk; ++q) {
@@ -290,147 +325,184 @@ __global__ void __launch_bounds__(256, 1)
                     mma_commit<kCG>(&tfull2[s]);
                 }
             }
+            if (args.dbg & 32) {
+                prof[4] = (unsigned long long)(clock64() - tm0);
+                for (int i = 0; i < 5; ++i) g_b2b_prof[blockIdx.x][i] = prof[i];
+            }
         }
     } else if (warp >= 4) {
         // ---------------------------------------------------------------- epilogue
+        // Two warpgroups (warps 4-7, 8-11).  A warp may only touch its TMEM lane
+        // quarter (warp % 4), so both groups cover all 128 rows and split the
+        // columns: group wg converts / stores columns [wg*W/2, (wg+1)*W/2) of
+        // every GEMM1 chunk and GEMM2 tile.
         const uint32_t q = warp & 3;
+        const uint32_t wg = (warp - 4) >> 2;
         const uint32_t lane = lane_id();
         const uint32_t lane_base = (q * 32u) << 16;
+        const uint32_t srow = q * 32 + lane;  // TMEM lane == tile row
         uint32_t slot_seq = 0;
         uint32_t tf_par0 = 0, tf_par1 = 0;
-        uint32_t sbuf = 0;                       // output staging buffer toggle
-        const bool issuer = (q == 0 && lane == 0);  // issues / waits the bulk stores
+        const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
+        uint8_t* buf = stage_out + wg * 16384;        // this group's output staging buffer
+        float* bias_g = bias_s + wg * 128;            // [2 slots][64]
+        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SKL_B2B_DEBUG & 32
+        const long long te0 = clock64();
+        auto load_bias_col = [&](int col) -> float {
+            if (args.bias == nullptr || col >= args.N2) return 0.f;
+            return args.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[col])
+                                  : __ldg(args.bias + col);
+        };
+        float bias_pref = 0.f;
+        if constexpr (kMode == 1) {
+            // whole bias resident in smem for the kernel's lifetime
+            const int tid = (int)((warp - 4) * 32 + lane);
+            for (int i = tid; i < args.N2; i += 256) bias_tab[i] = load_bias_col(i);
+            named_bar_sync(3, 256);
+        } else {
+            bias_pref = load_bias_col((int)(wg * 64 + (srow & 63)));  // tile j = 0
+        }
+        const float alpha = args.alpha;
+        auto arrive_leader = [&](uint64_t* bar) {
+            if (leader) mbar_arrive(bar);
+            else mbar_arrive_cluster(bar, 0);
+        };
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
-            const int row = t * tile_rows + (int)rank * 128 + (int)(q * 32 + lane);
+            const int row = t * tile_rows + (int)rank * 128 + (int)srow;
             const bool row_ok = row < args.T;
             // ---- convert GEMM1 chunks: fp32 -> bf16 H in TMEM (+ saved columns)
             for (int c = 0; c < nch; ++c) {
                 const int wc = min(256, args.R_pad - 256 * c);
-                mbar_wait(&tfull1[c], it & 1);
+                // In-place fp32 -> bf16 compaction, split over both warpgroups in
+                // two rounds of quarter-chunks (W = wc/4 columns each).  Quarter qi
+                // lands in fp32 columns [qi*W/2, (qi+1)*W/2), i.e. inside quarters
+                // 0/1, so round 0 reads Q0,Q1 before anyone writes (barrier), and
+                // round 1's writes only hit Q1, which round 0 already consumed.
+                const int W = wc / 4;
+                SKL_TIMED(4, mbar_wait(&tfull1[c], it & 1));
                 tc_fence_after();
+                const long long tc0 = clock64();
 #pragma unroll 1
-                for (int g2 = 0; g2 < wc / 32; ++g2) {
-                  uint32_t rr[2][16];
-                  tmem_ld16(tmem_base + lane_base + 256 * c + 32 * g2, rr[0]);
-                  tmem_ld16(tmem_base + lane_base + 256 * c + 32 * g2 + 16, rr[1]);
-                  tmem_ld_wait();
+                for (int rd = 0; rd < 2; ++rd) {
+                    const int qi = 2 * rd + (int)wg;
+                    uint32_t rr[4][16];
 #pragma unroll
-                  for (int hh = 0; hh < 2; ++hh) {
-                    const int g = 2 * g2 + hh;
-                    const uint32_t (&r)[16] = rr[hh];
-                    uint32_t p[8];
+                    for (int g = 0; g < 4; ++g)
+                        if (16 * g < W) tmem_ld16(tmem_base + lane_base + 256 * c + qi * W + 16 * g, rr[g]);
+                    tmem_ld_wait();
+                    if (rd == 0) {
+                        tc_fence_before();
+                        named_bar_sync(3, 256);  // both groups hold Q0/Q1 in registers
+                        tc_fence_after();
+                    }
 #pragma unroll
-                    for (int i = 0; i < 8; ++i) p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
-                    tmem_st8(tmem_base + lane_base + 128 * c + 8 * g, p);
-                    const int col = 256 * c + 16 * g;  // H column (R order)
-                    if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
-                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) +
-                                             (long long)row * args.ld_save + (col - args.save_col0);
-                        if (col >= args.save_col0 && col + 16 <= args.save_col0 + args.save_cols &&
-                            (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                            reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-                            reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
-                        } else {
-                            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
-                            for (int i = 0; i < 16; ++i)
-                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
-                                    dst[i] = pb[i];
+                    for (int g = 0; g < 4; ++g) {
+                        if (16 * g >= W) break;
+                        const uint32_t(&r)[16] = rr[g];
+                        uint32_t p[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i)
+                            p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
+                        const int cl = qi * W + 16 * g;  // chunk-local fp32 column
+                        tmem_st8(tmem_base + lane_base + 128 * c + cl / 2, p);
+                        const int col = 256 * c + cl;  // H column (R order)
+                        if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
+                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) +
+                                                 (long long)row * args.ld_save + (col - args.save_col0);
+                            if (col >= args.save_col0 && col + 16 <= args.save_col0 + args.save_cols &&
+                                (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                                reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
+                                reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
+                            } else {
+                                const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
+                                for (int i = 0; i < 16; ++i)
+                                    if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
+                                        dst[i] = pb[i];
+                            }
                         }
                     }
-                  }
                 }
                 tmem_st_wait();
+                if (args.dbg & 32) prof[6] += (unsigned long long)(clock64() - tc0);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    if (leader) mbar_arrive(&hready[c]);
-                    else mbar_arrive_cluster(&hready[c], 0);
+                    arrive_leader(&hready[c]);
                     if (c == 1) {  // release the two slots chunk 1 overlaid
-                        for (int u = 0; u < 2; ++u) {
-                            const uint32_t s = (slot_seq + u) & 1;
-                            if (leader) mbar_arrive(&tempty2[s]);
-                            else mbar_arrive_cluster(&tempty2[s], 0);
-                        }
+                        arrive_leader(&tempty2[slot_seq & 1]);
+                        arrive_leader(&tempty2[(slot_seq + 1) & 1]);
                     }
                 }
                 if (c == 1) slot_seq += 2;
             }
-            // ---- GEMM2 output tiles
+            // ---- GEMM2 output tiles: this group's 64 columns of every 128-wide tile
             for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                 const uint32_t s = slot_seq & 1;
-                const uint32_t srow = q * 32 + lane;
-                // The tile's 128 bias values go through shared memory: with
-                // ~226 KB of smem in use L1 is tiny, so per-thread global bias
-                // loads would each pay L2 latency inside the epilogue.
-                const int bcol = j * 128 + (int)srow;
+                // Bias through smem (L1 is tiny with ~226 KB of smem in use);
+                // software-pipelined: this tile's value was loaded one tile ago.
                 float bval = 0.f;
-                if (args.bias != nullptr && bcol < args.N2)
-                    bval = args.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[bcol])
-                                          : __ldg(args.bias + bcol);
+                if constexpr (kMode != 1) {
+                    bval = bias_pref;
+                    bias_pref = load_bias_col((j + 1 == n2_tiles ? 0 : j + 1) * 128 + (int)(wg * 64 + (srow & 63)));
+                }
                 // tfull2[s] completes once per GEMM2 job on slot s (chunk-1
                 // acquisitions never commit it), so count its phases per slot.
-                mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
+                SKL_TIMED(0, mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0));
                 if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
                 tc_fence_after();
-                bias_s[s * 128 + srow] = bval;  // published by the named barrier below
-                // Two 64-column halves per tile: TMEM -> alpha*acc + b -> bf16 ->
-                // 128B-swizzled smem staging buffer -> one TMA bulk store each
-                // (coalesced, clipped at T / N2 by the tensor map).
+                if (kMode != 1 && srow < 64) bias_g[s * 64 + srow] = bval;  // published by the barrier below
                 if (args.dbg & 1) {  // perf bisection: release the slot without reading it
                     tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) {
-                        if (leader) mbar_arrive(&tempty2[s]);
-                        else mbar_arrive_cluster(&tempty2[s], 0);
-                    }
+                    if (lane == 0) arrive_leader(&tempty2[s]);
                     continue;
                 }
-#pragma unroll 1
-                for (int h = 0; h < 2; ++h) {
-                    uint32_t ra[32], rb[32];
-                    tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * h, ra);
-                    tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * h + 32, rb);
-                    tmem_ld_wait();
-                    if (h == 1) {  // every TMEM read of this slot has completed
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) {
-                            if (leader) mbar_arrive(&tempty2[s]);
-                            else mbar_arrive_cluster(&tempty2[s], 0);
-                        }
-                    }
-                    const int n0 = j * 128 + 64 * h;
-                    if (args.dbg & 16) continue;  // perf bisection: TMEM reads only
-                    uint8_t* buf = stage_out + sbuf * 16384;
-                    if (issuer) bulk_wait_read<1>();  // the store that used `buf` has read it
-                    named_bar_sync(1, 128);
-                    const uint32_t row_addr = smem_u32(buf) + srow * 128;
+                uint32_t ra[32], rb[32];
+                const long long tl0 = clock64();
+                tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg, ra);
+                tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg + 32, rb);
+                tmem_ld_wait();
+                if (args.dbg & 32) prof[7] += (unsigned long long)(clock64() - tl0);
+                // every TMEM read of this slot by this warp has completed
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) arrive_leader(&tempty2[s]);
+                if (args.dbg & 16) continue;  // perf bisection: TMEM reads only
+                const int n0 = j * 128 + 64 * (int)wg;
+                if (issuer) SKL_TIMED(2, bulk_wait_read<0>());  // our previous store has read `buf`
+                SKL_TIMED(3, named_bar_sync(1 + wg, 128));
+                const uint32_t row_addr = smem_u32(buf) + srow * 128;
+                const long long tm0 = clock64();
 #pragma unroll
-                    for (int c = 0; c < 8; ++c) {
-                        const float4* bp = reinterpret_cast<const float4*>(bias_s + s * 128 + 64 * h + 8 * c);
-                        const float4 b0 = bp[0], b1 = bp[1];
-                        const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
-                        const uint32_t* src = (c < 4) ? ra : rb;
-                        const int o = (c & 3) * 8;
-                        uint32_t w[4];
+                for (int c = 0; c < 8; ++c) {
+                    const float4* bp = kMode == 1 ? reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)
+                                                  : reinterpret_cast<const float4*>(bias_g + s * 64 + 8 * c);
+                    const float4 b0 = bp[0], b1 = bp[1];
+                    const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    const uint32_t* src = (c < 4) ? ra : rb;
+                    const int o = (c & 3) * 8;
+                    uint32_t w[4];
 #pragma unroll
-                        for (int i = 0; i < 4; ++i)
-                            w[i] = pack_bf16x2(fmaf(__uint_as_float(src[o + 2 * i]), args.alpha, bv[2 * i]),
-                                               fmaf(__uint_as_float(src[o + 2 * i + 1]), args.alpha, bv[2 * i + 1]));
-                        st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
-                    }
-                    fence_proxy_async_smem();
-                    named_bar_sync(1, 128);
-                    if (issuer && !(args.dbg & 8)) {
-                        tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
-                        bulk_commit();
-                    }
-                    sbuf ^= 1;
+                    for (int i = 0; i < 4; ++i)
+                        w[i] = pack_bf16x2(fmaf(__uint_as_float(src[o + 2 * i]), alpha, bv[2 * i]),
+                                           fmaf(__uint_as_float(src[o + 2 * i + 1]), alpha, bv[2 * i + 1]));
+                    st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
+                }
+                fence_proxy_async_smem();
+                if (args.dbg & 32) prof[1] += (unsigned long long)(clock64() - tm0);
+                named_bar_sync(1 + wg, 128);
+                if (issuer && !(args.dbg & 8)) {
+                    tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
+                    bulk_commit();
                 }
             }
         }
         if (issuer) bulk_wait<0>();
+        if ((args.dbg & 32) && issuer && wg == 0) {
+            prof[5] = (unsigned long long)(clock64() - te0);
+            for (int i = 0; i < 8; ++i) g_b2b_eprof[blockIdx.x][i] = prof[i];
+        }
     }
 
     tc_fence_before();

@@ -180,7 +180,7 @@ struct B2BSrc {
 
 template <int kCG, int kMode>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG>;
+    using C = dev::B2BCfg<kCG, kMode>;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty;
     SKL_TRY(make_tmap(&ta, src.a1, 2, a.K1, a.T, a.K1, 64, 128));
     if constexpr (kMode == 0) {
@@ -203,6 +203,11 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     }
     SKL_TRY(make_tmap(&ty, a.out, 2, a.N2, a.T, a.ldo, 64, 128));
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
+    static const int grid_cap = [] {  // SKL_B2B_GRID: cap on CTAs (experiments)
+        const char* e = getenv("SKL_B2B_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    if (grid_cap > 0) sms = std::min(sms, grid_cap);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
     auto kern = dev::b2b_kernel<kCG, kMode>;
     static bool attr_set = false;
@@ -212,7 +217,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(384);  // 4 control warps + 2 epilogue warpgroups
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
@@ -260,7 +265,8 @@ void read_b2b_env() {
 // Direct (pack-free) operand streaming needs 64-wide rank blocks inside one term.
 bool direct_ok(const SklDims& d, skl_dtype t) {
     read_b2b_env();
-    return g_b2b_direct && t == SKL_BF16 && d.k % 64 == 0 && d.R_pad == d.R;
+    return g_b2b_direct && t == SKL_BF16 && d.k % 64 == 0 && d.R_pad == d.R &&
+           d.d_out <= dev::B2BCfg<2, 1>::kMaxBiasTab;
 }
 
 int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
@@ -750,3 +756,20 @@ skl_status skl_allreduce_grads(void* nccl_comm, float* grad_bucket, size_t count
 }
 
 }  // extern "C"
+
+// Perf-analysis hook (not part of skl.h): per-CTA cycle counters of the last
+// fused-kernel launch run with SKL_B2B_DEBUG bit 32.
+extern "C" int skl_debug_b2b_prof(unsigned long long* out, int n) {
+    const int total = 296 * 8;
+    if (n > total) n = total;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_prof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
+extern "C" int skl_debug_b2b_eprof(unsigned long long* out, int n) {
+    const int total = 296 * 8;
+    if (n > total) n = total;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_eprof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
