@@ -44,6 +44,9 @@ struct B2BArgs {
     int save_col0, save_cols;
     int Lk, k, dS;      // direct modes: L*k, k, and the term row stride of the [L*d][k] views
     int bias_bf16;      // bias pointer holds bf16 (direct modes skip the fp32 copy)
+    int b2tall;         // kMode 1: B2 maps use {64, 64*kKbPerStage2} boxes (one load per stage)
+    int b1rows;         // rows per K-major B1 TMA box (largest that tiles every chunk; big boxes
+                        // matter: per-SM TMA ingest grows ~2.5x from 4 KB to 16 KB boxes)
     int dbg;            // perf-bisection switches (SKL_B2B_DEBUG): 1 skip GEMM2 epilogue math/stores, 4 skip GEMM2 MMAs
     long long ld_save;
 };
@@ -95,12 +98,16 @@ __device__ unsigned long long g_b2b_eprof[296][8];
 
 template <int kCG, int kMode>
 struct B2BCfg {
-    static constexpr int kStageBytes = kCG == 1 ? 48 * 1024 : 32 * 1024;
+    // The backward's GEMM1 (K = d_out, 80% of its MMAs) runs single-pass: one
+    // A1 tile feeds both 256-wide chunks, so G is read once instead of twice;
+    // its stages therefore hold A1 + B1 for all of R (48 KB).
+    static constexpr bool kSinglePassG1 = kMode == 2 && kCG == 2;
+    static constexpr int kStageBytes = (kCG == 1 || kSinglePassG1) ? 48 * 1024 : 32 * 1024;
     // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
     static constexpr int kBiasTabBytes = kMode == 1 ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages = (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0);
+    static constexpr int kStages = kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0);
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
@@ -191,32 +198,40 @@ __global__ void __launch_bounds__(384, 1)
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             for (int t = cluster_id; t < num_tiles; t += num_clusters) {
                 const int am = t * tile_rows + (int)rank * 128;
-                for (int c = 0; c < nch; ++c) {
-                    const int wc = min(256, args.R_pad - 256 * c);
-                    const int brows = wc / kCG;
-                    const int b0 = 256 * c + (int)rank * brows;
-                    const uint32_t bytes = 16384 + brows * 128;
+                // GEMM1 passes: one per chunk, or (single-pass mode) one pass that
+                // feeds every chunk from the same A1 stage -> A1 is read once.
+                const int npass = C::kSinglePassG1 ? 1 : nch;
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int c_lo = C::kSinglePassG1 ? 0 : pass, c_hi = C::kSinglePassG1 ? nch : pass + 1;
+                    uint32_t bytes = 16384;
+                    for (int c = c_lo; c < c_hi; ++c) bytes += (min(256, args.R_pad - 256 * c) / kCG) * 128;
                     for (int kb = 0; kb < nkb1; ++kb) {
                         SKL_TIMED(5, mbar_wait(&empty[stage], phase ^ 1));
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
                         tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * 64, am);
-                        if constexpr (kMode == 0) {
-                            for (int r = 0; r < brows; r += C::kB1BoxRows)
-                                tma_load_2d<kCG>(&tmB1, &full[stage], st + 16384 + r * 128, kb * 64, b0 + r);
-                        } else if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
-                            for (int r = 0; r < brows; r += C::kB1BoxRows) {
-                                const int rg = b0 + r;
-                                tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], st + 16384 + r * 128, kb * 64,
-                                                 rg < args.Lk ? rg : rg - args.Lk);
-                            }
-                        } else {  // MN-major [64 d_in rows x 64 rank cols] blocks of S1s | U2s
-                            for (int jb = 0; jb < brows / 64; ++jb) {
-                                const int rg = b0 + 64 * jb;
-                                const int rr = rg < args.Lk ? rg : rg - args.Lk;
-                                tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], st + 16384 + jb * 8192,
-                                                 rr % args.k, (rr / args.k) * args.dS + kb * 64);
+                        for (int c = c_lo; c < c_hi; ++c) {
+                            const int wc = min(256, args.R_pad - 256 * c);
+                            const int brows = wc / kCG;
+                            const int b0 = 256 * c + (int)rank * brows;
+                            uint8_t* bst = st + 16384 + (c - c_lo) * (256 / kCG) * 128;
+                            if constexpr (kMode == 0) {
+                                for (int r = 0; r < brows; r += args.b1rows)
+                                    tma_load_2d<kCG>(&tmB1, &full[stage], bst + r * 128, kb * 64, b0 + r);
+                            } else if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
+                                for (int r = 0; r < brows; r += args.b1rows) {
+                                    const int rg = b0 + r;
+                                    tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + r * 128, kb * 64,
+                                                     rg < args.Lk ? rg : rg - args.Lk);
+                                }
+                            } else {  // MN-major [64 d_in rows x 64 rank cols] blocks of S1s | U2s
+                                for (int jb = 0; jb < brows / 64; ++jb) {
+                                    const int rg = b0 + 64 * jb;
+                                    const int rr = rg < args.Lk ? rg : rg - args.Lk;
+                                    tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + jb * 8192,
+                                                     rr % args.k, (rr / args.k) * args.dS + kb * 64);
+                                }
                             }
                         }
                         next();
@@ -231,6 +246,15 @@ __global__ void __launch_bounds__(384, 1)
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
                         else mbar_arrive_cluster(&full[stage], 0);
+                        if (kMode == 1 && args.b2tall) {
+                            // whole stage (kKbPerStage2 k-blocks, one source half) in one
+                            // {64 x 64*kKbPerStage2} box; layouts coincide for 64-wide N.
+                            const int r0 = kb0 * 64;
+                            tma_load_2d<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st, brow,
+                                             r0 < args.Lk ? r0 : r0 - args.Lk);
+                            next();
+                            continue;
+                        }
                         for (int q = 0; q < nk; ++q) {
                             const int r0 = (kb0 + q) * 64;  // rank index of this k-block
                             if constexpr (kMode == 0) {
@@ -267,31 +291,35 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
             int it = 0;
             for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
-                // ---- GEMM1: H chunks
-                for (int c = 0; c < nch; ++c) {
-                    const int wc = min(256, args.R_pad - 256 * c);
-                    if (c == 1) {  // chunk 1 overlays both GEMM2 slots
+                // ---- GEMM1: H chunks (one pass per chunk, or one pass for all)
+                const int npass = C::kSinglePassG1 ? 1 : nch;
+                for (int pass = 0; pass < npass; ++pass) {
+                    const int c_lo = C::kSinglePassG1 ? 0 : pass, c_hi = C::kSinglePassG1 ? nch : pass + 1;
+                    if (c_hi > 1 && c_lo <= 1) {  // chunk 1 overlays both GEMM2 slots
                         for (int u = 0; u < 2; ++u, ++slot_seq)
                             SKL_TIMED(2, mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1));
                         tc_fence_after();
                     }
-                    const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
-                    const uint32_t d = tmem_base + 256 * c;
                     for (int kb = 0; kb < nkb1; ++kb) {
                         SKL_TIMED(0, mbar_wait(&full[stage], phase));
                         tc_fence_after();
                         const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
-                        const uint32_t b_addr = a_addr + 16384;
+                        for (int c = c_lo; c < c_hi; ++c) {
+                            const int wc = min(256, args.R_pad - 256 * c);
+                            const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
+                            const uint32_t d = tmem_base + 256 * c;
+                            const uint32_t b_addr = a_addr + 16384 + (c - c_lo) * (256 / kCG) * 128;
 #pragma unroll
-                        for (int k = 0; k < 4; ++k)
-                            mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024),
-                                           kMode == 1 ? make_sdesc(b_addr + k * 2048, 8192, 1024)
-                                                      : make_sdesc(b_addr + k * 32, 0, 1024),
-                                           idesc1, (kb > 0 || k > 0) ? 1u : 0u);
+                            for (int k = 0; k < 4; ++k)
+                                mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024),
+                                               kMode == 1 ? make_sdesc(b_addr + k * 2048, 8192, 1024)
+                                                          : make_sdesc(b_addr + k * 32, 0, 1024),
+                                               idesc1, (kb > 0 || k > 0) ? 1u : 0u);
+                        }
                         mma_commit<kCG>(&empty[stage]);
                         next();
                     }
-                    mma_commit<kCG>(&tfull1[c]);
+                    for (int c = c_lo; c < c_hi; ++c) mma_commit<kCG>(&tfull1[c]);
                 }
                 // ---- wait for the bf16 H of this tile (both CTAs)
                 for (int c = 0; c < nch; ++c) SKL_TIMED(3, mbar_wait(&hready[c], it & 1));

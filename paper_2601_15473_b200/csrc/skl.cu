@@ -184,7 +184,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty;
     SKL_TRY(make_tmap(&ta, src.a1, 2, a.K1, a.T, a.K1, 64, 128));
     if constexpr (kMode == 0) {
-        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.R_pad, a.K1, 64, C::kB1BoxRows));
+        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.R_pad, a.K1, 64, a.b1rows));
         SKL_TRY(make_tmap(&tb2, src.b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
         tb1b = tb1;
         tb2b = tb2;
@@ -192,12 +192,16 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
         SKL_TRY(make_tmap(&tb1, src.b1, 2, a.k, srows, a.k, 64, 64));
         SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.k, srows, a.k, 64, 64));
-        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.N2, a.Lk, a.N2, 64, 64));
-        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.N2, a.Lk, a.N2, 64, 64));
+        const int tall = 64 * C::kKbPerStage2;
+        // Measured slower than per-k-block boxes for the c2 forward; opt-in only.
+        static const bool tall_on = getenv("SKL_B2B_TALL") && atoi(getenv("SKL_B2B_TALL")) != 0;
+        a.b2tall = (tall_on && kCG == 2 && a.Lk % tall == 0 && a.R_pad % tall == 0 && tall <= 256) ? 1 : 0;
+        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.N2, a.Lk, a.N2, 64, a.b2tall ? tall : 64));
+        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.N2, a.Lk, a.N2, 64, a.b2tall ? tall : 64));
     } else {
         const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
-        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.Lk, a.K1, 64, C::kB1BoxRows));
-        SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.K1, a.Lk, a.K1, 64, C::kB1BoxRows));
+        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.Lk, a.K1, 64, a.b1rows));
+        SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.K1, a.Lk, a.K1, 64, a.b1rows));
         SKL_TRY(make_tmap(&tb2, src.b2, 2, a.k, srows, a.k, 64, C::kB2Rows));
         SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.k, srows, a.k, 64, C::kB2Rows));
     }
@@ -242,6 +246,17 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
+    {  // B1 box rows: largest power of two <= 128 dividing every chunk's per-CTA rows (and Lk in mode 2)
+        const int cg = g_b2b_cg;
+        int r = 128;
+        auto ok = [&](int v) {
+            for (int c = 0; c * 256 < a.R_pad; ++c)
+                if ((std::min(256, a.R_pad - 256 * c) / cg) % v) return false;
+            return mode != 2 || a.Lk % v == 0;
+        };
+        while (r > 8 && !ok(r)) r /= 2;
+        a.b1rows = r;
+    }
     if (g_b2b_cg == 2) {
         if (mode == 1) return run_b2b_cg<2, 1>(name, src, a, sms, st);
         if (mode == 2) return run_b2b_cg<2, 2>(name, src, a, sms, st);
