@@ -199,7 +199,7 @@ def main():
     X = torch.randn(T, D_IN, device=dev, generator=gen).to(bf)
     G = torch.randn(T, D_OUT, device=dev, generator=gen).to(bf)
     Y = torch.empty(T, D_OUT, dtype=bf, device=dev)
-    saved = torch.empty(T, L * K_RANK, dtype=bf, device=dev)
+    saved = torch.empty(L * K_RANK, (T + 7) // 8 * 8, dtype=bf, device=dev)  # Savedᵀ [L*k][round8(T)]
     GX = torch.empty(T, D_IN, dtype=bf, device=dev)
     n1, n2 = L * K_RANK * D_OUT, L * D_IN * K_RANK
     bucket = torch.empty(n1 + n2 + D_OUT, dtype=torch.float32, device=dev)  # dU1s | dU2s | db

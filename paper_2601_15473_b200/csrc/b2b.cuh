@@ -40,7 +40,7 @@ struct B2BArgs {
     const float* bias;  // [N2] fp32, nullable
     void* out;          // [T, N2] bf16, row stride ldo
     long long ldo;
-    void* save;         // H columns [save_col0, save_col0 + save_cols) -> save[t][c - save_col0]
+    void* save;         // H columns [save_col0, save_col0 + save_cols) -> save[c - save_col0][t] (transposed)
     int save_col0, save_cols;
     int Lk, k, dS;      // direct modes: L*k, k, and the term row stride of the [L*d][k] views
     int bias_bf16;      // bias pointer holds bf16 (direct modes skip the fp32 copy)
@@ -435,19 +435,16 @@ __global__ void __launch_bounds__(384, 1)
                         const int cl = qi * W + 16 * g;  // chunk-local fp32 column
                         tmem_st8(tmem_base + lane_base + 128 * c + cl / 2, p);
                         const int col = 256 * c + cl;  // H column (R order)
+                        // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
+                        // ld_save >= T): the token-reduction GEMMs then read them K-major.
+                        // Lanes are consecutive tokens, so each store is 64 contiguous bytes.
                         if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
-                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) +
-                                                 (long long)row * args.ld_save + (col - args.save_col0);
-                            if (col >= args.save_col0 && col + 16 <= args.save_col0 + args.save_cols &&
-                                (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                                reinterpret_cast<uint4*>(dst)[0] = make_uint4(p[0], p[1], p[2], p[3]);
-                                reinterpret_cast<uint4*>(dst)[1] = make_uint4(p[4], p[5], p[6], p[7]);
-                            } else {
-                                const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
-                                for (int i = 0; i < 16; ++i)
-                                    if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
-                                        dst[i] = pb[i];
-                            }
+                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) + row;
+                            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
+                                    dst[(long long)(col + i - args.save_col0) * args.ld_save] = pb[i];
                         }
                     }
                 }

@@ -1,23 +1,28 @@
 // du.cuh -- the fused parameter-gradient kernel of the SKLinear backward.
 //
-//   dU1s = inv · Savedᵀ · G      [L·k, d_out]          Saved = x·S1 (from the forward)
-//   dU2s = inv · Xᵀ · P_S2       [d_in, L·k] -> [L][d_in][k]   P_S2 = G·S2ᵀ (from b2b_bwd)
-//   db   = Σ_t G[t, :]                                  (nn_layers.cpp:99, unscaled)
+//   dU1s  = inv · Savedᵀ · G      [L·k, d_out]                Saved = x·S1 (forward)
+//   dU2sᵀ = inv · P_S2ᵀ · X       [L·k, d_in] -> [L][d_in][k] P_S2  = G·S2ᵀ (b2b_bwd)
+//   db    = Σ_t G[t, :]                                        (nn_layers.cpp:99, unscaled)
 //
 // Reference: SkLinear::backward grad_u1 / grad_u2 / grad_b (nn_layers.cpp:88-99).
-// All three are reductions over the T tokens.  One persistent launch covers
-// both GEMMs as a grouped problem list, split along T (split-K) so every SM
-// has work; the column sums of G ride along on the G tiles already staged in
-// shared memory for dU1 (warp 3 sums them while the tensor core consumes the
-// same stage), so G is read from HBM once for dU1 and db together.
+// All three reduce over the T tokens.  One persistent launch covers both GEMMs
+// as a grouped problem list (both have M = L·k), split along T so every CTA
+// pair has a unit.  The fused kernels wrote Saved and P_S2 TRANSPOSED
+// ([L·k][T]), so A is a K-major operand (one 16 KB TMA box per stage); G and
+// X are token-major, i.e. MN-major B tiles.  MMAs are cta_group::2 (M = 256:
+// each CTA keeps 128 rows of A and half of the 256 B columns), which halves
+// per-SM operand ingest versus one CTA per tile.
 //
-// Reduction is deterministic and in-kernel: every (tile, split) unit writes
-// its fp32 partial to the workspace; the last unit of a tile to finish (an
-// atomic ticket per tile) sums the partials in split order 0..S-1, applies
-// alpha and the output layout, and resets the ticket.  No extra launches.
+// db rides along: the column sums of G are taken by the epilogue warps from
+// the G tiles already staged in shared memory for dU1.  Because cta_group::2
+// TMA completion only reaches the leader's barrier, each CTA here loads its
+// own half with plain TMA onto its OWN full barrier, and a relay thread on
+// the peer CTA forwards completion to the leader (so both CTAs can observe
+// their own stages).
 //
-// Operands are token-major in HBM, so both A and B are MN-major UMMA tiles
-// (128B-swizzled TMA boxes of [64 tokens x 64 features]).
+// Reduction is deterministic and in-kernel: every (tile, split, rank) writes
+// its fp32 partial; with a cooperative launch all units are co-resident and
+// the 2·S CTAs of a tile each reduce a 1/(2S) slice in split order 0..S-1.
 #pragma once
 
 #include "sm100.cuh"
@@ -26,31 +31,31 @@ namespace skl {
 
 struct DuProblem {
     int M, N;             // output is M x N
-    int m_tiles, n_tiles;  // 128 x 256 tiles
+    int m_tiles, n_tiles;  // 256 x 256 pair tiles
     int tile0;            // first global tile index of this problem
     int colsum;           // 1: also sum the B operand over K (db)
     float alpha;
-    float* out;           // out[(n / nb) * blk + m * ldm + n % nb]
-    long long nb, blk, ldm;
+    float* out;           // out[(m / mb) * mbs + (m % mb) * ms + n * ns]
+    long long mb, mbs, ms, ns;
     float* db;            // [N] when colsum
 };
 
 struct DuArgs {
     int k_blocks, splits, num_tiles;
     DuProblem p[2];
-    float* part;     // [num_tiles][splits][128][256]
+    float* part;     // [num_tiles][splits][256][256]
     float* cpart;    // [p0.n_tiles][splits][256]
     int* tickets;    // [num_tiles], zero on entry, left zero on exit
-    int coop;        // 1: cooperative launch (all units co-resident) -> split-parallel reduction
+    int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
 };
 
 namespace dev {
 
-constexpr int kDuBM = 128, kDuBN = 256, kDuBK = 64, kDuStages = 4;
-constexpr int kDuABytes = kDuBM * 128;   // 2 blocks of [64 rows x 128 B]
-constexpr int kDuBBytes = kDuBN * 128;   // 4 blocks of [64 rows x 128 B]
+constexpr int kDuBM = 128, kDuBN = 256, kDuStages = 6;
+constexpr int kDuABytes = kDuBM * 128;        // K-major [128 rows x 64 tokens]
+constexpr int kDuBBytes = (kDuBN / 2) * 128;  // MN-major 2 x [64 tokens x 64 cols]
 constexpr int kDuStageBytes = kDuABytes + kDuBBytes;
-constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 4096;
+constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 8 * 128 * 4;
 
 __global__ void __launch_bounds__(256, 1)
     du_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
@@ -67,10 +72,12 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* ticket_s = reinterpret_cast<int*>(tmem_slot + 1);
-    float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [4][256]
+    float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [8][128]
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
 
     if (warp == 0 && elect_one()) {
         prefetch_tmap(&tmA0);
@@ -78,25 +85,26 @@ __global__ void __launch_bounds__(256, 1)
         prefetch_tmap(&tmA1);
         prefetch_tmap(&tmB1);
         for (int s = 0; s < kDuStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 5);  // MMA commit + 4 colsum warps (or 4 extra commits)
+            mbar_init(&full[s], leader ? 2 : 1);  // leader: own tx + peer relay
+            mbar_init(&empty[s], 5);              // MMA commit + 4 colsum warps (or 4 extra commits)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 8);
         }
         fence_barrier_init();
     }
     if (warp == 2) {
-        tmem_alloc<1>(tmem_slot, 512);
-        tmem_relinquish<1>();
+        tmem_alloc<2>(tmem_slot, 512);
+        tmem_relinquish<2>();
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     const int units = args.num_tiles * args.splits;
+    const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     struct Unit {
         int p, mt, nt, tile, split, kb0, kb1;
         bool colsum;
@@ -116,37 +124,36 @@ __global__ void __launch_bounds__(256, 1)
     };
 
     if (warp == 0) {
-        // ------------------------------------------------------------ producer
+        // ------------------------------------------------------------ producer (both CTAs, own half)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x) {
+            for (int u = pair; u < units; u += npairs) {
                 const Unit x = decode(u);
                 const CUtensorMap* ma = x.p ? &tmA1 : &tmA0;
                 const CUtensorMap* mb = x.p ? &tmB1 : &tmB0;
-                const int m0 = x.mt * kDuBM, n0 = x.nt * kDuBN;
+                const int m0 = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256 + (int)rank * 128;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
-                    const int k0 = kb * kDuBK;
+                    const int k0 = kb * 64;
                     mbar_arrive_expect_tx(&full[stage], kDuStageBytes);
-                    tma_load_2d<1>(ma, &full[stage], a_dst, m0, k0);
-                    tma_load_2d<1>(ma, &full[stage], a_dst + 64 * 128, m0 + 64, k0);
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) tma_load_2d<1>(mb, &full[stage], b_dst + j * 64 * 128, n0 + 64 * j, k0);
+                    tma_load_2d<1>(ma, &full[stage], a_dst, k0, m0);
+                    tma_load_2d<1>(mb, &full[stage], b_dst, n0, k0);
+                    tma_load_2d<1>(mb, &full[stage], b_dst + 64 * 128, n0 + 64, k0);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------------------ MMA issuer
-        if (elect_one()) {
-            constexpr uint32_t idesc = make_idesc(0, kDuBM, kDuBN, 1, 1);
+        // ------------------------------------------------------------ MMA issuer (leader)
+        if (leader && elect_one()) {
+            constexpr uint32_t idesc = make_idesc(0, 256, kDuBN, 0, 1);
             int stage = 0;
             uint32_t phase = 0;
             int iter = 0;
-            for (int u = blockIdx.x; u < units; u += gridDim.x, ++iter) {
+            for (int u = pair; u < units; u += npairs, ++iter) {
                 const Unit x = decode(u);
                 const int acc = iter & 1;
                 mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
@@ -159,15 +166,29 @@ __global__ void __launch_bounds__(256, 1)
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        mma_ss<1, 0>(d_tmem, make_sdesc(a_addr + k * 16 * 128, 64 * 128, 1024),
+                        mma_ss<2, 0>(d_tmem, make_sdesc(a_addr + k * 32, 0, 1024),
                                      make_sdesc(b_addr + k * 16 * 128, 64 * 128, 1024), idesc,
                                      (kb > x.kb0 || k > 0) ? 1u : 0u);
-                    mma_commit<1>(&empty[stage]);
-                    if (!x.colsum)  // stand in for the 4 colsum warps
-                        for (int i = 0; i < 4; ++i) mma_commit<1>(&empty[stage]);
+                    mma_commit<2>(&empty[stage]);
+                    if (!x.colsum)  // stand in for the 4 colsum warps (multicast to both CTAs)
+                        for (int i = 0; i < 4; ++i) mma_commit<2>(&empty[stage]);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
-                mma_commit<1>(&tfull[acc]);
+                mma_commit<2>(&tfull[acc]);
+            }
+        }
+    } else if (warp == 3) {
+        // ------------------------------------------------------------ relay (peer CTA)
+        if (!leader && elect_one()) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = pair; u < units; u += npairs) {
+                const Unit x = decode(u);
+                for (int kb = x.kb0; kb < x.kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);        // our half has landed
+                    mbar_arrive_cluster(&full[stage], 0);  // tell the leader's MMA issuer
+                    if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+                }
             }
         }
     } else if (warp >= 4) {
@@ -177,21 +198,20 @@ __global__ void __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0;
         int iter = 0;
-        for (int u = blockIdx.x; u < units; u += gridDim.x, ++iter) {
+        for (int u = pair; u < units; u += npairs, ++iter) {
             const Unit x = decode(u);
             const DuProblem& P = args.p[x.p];
-            const int m0 = x.mt * kDuBM, n0 = x.nt * kDuBN;
+            const int m0 = x.mt * 256, n0 = x.nt * 256;
             if (x.colsum) {
-                // ---- column sums of the staged G tiles while the tensor core
-                // consumes them: thread -> one 16-B chunk (8 columns) of one of the
-                // four 64-column blocks, 16 of the 64 token rows of each stage.
-                const int chunk = t & 31, blk = chunk >> 3, ch = chunk & 7, r0 = (t >> 5) * 16;
+                // ---- column sums of this CTA's 128 staged G columns: thread ->
+                // one 16-B chunk (8 columns) of one 64-column block, 8 token rows.
+                const int chunk = t & 15, blk = chunk >> 3, ch = chunk & 7, r0 = (t >> 4) * 8;
                 float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes) + blk * 64 * 128;
 #pragma unroll
-                    for (int r = r0; r < r0 + 16; ++r) {
+                    for (int r = r0; r < r0 + 8; ++r) {
                         uint32_t w[4];
                         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
@@ -207,25 +227,28 @@ __global__ void __launch_bounds__(256, 1)
                     if (lane == 0) mbar_arrive(&empty[stage]);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
-                // combine the four row groups in order -> cpart[nt][split][256]
+                // combine the 8 row groups in order -> cpart[nt][split][rank*128 + col]
 #pragma unroll
-                for (int i = 0; i < 8; ++i) csum_s[(t >> 5) * 256 + chunk * 8 + i] = cs[i];
+                for (int i = 0; i < 8; ++i) csum_s[(t >> 4) * 128 + chunk * 8 + i] = cs[i];
                 named_bar_sync(2, 128);
-                for (int c = t; c < kDuBN; c += 128)
-                    __stcg(args.cpart + ((long long)x.nt * args.splits + x.split) * kDuBN + c,
-                           csum_s[c] + csum_s[256 + c] + csum_s[512 + c] + csum_s[768 + c]);
+                {
+                    float s = 0.f;
+#pragma unroll
+                    for (int g = 0; g < 8; ++g) s += csum_s[g * 128 + t];
+                    __stcg(args.cpart + ((long long)x.nt * args.splits + x.split) * kDuBN + rank * 128 + t, s);
+                }
                 named_bar_sync(2, 128);
             } else {
                 // the MMA issuer arrives for us on non-colsum units; keep the ring position
                 for (int kb = x.kb0; kb < x.kb1; ++kb)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
             }
-            // ---- accumulator -> fp32 partial [tile][split][128][256]
+            // ---- accumulator -> fp32 partial [tile][split][256][256], our 128 rows
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
             {
-                float* prow = args.part + (((long long)x.tile * args.splits + x.split) * kDuBM + t) * kDuBN;
+                float* prow = args.part + (((long long)x.tile * args.splits + x.split) * 256 + rank * 128 + t) * kDuBN;
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
 #pragma unroll 1
                 for (int c = 0; c < kDuBN; c += 32) {
@@ -241,36 +264,39 @@ __global__ void __launch_bounds__(256, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if (leader) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(&tempty[acc], 0);
+            }
 
             // ---- deterministic split reduction (sum in split order 0..S-1)
             __threadfence();
             named_bar_sync(2, 128);
             int* tk = args.tickets + x.tile;
+            const int parts = 2 * args.splits;  // CTAs contributing to this tile
             int row_lo, row_hi, col_lo, col_hi;
             if (args.coop) {
-                // all units are co-resident (cooperative launch): wait for the S
-                // partials, then unit `split` reduces its 1/S slice of the tile.
                 if (t == 0) {
                     atomicAdd(tk, 1);
-                    while (ld_acquire_gpu(tk) < args.splits) __nanosleep(64);
+                    while (ld_acquire_gpu(tk) < parts) __nanosleep(64);
                 }
                 named_bar_sync(2, 128);
-                row_lo = x.split * kDuBM / args.splits;
-                row_hi = (x.split + 1) * kDuBM / args.splits;
-                col_lo = x.split * kDuBN / args.splits;
-                col_hi = (x.split + 1) * kDuBN / args.splits;
+                const int z = 2 * x.split + (int)rank;
+                row_lo = z * 256 / parts;
+                row_hi = (z + 1) * 256 / parts;
+                col_lo = z * kDuBN / parts;
+                col_hi = (z + 1) * kDuBN / parts;
             } else {
                 if (t == 0) *ticket_s = atomicAdd(tk, 1);
                 named_bar_sync(2, 128);
-                const bool last = *ticket_s == args.splits - 1;
+                const bool last = *ticket_s == parts - 1;
                 named_bar_sync(2, 128);
-                row_lo = 0; row_hi = last ? kDuBM : 0;
+                row_lo = 0; row_hi = last ? 256 : 0;
                 col_lo = 0; col_hi = last ? kDuBN : 0;
             }
             __threadfence();
-            const float* pbase = args.part + (long long)x.tile * args.splits * kDuBM * kDuBN;
-            const bool vec = (P.nb & 3) == 0 && (P.ldm & 3) == 0 && (P.blk & 3) == 0 &&
+            const float* pbase = args.part + (long long)x.tile * args.splits * 256 * kDuBN;
+            const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
                              (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
             for (int f = t; f < (row_hi - row_lo) * (kDuBN / 4); f += 128) {
                 const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
@@ -278,18 +304,16 @@ __global__ void __launch_bounds__(256, 1)
                 if (m >= P.M || n >= P.N) continue;
                 float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
                 for (int sp = 0; sp < args.splits; ++sp) {
-                    const float4 v = __ldcg(reinterpret_cast<const float4*>(pbase + ((long long)sp * kDuBM + r) * kDuBN + c));
+                    const float4 v =
+                        __ldcg(reinterpret_cast<const float4*>(pbase + ((long long)sp * 256 + r) * kDuBN + c));
                     sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
                 }
                 const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
+                const long long mo = (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
                 if (vec && n + 4 <= P.N) {
-                    *reinterpret_cast<float4*>(P.out + (n / P.nb) * P.blk + (long long)m * P.ldm + n % P.nb) =
-                        make_float4(o[0], o[1], o[2], o[3]);
+                    *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
                 } else {
-                    for (int i = 0; i < 4 && n + i < P.N; ++i) {
-                        const long long nn = n + i;
-                        P.out[(nn / P.nb) * P.blk + (long long)m * P.ldm + nn % P.nb] = o[i];
-                    }
+                    for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
                 }
             }
             if (x.colsum) {
@@ -302,12 +326,12 @@ __global__ void __launch_bounds__(256, 1)
                     P.db[n] = sum;
                 }
             }
-            // ---- ticket release: the last of the S units to get here resets it
+            // ---- ticket release: the last CTA of the tile to get here resets it
             named_bar_sync(2, 128);
             if (t == 0) {
                 if (args.coop) {
-                    if (atomicAdd(tk, 1) == 2 * args.splits - 1) atomicExch(tk, 0);
-                } else if (*ticket_s == args.splits - 1) {
+                    if (atomicAdd(tk, 1) == 2 * parts - 1) atomicExch(tk, 0);
+                } else if (*ticket_s == parts - 1) {
                     atomicExch(tk, 0);
                 }
             }
@@ -315,10 +339,10 @@ __global__ void __launch_bounds__(256, 1)
     }
 
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<1>(tmem_base, 512);
+        tmem_dealloc<2>(tmem_base, 512);
     }
 }
 

@@ -32,13 +32,14 @@ struct GemmArgs {
     int num_m_tiles, num_n_tiles, splits, k_blocks;
     float alpha;
     const float* bias;  // [N] fp32, nullable (direct mode only)
-    // direct mode (partial == nullptr): all columns -> out; columns n < n_split
-    // are additionally copied to out2 (row stride ldo2)
+    // direct mode (partial == nullptr): all columns -> out (nullable); columns
+    // [out2_c0, out2_c1) are additionally written transposed to out2
+    // (out2[(n - out2_c0) * ldo2 + m]) -- the layout the dU kernel reads.
     void* out;
     long long ldo;
     void* out2;
     long long ldo2;
-    int n_split;
+    int out2_c0, out2_c1;
     int out_f32;  // 1: fp32 output, 0: bf16 output
     // split-K mode
     float* partial;  // [splits][M][N] fp32
@@ -246,11 +247,20 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], args.alpha, bv[j]);
                 const int nvalid = min(16, args.N - n);
-                for (int w = 0; w < 2; ++w) {
-                    void* obase = w == 0 ? args.out : args.out2;
-                    const long long ld = w == 0 ? args.ldo : args.ldo2;
-                    if (w == 1 && (!obase || n >= args.n_split)) break;
-                    const int nv = w == 0 ? nvalid : min(nvalid, args.n_split - n);
+                // columns [out2_c0, out2_c1) also go out transposed: out2[(n - c0) * ldo2 + row]
+                if (args.out2 && n + 16 > args.out2_c0 && n < args.out2_c1) {
+                    for (int j = 0; j < 16; ++j) {
+                        const int nn = n + j;
+                        if (nn < args.out2_c0 || nn >= args.out2_c1 || nn >= args.N) continue;
+                        const long long o = (long long)(nn - args.out2_c0) * args.ldo2 + row;
+                        if (args.out_f32) reinterpret_cast<float*>(args.out2)[o] = v[j];
+                        else reinterpret_cast<__nv_bfloat16*>(args.out2)[o] = __float2bfloat16_rn(v[j]);
+                    }
+                }
+                if (args.out) {
+                    void* obase = args.out;
+                    const long long ld = args.ldo;
+                    const int nv = nvalid;
                     if (args.out_f32) {
                         float* dst = reinterpret_cast<float*>(obase) + (long long)row * ld + n;
                         if (nv == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {

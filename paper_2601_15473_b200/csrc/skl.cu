@@ -337,25 +337,29 @@ bool use_fused(const SklDims& d, skl_dtype t) {
 }
 
 struct Plan {
-    size_t acat, bcat, acatT, bcatT, bias32, inter, saved, part, colsum, total;
+    size_t acat, bcat, acatT, bcatT, bias32, inter, saved, p2t, colsum, total;
     size_t du_part, du_cpart, du_tickets;
-    int s_du1, s_du2;
 };
 
+// Row stride (elements) of the transposed token-reduction operands Saved and
+// P_S2 ([L*k][T8]): T rounded up to 8 so every row starts 16-byte aligned.
+int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
+
 // Tiling of the fused dU kernel (du.cuh): problem 0 = dU1 [Lk, d_out],
-// problem 1 = dU2 [d_in, Lk]; 128 x 256 tiles; T split so ~one unit per SM.
+// problem 1 = dU2ᵀ [Lk, d_in]; 256 x 256 pair tiles; T split so ~one unit
+// per CTA pair.
 struct DuShape {
     int m0, n0t, m1, n1t, tiles, splits, kb;
 };
 DuShape du_shape(const SklDims& d, int64_t T, int sms) {
     DuShape s;
-    s.m0 = (int)((d.Lk + 127) / 128);
+    s.m0 = (int)((d.Lk + 255) / 256);
     s.n0t = (int)((d.d_out + 255) / 256);
-    s.m1 = (int)((d.d_in + 127) / 128);
-    s.n1t = (int)((d.Lk + 255) / 256);
+    s.m1 = (int)((d.Lk + 255) / 256);
+    s.n1t = (int)((d.d_in + 255) / 256);
     s.tiles = s.m0 * s.n0t + s.m1 * s.n1t;
     s.kb = (int)std::max<int64_t>(1, (T + 63) / 64);
-    s.splits = std::max(1, std::min(sms / s.tiles, std::max(1, s.kb / 2)));
+    s.splits = std::max(1, std::min((sms / 2) / s.tiles, std::max(1, s.kb / 2)));
     return s;
 }
 
@@ -375,22 +379,17 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.bcatT = take((size_t)d.d_out * d.R_pad * e);
     p.bias32 = take((size_t)d.d_out * 4);
     const bool fused = use_fused(d, t);
-    // fwd: H [T, R_pad] only when unfused; bwd: P [T, R_pad] (P_S2 always goes out)
-    p.inter = take((bwd || !fused) ? (size_t)T * d.R_pad * e : 0);
-    p.saved = take(bwd ? (size_t)T * d.Lk * e : 0);
-    p.s_du1 = pick_splits((int)d.Lk, (int)d.d_out, (int)T, 256, 1, sms, t == SKL_BF16 ? 64 : 32);
-    p.s_du2 = pick_splits((int)d.d_in, (int)d.Lk, (int)T, 256, 1, sms, t == SKL_BF16 ? 64 : 32);
-    size_t part = 0;
+    // unfused only: H [T, R_pad] (fwd) / P [T, R_pad] (bwd) through HBM
+    p.inter = take(!fused ? (size_t)T * d.R_pad * e : 0);
+    p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
+    p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
     if (bwd) {
-        part = std::max((size_t)p.s_du1 * d.Lk * d.d_out, (size_t)p.s_du2 * d.d_in * d.Lk) * 4;
-        if (t == SKL_F32_TF32) part += (size_t)T * (d.d_in + d.d_out + 2 * d.Lk) * 4;  // transposed operands
         const DuShape u = du_shape(d, T, sms);
-        p.du_part = take((size_t)u.tiles * u.splits * 128 * 256 * 4);
+        p.du_part = take((size_t)u.tiles * u.splits * 256 * 256 * 4);
         p.du_cpart = take((size_t)u.n0t * u.splits * 256 * 4);
         p.du_tickets = take((size_t)u.tiles * 4);
     }
-    p.part = take(part);
-    p.colsum = take(bwd ? (size_t)colsum_chunks(T) * d.d_out * 4 : 0);
+    p.colsum = take(0);
     p.total = off;
     return p;
 }
@@ -469,7 +468,7 @@ skl_status skl_workspace_size(const skl_shape* s, int64_t T, size_t* fwd_bytes, 
     if (T < 0) return fail(SKL_ERR_SHAPE, "T must be >= 0");
     DevInfo di = dev_info();
     const int sms = di.sms ? di.sms : 148;
-    if (fwd_bytes) *fwd_bytes = plan(d, s->dtype, T, false, sms).total;
+    if (fwd_bytes) *fwd_bytes = plan(d, s->dtype, T, false, sms).total;  // saved_proj: [L*k][round8(T)]
     if (bwd_bytes) *bwd_bytes = plan(d, s->dtype, T, true, sms).total;
     return SKL_OK;
 }
@@ -492,13 +491,9 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     const int elem = elem_of(s->dtype);
     const int eb = ebytes(s->dtype);
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
-    void* acat = at<void>(workspace, p.acat);
-    void* bcat = at<void>(workspace, p.bcat);
     void* acatT = at<void>(workspace, p.acatT);
     void* bcatT = at<void>(workspace, p.bcatT);
     float* bias32 = at<float>(workspace, p.bias32);
-    (void)acat;
-    (void)bcat;
     const bool fused = use_fused(d, s->dtype);
     const bool direct = fused && direct_ok(d, s->dtype);
     if (!direct) SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, bcatT, bias, bias32, st));
@@ -515,10 +510,10 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
         a.bias_bf16 = direct ? 1 : 0;
         a.out = y;
         a.ldo = d.d_out;
-        a.save = saved_proj;
+        a.save = saved_proj;  // Savedᵀ [Lk][T8]
         a.save_col0 = 0;
         a.save_cols = (int)d.Lk;
-        a.ld_save = d.Lk;
+        a.ld_save = t8(T);
         a.Lk = (int)d.Lk;
         a.k = (int)d.k;
         a.dS = (int)d.d_in;
@@ -527,15 +522,16 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
                        di.sms, st);
     }
 
-    // Unfused fallback: H through HBM.
+    // Unfused fallback (R > 512 or SKL_FORCE_UNFUSED): H through HBM.
     void* H = at<void>(workspace, p.inter);
     GemmArgs g1 = {};
     g1.alpha = 1.f;
     g1.out = H;
     g1.ldo = d.R_pad;
     g1.out2 = saved_proj;
-    g1.ldo2 = d.Lk;
-    g1.n_split = saved_proj ? (int)d.Lk : 0;
+    g1.ldo2 = t8(T);
+    g1.out2_c0 = 0;
+    g1.out2_c1 = (int)d.Lk;
     g1.out_f32 = eb == 4;
     g1.splits = 1;
     View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
@@ -548,7 +544,6 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g2.bias = bias32;
     g2.out = y;
     g2.ldo = d.d_out;
-    g2.n_split = 0;
     g2.out_f32 = eb == 4;
     g2.splits = 1;
     View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
@@ -581,38 +576,40 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         if (grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
         return SKL_OK;
     }
+    if (s->dtype != SKL_BF16)
+        return fail(SKL_ERR_UNSUPPORTED, "the TF32 (fp32 I/O) backward is not implemented yet; use SKL_BF16");
     const int elem = elem_of(s->dtype);
-    const int eb = ebytes(s->dtype);
-    const bool bf16 = s->dtype == SKL_BF16;
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    const int64_t ldt = t8(T);
     void* acat = at<void>(workspace, p.acat);
     void* bcat = at<void>(workspace, p.bcat);
     void* acatT = at<void>(workspace, p.acatT);
     void* P = at<void>(workspace, p.inter);
-    float* part = at<float>(workspace, p.part);
-    const bool bwd_direct = use_fused(d, s->dtype) && grad_x != nullptr && direct_ok(d, s->dtype);
+    void* p2t = at<void>(workspace, p.p2t);
+    const bool fused = use_fused(d, s->dtype);
+    const bool bwd_direct = fused && grad_x != nullptr && direct_ok(d, s->dtype);
     if (!bwd_direct || !saved_proj)
         SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, nullptr,
                               nullptr, st));
 
-    // Saved projection x·S1 (recomputed only when the caller did not keep it).
+    // Savedᵀ = (x·S1)ᵀ, recomputed only when the caller did not keep it.
     const void* saved = saved_proj;
     if (!saved) {
         void* sv = at<void>(workspace, p.saved);
         GemmArgs g = {};
         g.alpha = 1.f;
-        g.out = sv;
-        g.ldo = d.Lk;
-        g.out_f32 = eb == 4;
+        g.out2 = sv;
+        g.ldo2 = ldt;
+        g.out2_c0 = 0;
+        g.out2_c1 = (int)d.Lk;
         g.splits = 1;
         View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
-        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
-        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
         saved = sv;
     }
 
-    // P = G·Bcatᵀ and dX = inv·P·Acatᵀ
-    if (use_fused(d, s->dtype) && grad_x) {
+    // P = G·Bcatᵀ (P_S2ᵀ leaves the chip) and dX = inv·P·Acatᵀ
+    if (fused && grad_x) {
         B2BArgs a = {};
         a.T = (int)T;
         a.K1 = (int)d.d_out;
@@ -623,116 +620,91 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         a.bias = nullptr;
         a.out = grad_x;
         a.ldo = d.d_in;
-        a.save = at<uint8_t>(P, (size_t)d.Lk * eb);  // only the S2 half of P leaves the chip
+        a.save = p2t;  // P_S2ᵀ [Lk][T8]
         a.save_col0 = (int)d.Lk;
         a.save_cols = (int)d.Lk;
-        a.ld_save = d.R_pad;
+        a.ld_save = ldt;
         a.Lk = (int)d.Lk;
         a.k = (int)d.k;
         a.dS = (int)d.d_in;
         if (bwd_direct)
             SKL_TRY(run_b2b("b2b_bwd", 0, 2, B2BSrc{grad_y, U1s, S2s, S1s, U2s}, a, di.sms, st));
         else
-            SKL_TRY(run_b2b("b2b_bwd", bf16 ? 0 : 1, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
+            SKL_TRY(run_b2b("b2b_bwd", 0, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
     } else {
         GemmArgs g = {};
         g.alpha = 1.f;
-        g.out = P;
+        g.out = fused ? nullptr : P;  // P only feeds the unfused dX GEMM
         g.ldo = d.R_pad;
-        g.out_f32 = eb == 4;
+        g.out2 = p2t;
+        g.ldo2 = ldt;
+        g.out2_c0 = (int)d.Lk;
+        g.out2_c1 = (int)(2 * d.Lk);
         g.splits = 1;
         View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
-        if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
-        else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
         if (grad_x) {
             GemmArgs g2 = {};
             g2.alpha = inv;
             g2.out = grad_x;
             g2.ldo = d.d_in;
-            g2.out_f32 = eb == 4;
             g2.splits = 1;
             View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
-            if (bf16) SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
-            else SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+            SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
         }
     }
 
-    // dU1s = inv·Savedᵀ·G  ([Lk, d_out] == [L][k][d_out])
-    // dU2s = inv·Xᵀ·P_S2   ([d_in, Lk] scattered to [L][d_in][k])
-    const void* P_S2 = at<uint8_t>(P, (size_t)d.Lk * eb);
-    static const bool legacy_du = [] {
-        const char* e = getenv("SKL_DU_LEGACY");
-        return e && atoi(e) != 0;
-    }();
-    if (bf16 && !legacy_du) {
-        // fused dU1 + dU2 (+ db) with in-kernel deterministic split reduction
-        const DuShape u = du_shape(d, T, di.sms);
-        DuArgs a = {};
-        a.k_blocks = u.kb;
-        a.splits = u.splits;
-        a.num_tiles = u.tiles;
-        a.p[0] = DuProblem{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
-                           (long long)d.d_out, 0, (long long)d.d_out, grad_bias};
-        a.p[1] = DuProblem{(int)d.d_in, (int)d.Lk, u.m1, u.n1t, u.m0 * u.n0t, 0, inv, grad_U2s,
-                           (long long)d.k, (long long)(d.d_in * d.k), (long long)d.k, nullptr};
-        a.part = at<float>(workspace, p.du_part);
-        a.cpart = at<float>(workspace, p.du_cpart);
-        a.tickets = at<int>(workspace, p.du_tickets);
-        CUtensorMap ta0, tb0, ta1, tb1;
-        SKL_TRY(make_tmap(&ta0, saved, 2, d.Lk, T, d.Lk, 64, 64));
-        SKL_TRY(make_tmap(&tb0, grad_y, 2, d.d_out, T, d.d_out, 64, 64));
-        SKL_TRY(make_tmap(&ta1, x, 2, d.d_in, T, d.d_in, 64, 64));
-        SKL_TRY(make_tmap(&tb1, P_S2, 2, d.Lk, T, d.R_pad, 64, 64));
-        SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
-        static bool attr_set = false;
-        if (!attr_set) {
-            SKL_CUDA(cudaFuncSetAttribute(dev::du_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
-            attr_set = true;
-        }
-        const int units = u.tiles * u.splits;
-        // One unit per SM and all units co-resident -> cooperative launch, and
-        // the S units of a tile reduce its partials in parallel (1/S each).
-        a.coop = units <= di.sms ? 1 : 0;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(a.coop ? units : std::min(di.sms, units));
-        cfg.blockDim = dim3(256);
-        cfg.dynamicSmemBytes = dev::kDuSmem;
-        cfg.stream = st;
-        cudaLaunchAttribute attr[1];
-        attr[0].id = cudaLaunchAttributeCooperative;
-        attr[0].val.cooperative = a.coop;
-        cfg.attrs = attr;
-        cfg.numAttrs = 1;
-        ProfScope ps_("du_fused", st);
-        SKL_CUDA(cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a));
-        return SKL_OK;
+    // dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
+    // ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.
+    const DuShape u = du_shape(d, T, di.sms);
+    DuArgs a = {};
+    a.k_blocks = u.kb;
+    a.splits = u.splits;
+    a.num_tiles = u.tiles;
+    a.p[0] = DuProblem{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
+                       (long long)1 << 40, 0, (long long)d.d_out, 1, grad_bias};
+    a.p[1] = DuProblem{(int)d.Lk, (int)d.d_in, u.m1, u.n1t, u.m0 * u.n0t, 0, inv, grad_U2s,
+                       (long long)d.k, (long long)(d.d_in * d.k), 1, (long long)d.k, nullptr};
+    a.part = at<float>(workspace, p.du_part);
+    a.cpart = at<float>(workspace, p.du_cpart);
+    a.tickets = at<int>(workspace, p.du_tickets);
+    CUtensorMap ta0, tb0, ta1, tb1;
+    SKL_TRY(make_tmap(&ta0, saved, 2, T, d.Lk, ldt, 64, 128));           // Savedᵀ, K-major
+    SKL_TRY(make_tmap(&tb0, grad_y, 2, d.d_out, T, d.d_out, 64, 64));    // G, MN-major
+    SKL_TRY(make_tmap(&ta1, p2t, 2, T, d.Lk, ldt, 64, 128));             // P_S2ᵀ, K-major
+    SKL_TRY(make_tmap(&tb1, x, 2, d.d_in, T, d.d_in, 64, 64));           // X, MN-major
+    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKL_CUDA(cudaFuncSetAttribute(dev::du_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
+        attr_set = true;
     }
-    if (bf16) {
-        GemmArgs g = {};
-        g.partial = part;
-        g.splits = p.s_du1;
-        View va{saved, T, d.Lk, d.Lk}, vb{grad_y, T, d.d_out, d.d_out};
-        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>("gemm_dU1", va, vb, (int)d.Lk, (int)d.d_out, (int)T, g, di.sms, st)));
-        SKL_CUDA(launch_reduce_partials(part, g.splits, d.Lk, d.d_out, inv,
-                                        grad_U1s, d.d_out, 0, d.d_out, st));
-        GemmArgs g2 = {};
-        g2.partial = part;
-        g2.splits = p.s_du2;
-        View vx{x, T, d.d_in, d.d_in}, vp{P_S2, T, d.Lk, d.R_pad};
-        SKL_TRY((run_gemm<1, 0, true, true, 256, 4>("gemm_dU2", vx, vp, (int)d.d_in, (int)d.Lk, (int)T, g2, di.sms, st)));
-        SKL_CUDA(launch_reduce_partials(part, g2.splits, d.d_in, d.Lk, inv,
-                                        grad_U2s, d.k, d.d_in * d.k, d.k, st));
-    } else {
-        // TF32: MN-major fp32 operands are not staged by TMA here; transpose the
-        // token-major operands once so both dU GEMMs run K-major.
-        float* tX = part + std::max((size_t)p.s_du1 * d.Lk * d.d_out, (size_t)p.s_du2 * d.d_in * d.Lk);
-        float* tG = tX + (size_t)T * d.d_in;
-        float* tS = tG + (size_t)T * d.d_out;
-        float* tP = tS + (size_t)T * d.Lk;
-        (void)tX; (void)tG; (void)tS; (void)tP;
-        return fail(SKL_ERR_UNSUPPORTED, "tf32 backward dU path not built yet");
+    const int units = u.tiles * u.splits;  // CTA pairs
+    a.coop = 2 * units <= di.sms ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (a.coop ? units : std::min(di.sms / 2, units)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = dev::kDuSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = a.coop;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    ProfScope ps_("du_fused", st);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a);
+    if (le != cudaSuccess && a.coop) {  // cooperative + cluster refused: last-CTA reduction instead
+        (void)cudaGetLastError();
+        a.coop = 0;
+        attr[1].val.cooperative = 0;
+        cfg.gridDim = dim3(2 * std::min(di.sms / 2, units));
+        le = cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a);
     }
-    if (grad_bias) SKL_CUDA(launch_colsum(grad_y, elem, T, d.d_out, at<float>(workspace, p.colsum), grad_bias, st));
+    SKL_CUDA(le);
     return SKL_OK;
 }
 

@@ -124,16 +124,16 @@ def test_forward_parity_bf16(skl, port, monkeypatch, unfused, d_in, d_out, L, k,
         pytest.skip("unfused path is exercised in a separate process (SKL_FORCE_UNFUSED=1)")
     s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
     y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
-    saved = torch.empty(T, L * k, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(L * k, (T + 7) // 8 * 8, dtype=torch.bfloat16, device="cuda")
     ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
     skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
     torch.cuda.synchronize()
     y_ref = port.forward(P, b64, x64).T
     from tests._util import check_close
     check_close("y", _np(y), y_ref, "bf16")
-    # saved projection x·S1_i, term-major columns
+    # saved projection (x·S1_i, term-major) is kept transposed: [L*k][round8(T)]
     sv_ref = np.concatenate([x64.T @ P.s2[i].T for i in range(L)], axis=1)
-    check_close("saved", _np(saved), sv_ref, "bf16")
+    check_close("saved", _np(saved)[:, :T].T, sv_ref, "bf16")
 
 
 @pytest.mark.parametrize("d_in,d_out,L,k,T", CASES)
@@ -141,7 +141,7 @@ def test_backward_parity_bf16(skl, port, d_in, d_out, L, k, T):
     import oracle
     s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
     y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
-    saved = torch.empty(T, L * k, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(L * k, (T + 7) // 8 * 8, dtype=torch.bfloat16, device="cuda")
     ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
     skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
     gx = torch.empty(T, d_in, dtype=torch.bfloat16, device="cuda")
