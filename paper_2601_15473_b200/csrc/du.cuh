@@ -47,6 +47,7 @@ struct DuArgs {
     float* cpart;    // [p0.n_tiles][splits][256]
     int* tickets;    // [num_tiles], zero on entry, left zero on exit
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
+    int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
 };
 
 namespace dev {
@@ -138,6 +139,16 @@ __global__ void __launch_bounds__(256, 1)
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
                     const int k0 = kb * 64;
+                    if (!args.relay) {
+                        // no colsum anywhere: pair-signalled TMA straight onto the leader's barrier
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kDuStageBytes);
+                        else mbar_arrive_cluster(&full[stage], 0);
+                        tma_load_2d<2>(ma, &full[stage], a_dst, k0, m0);
+                        tma_load_2d<2>(mb, &full[stage], b_dst, n0, k0);
+                        tma_load_2d<2>(mb, &full[stage], b_dst + 64 * 128, n0 + 64, k0);
+                        if (++stage == kDuStages) { stage = 0; phase ^= 1; }
+                        continue;
+                    }
                     mbar_arrive_expect_tx(&full[stage], kDuStageBytes);
                     tma_load_2d<1>(ma, &full[stage], a_dst, k0, m0);
                     tma_load_2d<1>(mb, &full[stage], b_dst, n0, k0);
@@ -179,7 +190,7 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp == 3) {
         // ------------------------------------------------------------ relay (peer CTA)
-        if (!leader && elect_one()) {
+        if (!leader && args.relay && elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
             for (int u = pair; u < units; u += npairs) {
@@ -278,7 +289,13 @@ __global__ void __launch_bounds__(256, 1)
             if (args.coop) {
                 if (t == 0) {
                     atomicAdd(tk, 1);
-                    while (ld_acquire_gpu(tk) < parts) __nanosleep(64);
+                    uint64_t t0, t1;
+                    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+                    while (ld_acquire_gpu(tk) < parts) {  // bounded: a scheduling bug traps, never hangs
+                        __nanosleep(64);
+                        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+                        if (t1 - t0 > 10000000000ull) __trap();
+                    }
                 }
                 named_bar_sync(2, 128);
                 const int z = 2 * x.split + (int)rank;

@@ -680,7 +680,9 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         attr_set = true;
     }
     const int units = u.tiles * u.splits;  // CTA pairs
-    a.coop = 2 * units <= di.sms ? 1 : 0;
+    a.relay = grad_bias ? 1 : 0;
+    static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
+    a.coop = (!no_coop && 2 * units <= di.sms) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(2 * (a.coop ? units : std::min(di.sms / 2, units)));
     cfg.blockDim = dim3(256);
