@@ -60,19 +60,30 @@ __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8])
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// D[tmem] (+)= A[tmem] * B[smem]  (kind::f16, A K-major bf16 packed 2/column)
-template <int kCG>
+// D[tmem] (+)= A[tmem] * B[smem].  kKind 0: kind::f16, A = bf16 packed 2 per
+// TMEM column; kKind 1: kind::tf32, A = one fp32 (TF32-rounded) per column.
+template <int kCG, int kKind>
 __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accumulate) {
-    if constexpr (kCG == 1)
+    if constexpr (kCG == 1 && kKind == 0)
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
-    else
+    else if constexpr (kCG == 2 && kKind == 0)
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+    else if constexpr (kCG == 1)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+            "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
@@ -96,8 +107,15 @@ __device__ unsigned long long g_b2b_eprof[296][8];
         }                                                                      \
     } while (0)
 
-template <int kCG, int kMode>
+template <int kCG, int kMode, int kKind = 0>
 struct B2BCfg {
+    // kKind 1 (TF32, fp32 I/O): a k-block is 32 fp32 (still 128 B per row, so
+    // every smem tile / descriptor has the bf16 byte geometry); the output
+    // staging doubles (fp32 tiles) and costs one stage.
+    static_assert(kKind == 0 || kMode == 0, "the TF32 fused kernel streams packed panels (kMode 0)");
+    static constexpr int kElem = kKind == 0 ? 2 : 4;
+    static constexpr int kBK = 128 / kElem;                  // elements per k-block
+    static constexpr int kOutBytes = kKind == 0 ? 16384 : 32768;  // per epilogue group
     // The backward's GEMM1 (K = d_out, 80% of its MMAs) runs single-pass: one
     // A1 tile feeds both 256-wide chunks, so G is read once instead of twice;
     // its stages therefore hold A1 + B1 for all of R (48 KB).
@@ -107,13 +125,13 @@ struct B2BCfg {
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
     static constexpr int kBiasTabBytes = kMode == 1 ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages = kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0);
+    static constexpr int kStages = kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0) - kKind;
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
     static constexpr int kSmem =
-        kStages * kStageBytes + 2 * 16384 + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 256;
+        kStages * kStageBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 256;
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -123,19 +141,19 @@ struct B2BCfg {
 //          [L*k][d_out] (MN-major tiles).  No packing pass.
 // kMode 2: backward straight from the stacks: B1 = U1s|S2s [L*k][d_out]
 //          (K-major), B2 = S1s|U2s [L*d_in][k] (K-major, per-term row offset).
-template <int kCG, int kMode>
+template <int kCG, int kMode, int kKind>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode>;
+    using C = B2BCfg<kCG, kMode, kKind>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
-    uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 2 x 16 KB output staging
-    float* bias_s = reinterpret_cast<float*>(stage_out + 2 * 16384);  // 2 slots x 128 bias values
-    float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * 16384 + 1024);  // kMode 1: bias[N2]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * 16384 + 1024 + C::kBiasTabBytes);
+    uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 2 x kOutBytes output staging
+    float* bias_s = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes);  // 2 slots x 128 bias values
+    float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes + 1024);  // kMode 1: bias[N2]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * C::kOutBytes + 1024 + C::kBiasTabBytes);
     uint64_t* full = bars;                            // [kStages]
     uint64_t* empty = bars + C::kStages;              // [kStages]
     uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
@@ -183,8 +201,8 @@ __global__ void __launch_bounds__(384, 1)
     const int cluster_id = blockIdx.x / kCG;
     const int num_clusters = gridDim.x / kCG;
     const int nch = (args.R_pad + 255) / 256;
-    const int nkb1 = (args.K1 + 63) / 64;
-    const int nkb2 = args.R_pad / 64;
+    const int nkb1 = (args.K1 + C::kBK - 1) / C::kBK;
+    const int nkb2 = args.R_pad / C::kBK;
     const int nst2 = (nkb2 + C::kKbPerStage2 - 1) / C::kKbPerStage2;
     const int n2_tiles = (args.N2 + 127) / 128;
 
@@ -210,7 +228,7 @@ __global__ void __launch_bounds__(384, 1)
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
-                        tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * 64, am);
+                        tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am);
                         for (int c = c_lo; c < c_hi; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
                             const int brows = wc / kCG;
@@ -218,7 +236,7 @@ __global__ void __launch_bounds__(384, 1)
                             uint8_t* bst = st + 16384 + (c - c_lo) * (256 / kCG) * 128;
                             if constexpr (kMode == 0) {
                                 for (int r = 0; r < brows; r += args.b1rows)
-                                    tma_load_2d<kCG>(&tmB1, &full[stage], bst + r * 128, kb * 64, b0 + r);
+                                    tma_load_2d<kCG>(&tmB1, &full[stage], bst + r * 128, kb * C::kBK, b0 + r);
                             } else if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
                                 for (int r = 0; r < brows; r += args.b1rows) {
                                     const int rg = b0 + r;
@@ -256,7 +274,7 @@ __global__ void __launch_bounds__(384, 1)
                             continue;
                         }
                         for (int q = 0; q < nk; ++q) {
-                            const int r0 = (kb0 + q) * 64;  // rank index of this k-block
+                            const int r0 = (kb0 + q) * C::kBK;  // rank index of this k-block
                             if constexpr (kMode == 0) {
                                 tma_load_2d<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, r0, brow);
                             } else if constexpr (kMode == 1) {  // MN-major rows of [U1s ; S2s]
@@ -288,7 +306,7 @@ __global__ void __launch_bounds__(384, 1)
             const long long tm0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             uint32_t slot_seq = 0;
-            const uint32_t idesc2 = make_idesc(0, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
+            const uint32_t idesc2 = make_idesc(kKind, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
             int it = 0;
             for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
                 // ---- GEMM1: H chunks (one pass per chunk, or one pass for all)
@@ -306,12 +324,12 @@ __global__ void __launch_bounds__(384, 1)
                         const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int c = c_lo; c < c_hi; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
-                            const uint32_t idesc1 = make_idesc(0, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
+                            const uint32_t idesc1 = make_idesc(kKind, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
                             const uint32_t d = tmem_base + 256 * c;
                             const uint32_t b_addr = a_addr + 16384 + (c - c_lo) * (256 / kCG) * 128;
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
-                                mma_ss<kCG, 0>(d, make_sdesc(a_addr + k * 32, 0, 1024),
+                                mma_ss<kCG, kKind>(d, make_sdesc(a_addr + k * 32, 0, 1024),
                                                kMode == 1 ? make_sdesc(b_addr + k * 2048, 8192, 1024)
                                                           : make_sdesc(b_addr + k * 32, 0, 1024),
                                                idesc1, (kb > 0 || k > 0) ? 1u : 0u);
@@ -344,7 +362,7 @@ __global__ void __launch_bounds__(384, 1)
                                 const uint64_t bdesc = kMode == 1
                                     ? make_sdesc(b_addr + q * C::kB2KbBytes + k * 2048, 8192, 1024)
                                     : make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024);
-                                mma_ts<kCG>(d, a_t, bdesc, idesc2, (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
+                                mma_ts<kCG, kKind>(d, a_t, bdesc, idesc2, (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
                             }
                         }
                         mma_commit<kCG>(&empty[stage]);
@@ -372,7 +390,7 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t slot_seq = 0;
         uint32_t tf_par0 = 0, tf_par1 = 0;
         const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
-        uint8_t* buf = stage_out + wg * 16384;        // this group's output staging buffer
+        uint8_t* buf = stage_out + wg * C::kOutBytes;  // this group's output staging buffer
         float* bias_g = bias_s + wg * 128;            // [2 slots][64]
         unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SKL_B2B_DEBUG & 32
         const long long te0 = clock64();
@@ -411,6 +429,31 @@ __global__ void __launch_bounds__(384, 1)
                 SKL_TIMED(4, mbar_wait(&tfull1[c], it & 1));
                 tc_fence_after();
                 const long long tc0 = clock64();
+                if constexpr (kKind == 1) {
+                    // TF32: H stays one fp32 word per column; round in place with
+                    // cvt.rna, group wg owns columns [wg*wc/2, (wg+1)*wc/2).
+#pragma unroll 1
+                    for (int cl = (int)wg * (wc / 2); cl < ((int)wg + 1) * (wc / 2); cl += 16) {
+                        uint32_t r[16];
+                        tmem_ld16(tmem_base + lane_base + 256 * c + cl, r);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(tf32_rna(__uint_as_float(r[i])));
+                        uint32_t lo[8], hi[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) { lo[i] = r[i]; hi[i] = r[8 + i]; }
+                        tmem_st8(tmem_base + lane_base + 256 * c + cl, lo);
+                        tmem_st8(tmem_base + lane_base + 256 * c + cl + 8, hi);
+                        const int col = 256 * c + cl;
+                        if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
+                            float* dst = reinterpret_cast<float*>(args.save) + row;
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
+                                    dst[(long long)(col + i - args.save_col0) * args.ld_save] = __uint_as_float(r[i]);
+                        }
+                    }
+                } else
 #pragma unroll 1
                 for (int rd = 0; rd < 2; ++rd) {
                     const int qi = 2 * rd + (int)wg;
@@ -499,6 +542,28 @@ __global__ void __launch_bounds__(384, 1)
                 SKL_TIMED(3, named_bar_sync(1 + wg, 128));
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
                 const long long tm0 = clock64();
+                if constexpr (kKind == 1) {
+                    // fp32 output: the group's 64 columns are two [128 x 32] fp32 boxes
+#pragma unroll
+                    for (int c = 0; c < 16; ++c) {
+                        const float4 b4 = reinterpret_cast<const float4*>(bias_g + s * 64)[c];
+                        const uint32_t* src = (c < 8) ? ra : rb;
+                        const int o = (c & 7) * 4;
+                        st_shared_v4(row_addr + (c >> 3) * 16384 + ((uint32_t)((c & 7) ^ (srow & 7)) << 4),
+                                     __float_as_uint(fmaf(__uint_as_float(src[o]), alpha, b4.x)),
+                                     __float_as_uint(fmaf(__uint_as_float(src[o + 1]), alpha, b4.y)),
+                                     __float_as_uint(fmaf(__uint_as_float(src[o + 2]), alpha, b4.z)),
+                                     __float_as_uint(fmaf(__uint_as_float(src[o + 3]), alpha, b4.w)));
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(1 + wg, 128);
+                    if (issuer) {
+                        tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
+                        tma_store_2d(&tmY, buf + 16384, n0 + 32, t * tile_rows + (int)rank * 128);
+                        bulk_commit();
+                    }
+                    continue;
+                }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const float4* bp = kMode == 1 ? reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)
@@ -541,6 +606,8 @@ __global__ void __launch_bounds__(384, 1)
 }  // namespace dev
 
 // Host side (skl.cu): whether the fused path handles this rank / dtype.
-inline bool b2b_supported(long long R_pad, int kind) { return kind == 0 && R_pad <= 512; }
+// bf16: H compacts to R/2 TMEM columns, R <= 512.  TF32: H keeps one column
+// per rank index next to the two 128-column GEMM2 slots, R <= 256.
+inline bool b2b_supported(long long R_pad, int kind) { return kind == 0 ? R_pad <= 512 : R_pad <= 256; }
 
 }  // namespace skl

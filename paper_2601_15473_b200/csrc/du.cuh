@@ -52,15 +52,27 @@ struct DuArgs {
 
 namespace dev {
 
+// A k-block is 128 bytes of tokens: 64 bf16 (kKind 0) or 32 fp32 words (kKind 1,
+// TF32).  Every tile therefore has the same byte geometry in both variants;
+// only the MN-major B blocks narrow from 64 to 32 columns.
 constexpr int kDuBM = 128, kDuBN = 256, kDuStages = 6;
-constexpr int kDuABytes = kDuBM * 128;        // K-major [128 rows x 64 tokens]
-constexpr int kDuBBytes = (kDuBN / 2) * 128;  // MN-major 2 x [64 tokens x 64 cols]
+constexpr int kDuABytes = kDuBM * 128;        // K-major [128 rows x 128 B of tokens]
+constexpr int kDuBBytes = (kDuBN / 2) * 128;  // MN-major blocks [tokens x 128 B of columns]
 constexpr int kDuStageBytes = kDuABytes + kDuBBytes;
 constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 8 * 128 * 4;
+template <int kKind>
+struct DuKind {
+    static constexpr int kElem = kKind == 0 ? 2 : 4;
+    static constexpr int kBK = 128 / kElem;   // tokens per k-block
+    static constexpr int kW = 128 / kElem;    // columns per MN-major block
+    static constexpr int kUK = kKind == 0 ? 16 : 8;  // K per MMA instruction
+};
 
+template <int kKind>
 __global__ void __launch_bounds__(256, 1)
     du_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1, DuArgs args) {
+    using KT = DuKind<kKind>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -138,21 +150,23 @@ __global__ void __launch_bounds__(256, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
-                    const int k0 = kb * 64;
+                    const int k0 = kb * KT::kBK;
                     if (!args.relay) {
                         // no colsum anywhere: pair-signalled TMA straight onto the leader's barrier
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kDuStageBytes);
                         else mbar_arrive_cluster(&full[stage], 0);
                         tma_load_2d<2>(ma, &full[stage], a_dst, k0, m0);
-                        tma_load_2d<2>(mb, &full[stage], b_dst, n0, k0);
-                        tma_load_2d<2>(mb, &full[stage], b_dst + 64 * 128, n0 + 64, k0);
+#pragma unroll
+                        for (int j = 0; j < 128 / KT::kW; ++j)
+                            tma_load_2d<2>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0);
                         if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                         continue;
                     }
                     mbar_arrive_expect_tx(&full[stage], kDuStageBytes);
                     tma_load_2d<1>(ma, &full[stage], a_dst, k0, m0);
-                    tma_load_2d<1>(mb, &full[stage], b_dst, n0, k0);
-                    tma_load_2d<1>(mb, &full[stage], b_dst + 64 * 128, n0 + 64, k0);
+#pragma unroll
+                    for (int j = 0; j < 128 / KT::kW; ++j)
+                        tma_load_2d<1>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -160,7 +174,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (leader)
         if (leader && elect_one()) {
-            constexpr uint32_t idesc = make_idesc(0, 256, kDuBN, 0, 1);
+            constexpr uint32_t idesc = make_idesc(kKind, 256, kDuBN, 0, 1);
             int stage = 0;
             uint32_t phase = 0;
             int iter = 0;
@@ -177,9 +191,10 @@ __global__ void __launch_bounds__(256, 1)
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        mma_ss<2, 0>(d_tmem, make_sdesc(a_addr + k * 32, 0, 1024),
-                                     make_sdesc(b_addr + k * 16 * 128, 64 * 128, 1024), idesc,
-                                     (kb > x.kb0 || k > 0) ? 1u : 0u);
+                        mma_ss<2, kKind>(d_tmem, make_sdesc(a_addr + k * 32, 0, 1024),
+                                         kKind == 0 ? make_sdesc(b_addr + k * KT::kUK * 128, KT::kBK * 128, 1024)
+                                                    : make_sdesc(b_addr + k * KT::kUK * 128, KT::kBK * 128, 512, 1),
+                                         idesc, (kb > x.kb0 || k > 0) ? 1u : 0u);
                     mma_commit<2>(&empty[stage]);
                     if (!x.colsum)  // stand in for the 4 colsum warps (multicast to both CTAs)
                         for (int i = 0; i < 4; ++i) mma_commit<2>(&empty[stage]);
@@ -215,37 +230,50 @@ __global__ void __launch_bounds__(256, 1)
             const int m0 = x.mt * 256, n0 = x.nt * 256;
             if (x.colsum) {
                 // ---- column sums of this CTA's 128 staged G columns: thread ->
-                // one 16-B chunk (8 columns) of one 64-column block, 8 token rows.
-                const int chunk = t & 15, blk = chunk >> 3, ch = chunk & 7, r0 = (t >> 4) * 8;
-                float cs[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+                // one 16-B chunk (kCPC columns) of one kW-column block, 8 token rows.
+                constexpr int kCPC = 16 / KT::kElem;          // columns per 16-B chunk
+                constexpr int kChunks = 128 / kCPC;           // chunks across 128 columns
+                constexpr int kGroups = 128 / kChunks;        // row groups of 8 tokens (= kBK / 8)
+                const int chunk = t % kChunks, blk = chunk >> 3, ch = chunk & 7, r0 = (t / kChunks) * 8;
+                float cs[kCPC];
+#pragma unroll
+                for (int i = 0; i < kCPC; ++i) cs[i] = 0.f;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
-                    const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes) + blk * 64 * 128;
+                    const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes) + blk * KT::kBK * 128;
 #pragma unroll
                     for (int r = r0; r < r0 + 8; ++r) {
                         uint32_t w[4];
+                        // physical 16-B chunk: 128B swizzle (bf16) / 128B-atom-32B swizzle (tf32)
+                        const uint32_t pch = kKind == 0 ? (uint32_t)(ch ^ (r & 7))
+                                                        : (uint32_t)((((ch >> 1) ^ (r & 3)) << 1) | (ch & 1));
                         asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
                                      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
-                                     : "r"(b_addr + r * 128 + ((uint32_t)(ch ^ (r & 7)) << 4)));
+                                     : "r"(b_addr + r * 128 + (pch << 4)));
+                        if constexpr (kKind == 0) {
 #pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
-                            cs[2 * i] += f.x;
-                            cs[2 * i + 1] += f.y;
+                            for (int i = 0; i < 4; ++i) {
+                                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[i]));
+                                cs[2 * i] += f.x;
+                                cs[2 * i + 1] += f.y;
+                            }
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) cs[i] += __uint_as_float(w[i]);
                         }
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[stage]);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
-                // combine the 8 row groups in order -> cpart[nt][split][rank*128 + col]
+                // combine the row groups in order -> cpart[nt][split][rank*128 + col]
 #pragma unroll
-                for (int i = 0; i < 8; ++i) csum_s[(t >> 4) * 128 + chunk * 8 + i] = cs[i];
+                for (int i = 0; i < kCPC; ++i) csum_s[(t / kChunks) * 128 + chunk * kCPC + i] = cs[i];
                 named_bar_sync(2, 128);
                 {
                     float s = 0.f;
 #pragma unroll
-                    for (int g = 0; g < 8; ++g) s += csum_s[g * 128 + t];
+                    for (int g = 0; g < kGroups; ++g) s += csum_s[g * 128 + t];
                     __stcg(args.cpart + ((long long)x.nt * args.splits + x.split) * kDuBN + rank * 128 + t, s);
                 }
                 named_bar_sync(2, 128);

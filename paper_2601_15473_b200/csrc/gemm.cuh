@@ -41,6 +41,7 @@ struct GemmArgs {
     long long ldo2;
     int out2_c0, out2_c1;
     int out_f32;  // 1: fp32 output, 0: bf16 output
+    int round_tf32;  // 1: round direct-mode outputs to TF32 (cvt.rna) -- they feed a TF32 GEMM
     // split-K mode
     float* partial;  // [splits][M][N] fp32
 };
@@ -246,6 +247,10 @@ __global__ void __launch_bounds__(256, 1)
                 load_bias16(args.bias, n, args.N, bv);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], args.alpha, bv[j]);
+                if (args.round_tf32) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) v[j] = tf32_rna(v[j]);
+                }
                 const int nvalid = min(16, args.N - n);
                 // columns [out2_c0, out2_c1) also go out transposed: out2[(n - c0) * ldo2 + row]
                 if (args.out2 && n + 16 > args.out2_c0 && n < args.out2_c1) {

@@ -97,7 +97,7 @@ EncodeFn get_encode() {
 // 2-D view: `inner` contiguous elements per row, `outer` rows `ld` elements
 // apart; box {box_inner, box_outer}; 128B swizzle; OOB reads return zero.
 skl_status make_tmap(CUtensorMap* m, const void* ptr, int elem_bytes, int64_t inner, int64_t outer, int64_t ld,
-                     int box_inner, int box_outer) {
+                     int box_inner, int box_outer, CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
     EncodeFn enc = get_encode();
     if (!enc) return fail(SKL_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || ((ld * elem_bytes) & 15) != 0)
@@ -108,7 +108,7 @@ skl_status make_tmap(CUtensorMap* m, const void* ptr, int elem_bytes, int64_t in
     cuuint32_t es[2] = {1, 1};
     CUresult r = enc(m, elem_bytes == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                      const_cast<void*>(ptr), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS)
         return fail(SKL_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): inner=%lld outer=%lld ld=%lld box=%dx%d",
@@ -169,6 +169,13 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     return SKL_OK;
 }
 
+// K-major x K-major GEMM in the variant's MMA kind (0 bf16, 1 tf32).
+skl_status gemm_any(int kind, const char* name, const View& A, const View& B, int M, int N, int K, GemmArgs args,
+                    int sms, cudaStream_t st) {
+    if (kind == 0) return run_gemm<1, 0, false, false, 256, 4>(name, A, B, M, N, K, args, sms, st);
+    return run_gemm<1, 1, false, false, 256, 4>(name, A, B, M, N, K, args, sms, st);
+}
+
 // Operand sources of the fused kernel.  kMode 0: b1 / b2 are packed panels.
 // kMode 1 (forward, direct): b1 = S1s, b1b = U2s ([L*d_in][k] views),
 //                            b2 = U1s, b2b = S2s ([L*k][d_out] views).
@@ -178,14 +185,15 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode>
+template <int kCG, int kMode, int kKind>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode>;
+    using C = dev::B2BCfg<kCG, kMode, kKind>;
+    constexpr int eb = C::kElem, bk = C::kBK;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty;
-    SKL_TRY(make_tmap(&ta, src.a1, 2, a.K1, a.T, a.K1, 64, 128));
+    SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
     if constexpr (kMode == 0) {
-        SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.R_pad, a.K1, 64, a.b1rows));
-        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.R_pad, a.N2, a.R_pad, 64, C::kB2Rows));
+        SKL_TRY(make_tmap(&tb1, src.b1, eb, a.K1, a.R_pad, a.K1, bk, a.b1rows));
+        SKL_TRY(make_tmap(&tb2, src.b2, eb, a.R_pad, a.N2, a.R_pad, bk, C::kB2Rows));
         tb1b = tb1;
         tb2b = tb2;
     } else if constexpr (kMode == 1) {
@@ -205,7 +213,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         SKL_TRY(make_tmap(&tb2, src.b2, 2, a.k, srows, a.k, 64, C::kB2Rows));
         SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.k, srows, a.k, 64, C::kB2Rows));
     }
-    SKL_TRY(make_tmap(&ty, a.out, 2, a.N2, a.T, a.ldo, 64, 128));
+    SKL_TRY(make_tmap(&ty, a.out, eb, a.N2, a.T, a.ldo, bk, 128));
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     static const int grid_cap = [] {  // SKL_B2B_GRID: cap on CTAs (experiments)
         const char* e = getenv("SKL_B2B_GRID");
@@ -213,7 +221,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     }();
     if (grid_cap > 0) sms = std::min(sms, grid_cap);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
-    auto kern = dev::b2b_kernel<kCG, kMode>;
+    auto kern = dev::b2b_kernel<kCG, kMode, kKind>;
     static bool attr_set = false;
     if (!attr_set) {
         SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -240,7 +248,7 @@ int g_b2b_cg = 2;       // CTA-group width of the fused kernel (SKL_B2B_CG=1 for
 int g_b2b_direct = 1;   // read the ABI stacks directly when k % 64 == 0 (SKL_B2B_PACKED=1 disables)
 
 skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    if (kind != 0) return fail(SKL_ERR_UNSUPPORTED, "fused kernel is bf16-only");
+    if (kind != 0 && mode != 0) return fail(SKL_ERR_UNSUPPORTED, "the TF32 fused kernel streams packed panels");
     static const int dbg = [] {
         const char* e = getenv("SKL_B2B_DEBUG");
         return e ? atoi(e) : 0;
@@ -257,14 +265,18 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         while (r > 8 && !ok(r)) r /= 2;
         a.b1rows = r;
     }
-    if (g_b2b_cg == 2) {
-        if (mode == 1) return run_b2b_cg<2, 1>(name, src, a, sms, st);
-        if (mode == 2) return run_b2b_cg<2, 2>(name, src, a, sms, st);
-        return run_b2b_cg<2, 0>(name, src, a, sms, st);
+    if (kind == 1) {
+        if (g_b2b_cg == 2) return run_b2b_cg<2, 0, 1>(name, src, a, sms, st);
+        return run_b2b_cg<1, 0, 1>(name, src, a, sms, st);
     }
-    if (mode == 1) return run_b2b_cg<1, 1>(name, src, a, sms, st);
-    if (mode == 2) return run_b2b_cg<1, 2>(name, src, a, sms, st);
-    return run_b2b_cg<1, 0>(name, src, a, sms, st);
+    if (g_b2b_cg == 2) {
+        if (mode == 1) return run_b2b_cg<2, 1, 0>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2, 0>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0, 0>(name, src, a, sms, st);
+    }
+    if (mode == 1) return run_b2b_cg<1, 1, 0>(name, src, a, sms, st);
+    if (mode == 2) return run_b2b_cg<1, 2, 0>(name, src, a, sms, st);
+    return run_b2b_cg<1, 0, 0>(name, src, a, sms, st);
 }
 
 void read_b2b_env() {
@@ -281,7 +293,7 @@ void read_b2b_env() {
 bool direct_ok(const SklDims& d, skl_dtype t) {
     read_b2b_env();
     return g_b2b_direct && t == SKL_BF16 && d.k % 64 == 0 && d.R_pad == d.R &&
-           d.d_out <= dev::B2BCfg<2, 1>::kMaxBiasTab;
+           d.d_out <= dev::B2BCfg<2, 1, 0>::kMaxBiasTab;
 }
 
 int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
@@ -351,14 +363,15 @@ int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
 struct DuShape {
     int m0, n0t, m1, n1t, tiles, splits, kb;
 };
-DuShape du_shape(const SklDims& d, int64_t T, int sms) {
+DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind) {
     DuShape s;
     s.m0 = (int)((d.Lk + 255) / 256);
     s.n0t = (int)((d.d_out + 255) / 256);
     s.m1 = (int)((d.Lk + 255) / 256);
     s.n1t = (int)((d.d_in + 255) / 256);
     s.tiles = s.m0 * s.n0t + s.m1 * s.n1t;
-    s.kb = (int)std::max<int64_t>(1, (T + 63) / 64);
+    const int bkt = kind == 0 ? 64 : 32;  // tokens per k-block
+    s.kb = (int)std::max<int64_t>(1, (T + bkt - 1) / bkt);
     s.splits = std::max(1, std::min((sms / 2) / s.tiles, std::max(1, s.kb / 2)));
     return s;
 }
@@ -384,7 +397,7 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
     p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
     if (bwd) {
-        const DuShape u = du_shape(d, T, sms);
+        const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1);
         p.du_part = take((size_t)u.tiles * u.splits * 256 * 256 * 4);
         p.du_cpart = take((size_t)u.n0t * u.splits * 256 * 4);
         p.du_tickets = take((size_t)u.tiles * 4);
@@ -533,12 +546,10 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g1.out2_c0 = 0;
     g1.out2_c1 = (int)d.Lk;
     g1.out_f32 = eb == 4;
+    g1.round_tf32 = eb == 4;  // H feeds a TF32 GEMM: round-to-nearest instead of hardware truncation
     g1.splits = 1;
     View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
-    if (s->dtype == SKL_BF16)
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
-    else
-        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st)));
+    SKL_TRY(gemm_any(eb == 4, "gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st));
     GemmArgs g2 = {};
     g2.alpha = inv;
     g2.bias = bias32;
@@ -547,10 +558,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g2.out_f32 = eb == 4;
     g2.splits = 1;
     View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
-    if (s->dtype == SKL_BF16)
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
-    else
-        SKL_TRY((run_gemm<1, 1, false, false, 256, 4>("gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st)));
+    SKL_TRY(gemm_any(eb == 4, "gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st));
     return SKL_OK;
 }
 
@@ -576,9 +584,9 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         if (grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
         return SKL_OK;
     }
-    if (s->dtype != SKL_BF16)
-        return fail(SKL_ERR_UNSUPPORTED, "the TF32 (fp32 I/O) backward is not implemented yet; use SKL_BF16");
     const int elem = elem_of(s->dtype);
+    const int eb = ebytes(s->dtype);
+    const int kind = s->dtype == SKL_BF16 ? 0 : 1;
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
     const int64_t ldt = t8(T);
     void* acat = at<void>(workspace, p.acat);
@@ -602,9 +610,11 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         g.ldo2 = ldt;
         g.out2_c0 = 0;
         g.out2_c1 = (int)d.Lk;
+        g.out_f32 = eb == 4;
+        g.round_tf32 = kind;
         g.splits = 1;
         View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st)));
+        SKL_TRY(gemm_any(kind, "gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st));
         saved = sv;
     }
 
@@ -630,7 +640,7 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         if (bwd_direct)
             SKL_TRY(run_b2b("b2b_bwd", 0, 2, B2BSrc{grad_y, U1s, S2s, S1s, U2s}, a, di.sms, st));
         else
-            SKL_TRY(run_b2b("b2b_bwd", 0, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
+            SKL_TRY(run_b2b("b2b_bwd", kind, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
     } else {
         GemmArgs g = {};
         g.alpha = 1.f;
@@ -640,23 +650,26 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         g.ldo2 = ldt;
         g.out2_c0 = (int)d.Lk;
         g.out2_c1 = (int)(2 * d.Lk);
+        g.out_f32 = eb == 4;
+        g.round_tf32 = kind;
         g.splits = 1;
         View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
-        SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st)));
+        SKL_TRY(gemm_any(kind, "gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st));
         if (grad_x) {
             GemmArgs g2 = {};
             g2.alpha = inv;
             g2.out = grad_x;
             g2.ldo = d.d_in;
+            g2.out_f32 = eb == 4;
             g2.splits = 1;
             View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
-            SKL_TRY((run_gemm<1, 0, false, false, 256, 4>("gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st)));
+            SKL_TRY(gemm_any(kind, "gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st));
         }
     }
 
     // dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
     // ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.
-    const DuShape u = du_shape(d, T, di.sms);
+    const DuShape u = du_shape(d, T, di.sms, kind);
     DuArgs a = {};
     a.k_blocks = u.kb;
     a.splits = u.splits;
@@ -668,16 +681,20 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     a.part = at<float>(workspace, p.du_part);
     a.cpart = at<float>(workspace, p.du_cpart);
     a.tickets = at<int>(workspace, p.du_tickets);
+    const int bkt = 128 / eb;  // tokens per k-block (= columns per MN-major block)
     CUtensorMap ta0, tb0, ta1, tb1;
-    SKL_TRY(make_tmap(&ta0, saved, 2, T, d.Lk, ldt, 64, 128));           // Savedᵀ, K-major
-    SKL_TRY(make_tmap(&tb0, grad_y, 2, d.d_out, T, d.d_out, 64, 64));    // G, MN-major
-    SKL_TRY(make_tmap(&ta1, p2t, 2, T, d.Lk, ldt, 64, 128));             // P_S2ᵀ, K-major
-    SKL_TRY(make_tmap(&tb1, x, 2, d.d_in, T, d.d_in, 64, 64));           // X, MN-major
+    SKL_TRY(make_tmap(&ta0, saved, eb, T, d.Lk, ldt, bkt, 128));            // Savedᵀ, K-major
+    // MN-major TF32 tiles use the 32-B-atom 128B swizzle (UMMA layout SWIZZLE_128B_BASE32B)
+    const CUtensorMapSwizzle mn_swz = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    SKL_TRY(make_tmap(&tb0, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));  // G, MN-major
+    SKL_TRY(make_tmap(&ta1, p2t, eb, T, d.Lk, ldt, bkt, 128));                    // P_S2ᵀ, K-major
+    SKL_TRY(make_tmap(&tb1, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));         // X, MN-major
     SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
-    static bool attr_set = false;
-    if (!attr_set) {
-        SKL_CUDA(cudaFuncSetAttribute(dev::du_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
-        attr_set = true;
+    auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[kind]) {
+        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
+        attr_set[kind] = true;
     }
     const int units = u.tiles * u.splits;  // CTA pairs
     a.relay = grad_bias ? 1 : 0;
@@ -698,13 +715,13 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     cfg.attrs = attr;
     cfg.numAttrs = 2;
     ProfScope ps_("du_fused", st);
-    cudaError_t le = cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
     if (le != cudaSuccess && a.coop) {  // cooperative + cluster refused: last-CTA reduction instead
         (void)cudaGetLastError();
         a.coop = 0;
         attr[1].val.cooperative = 0;
         cfg.gridDim = dim3(2 * std::min(di.sms / 2, units));
-        le = cudaLaunchKernelEx(&cfg, dev::du_kernel, ta0, tb0, ta1, tb1, a);
+        le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
     }
     SKL_CUDA(le);
     return SKL_OK;

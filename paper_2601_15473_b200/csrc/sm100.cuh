@@ -255,13 +255,17 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t
 //  K-major : rows of 128 B (one swizzle atom along K), 8-row groups SBO apart.
 //  MN-major: 128 B rows along MN (64 bf16 / 32 fp32), K rows 128 B apart,
 //            8-row K groups SBO apart, 128-B-wide MN blocks LBO apart.
-__device__ __forceinline__ uint64_t make_sdesc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+//  layout 2 = SWIZZLE_128B (16-B atoms, 8-row period); layout 1 =
+//  SWIZZLE_128B_BASE32B (32-B atoms, 4-row period; TMA ..._128B_ATOM_32B),
+//  the form MN-major TF32 operands require (SBO = 512 B between 4-row K groups).
+__device__ __forceinline__ uint64_t make_sdesc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                               uint32_t layout = 2) {
     uint64_t d = 0;
     d |= (uint64_t)((smem_addr >> 4) & 0x3FFFu);
     d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFFu) << 16;
     d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFFu) << 32;
     d |= (uint64_t)1 << 46;  // version
-    d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+    d |= (uint64_t)layout << 61;
     return d;
 }
 

@@ -163,3 +163,64 @@ def test_backward_parity_bf16(skl, port, d_in, d_out, L, k, T):
     torch.cuda.synchronize()
     check_close("dU1s(recompute)", _np(du1b), rgu1, "bf16")
     check_close("dU2s(recompute)", _np(du2b), rgu2, "bf16")
+
+
+# --------------------------------------------------------------------------- TF32 (fp32 I/O)
+TF32_CASES = [
+    (1024, 1024, 1, 64, 64),       # c1 shape (fused, R = 128)
+    (256, 512, 2, 64, 300),        # R = 256 (fused, widest on-chip TF32 H), ragged
+    (768, 3072, 2, 128, 200),      # c2 shape, R = 512 (TF32 H through HBM)
+    (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
+    (96, 160, 3, 8, 77),           # k % 64 != 0, odd tokens
+]
+
+
+@pytest.mark.parametrize("d_in,d_out,L,k,T", TF32_CASES)
+def test_forward_backward_parity_tf32(skl, port, d_in, d_out, L, k, T):
+    """fp32-in/fp32-out TF32 variant vs the f64 oracle: rel_fro <= 2e-3 and
+    max_abs <= 2e-3 * max|ref| on y, grad_x, dU1s, dU2s, db (tests/_util.py)."""
+    import oracle
+    from tests._util import check_close
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.F32_TF32)
+    y = torch.empty(T, d_out, device="cuda")
+    saved = torch.empty(L * k, (T + 7) // 8 * 8, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    gx = torch.empty(T, d_in, device="cuda")
+    du1 = torch.empty(L, k, d_out, device="cuda")
+    du2 = torch.empty(L, d_in, k, device="cuda")
+    db = torch.empty(d_out, device="cuda")
+    skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+    torch.cuda.synchronize()
+    check_close("y(tf32)", _np(y), port.forward(P, b64, x64).T, "tf32")
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    check_close("grad_x(tf32)", _np(gx), rgx, "tf32")
+    check_close("dU1s(tf32)", _np(du1), rgu1, "tf32")
+    check_close("dU2s(tf32)", _np(du2), rgu2, "tf32")
+    check_close("db(tf32)", _np(db), rgb, "tf32")
+    # recompute path (no saved projection)
+    du1b, du2b = torch.empty_like(du1), torch.empty_like(du2)
+    skl.backward(s, G, X, None, S1s, S2s, U1s, U2s, None, du1b, du2b, None, ws)
+    torch.cuda.synchronize()
+    check_close("dU1s(tf32, recompute)", _np(du1b), rgu1, "tf32")
+    check_close("dU2s(tf32, recompute)", _np(du2b), rgu2, "tf32")
+
+
+def test_backward_is_deterministic(skl, port):
+    """Split-T reduction order is fixed: two runs are bitwise identical."""
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, 768, 3072, 2, 128, 4096, skl.BF16)
+    ws = torch.empty(max(skl.workspace_size(s, 4096)), dtype=torch.uint8, device="cuda")
+    saved = torch.empty(256, 4096, dtype=torch.bfloat16, device="cuda")
+    y = torch.empty(4096, 3072, dtype=torch.bfloat16, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    outs = []
+    for _ in range(2):
+        gx = torch.empty(4096, 768, dtype=torch.bfloat16, device="cuda")
+        du1 = torch.empty(2, 128, 3072, device="cuda")
+        du2 = torch.empty(2, 768, 128, device="cuda")
+        db = torch.empty(3072, device="cuda")
+        skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+        outs.append((gx, du1, du2, db))
+    torch.cuda.synchronize()
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
