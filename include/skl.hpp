@@ -1,0 +1,236 @@
+/*
+ * skl.hpp -- C++ host mirror of rnla::nn::SkLinear over the C-ABI (skl.h).
+ *
+ * Reference interface this mirrors (/root/reference/proj):
+ *   class SkLinear { forward(x) -> Matrix; backward(x, grad_out) -> Grads; params(); }
+ *                                                     include/rnla/nn/layers.hpp:52-81
+ *   sk_linear_fresh(d_in, d_out, l, k, seed, dist)    layers.hpp:85-88, nn_layers.cpp:133-147
+ *   SketchOp::with_realized (test hook: explicit sketches) sketch.hpp:36-38
+ *   shape_error / parameter_error                     include/rnla/errors.hpp:10-19
+ *
+ * Same names, same argument meaning, same error behaviour (exceptions of the
+ * same names), but DEVICE-resident and row convention (x [T, d_in]) with the
+ * pawX [L, d, k] stacks of skl.h.  No PyTorch: memory is cudaMalloc'ed here,
+ * all arithmetic runs in libskl.so's sm_100a kernels.  Header-only; link
+ * with -lskl -lcudart.
+ */
+#ifndef SKL_HPP_
+#define SKL_HPP_
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "skl.h"
+
+namespace skl {
+
+// ---------------------------------------------------------------- errors (errors.hpp:10-19)
+struct shape_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct parameter_error : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct cuda_error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void check(skl_status s) {
+    if (s == SKL_OK) return;
+    const std::string msg = skl_last_error();
+    if (s == SKL_ERR_SHAPE) throw shape_error(msg);
+    if (s == SKL_ERR_PARAM) throw parameter_error(msg);
+    throw cuda_error(msg);
+}
+inline void check_cuda(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw cuda_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+inline size_t elem_bytes(skl_dtype t) { return t == SKL_BF16 ? 2 : 4; }
+
+// ---------------------------------------------------------------- device memory (RAII)
+class DeviceBuffer {
+  public:
+    DeviceBuffer() = default;
+    explicit DeviceBuffer(size_t bytes) : bytes_(bytes) {
+        if (bytes_) check_cuda(cudaMalloc(&ptr_, bytes_), "cudaMalloc");
+    }
+    ~DeviceBuffer() {
+        if (ptr_) cudaFree(ptr_);
+    }
+    DeviceBuffer(const DeviceBuffer&) = delete;
+    DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+    DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(std::exchange(o.ptr_, nullptr)), bytes_(std::exchange(o.bytes_, 0)) {}
+    DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+        if (this != &o) {
+            if (ptr_) cudaFree(ptr_);
+            ptr_ = std::exchange(o.ptr_, nullptr);
+            bytes_ = std::exchange(o.bytes_, 0);
+        }
+        return *this;
+    }
+    void* get() const { return ptr_; }
+    template <class T>
+    T* as() const { return static_cast<T*>(ptr_); }
+    size_t bytes() const { return bytes_; }
+    void upload(const void* host, size_t n, cudaStream_t st = nullptr) {
+        check_cuda(cudaMemcpyAsync(ptr_, host, n, cudaMemcpyHostToDevice, st), "upload");
+    }
+    void download(void* host, size_t n, cudaStream_t st = nullptr) const {
+        check_cuda(cudaMemcpyAsync(host, ptr_, n, cudaMemcpyDeviceToHost, st), "download");
+    }
+    void zero(cudaStream_t st = nullptr) {
+        if (bytes_) check_cuda(cudaMemsetAsync(ptr_, 0, bytes_, st), "memset");
+    }
+
+  private:
+    void* ptr_ = nullptr;
+    size_t bytes_ = 0;
+};
+
+// ---------------------------------------------------------------- SkLinear
+class SkLinear {
+  public:
+    // SkLinear::Grads (layers.hpp:72-78) in ABI layout: grad_x [T, d_in]
+    // (element type of the variant), grad_u1 = dU1s [L,k,d_out], grad_u2 =
+    // dU2s [L,d_in,k], grad_b [d_out] (fp32).
+    struct Grads {
+        DeviceBuffer grad_x, grad_u1, grad_u2, grad_b;
+    };
+
+    // sk_linear_fresh (nn_layers.cpp:133-147): sketches from derive_seed(seed,
+    // 2i / 2i+1), U ~ N(0, 2/(d_in+d_out)) from derive_seed(seed, 1000+i),
+    // zero bias -- generated on the device, bit-matching the reference stream.
+    static SkLinear fresh(int64_t d_in, int64_t d_out, int64_t l, int64_t k, uint64_t seed,
+                          skl_dist dist = SKL_DIST_GAUSSIAN, skl_dtype dtype = SKL_BF16,
+                          cudaStream_t st = nullptr) {
+        SkLinear s(d_in, d_out, l, k, dtype);
+        check(skl_generate_sketches(&s.shape_, dist, seed, s.S1s_.get(), s.S2s_.get(), st));
+        check(skl_init_params(&s.shape_, seed, s.U1s_.get(), s.U2s_.get(), st));
+        s.bias_.zero(st);
+        return s;
+    }
+
+    // Explicit parameters (host arrays in the variant's element type, ABI
+    // layouts) -- the analogue of SketchOp::with_realized (sketch.hpp:36-38).
+    static SkLinear with_params(int64_t d_in, int64_t d_out, int64_t l, int64_t k, skl_dtype dtype,
+                                const void* S1s, const void* S2s, const void* U1s, const void* U2s,
+                                const void* bias /*nullable*/, cudaStream_t st = nullptr) {
+        SkLinear s(d_in, d_out, l, k, dtype);
+        const size_t e = elem_bytes(dtype);
+        s.S1s_.upload(S1s, (size_t)(l * d_in * k) * e, st);
+        s.S2s_.upload(S2s, (size_t)(l * k * d_out) * e, st);
+        s.U1s_.upload(U1s, (size_t)(l * k * d_out) * e, st);
+        s.U2s_.upload(U2s, (size_t)(l * d_in * k) * e, st);
+        if (bias) s.bias_.upload(bias, (size_t)d_out * e, st);
+        else s.bias_.zero(st);
+        return s;
+    }
+
+    int64_t d_in() const { return shape_.d_in; }
+    int64_t d_out() const { return shape_.d_out; }
+    int64_t num_terms() const { return shape_.num_terms; }
+    int64_t low_rank() const { return shape_.low_rank; }
+    skl_dtype dtype() const { return shape_.dtype; }
+    const skl_shape& shape() const { return shape_; }
+
+    void* S1s() const { return S1s_.get(); }
+    void* S2s() const { return S2s_.get(); }
+    void* U1s() const { return U1s_.get(); }
+    void* U2s() const { return U2s_.get(); }
+    void* bias() const { return bias_.get(); }
+
+    // SkLinear::params (nn_layers.cpp:103-110)
+    skl_param_count params() const {
+        skl_param_count pc;
+        check(skl_params(&shape_, &pc));
+        return pc;
+    }
+
+    // Row stride (elements) of the saved projection [L*k][round8(T)].
+    static int64_t saved_ld(int64_t T) { return (T + 7) / 8 * 8; }
+    size_t saved_bytes(int64_t T) const {
+        return (size_t)(shape_.num_terms * shape_.low_rank) * (size_t)saved_ld(T) * elem_bytes(shape_.dtype);
+    }
+
+    // SkLinear::forward (nn_layers.cpp:61-76), device pointers:
+    // x [T, d_in] -> y [T, d_out]; saved (nullable) [L*k][round8(T)] keeps x·S1_i.
+    void forward(const void* x, int64_t T, void* y, void* saved = nullptr, cudaStream_t st = nullptr) const {
+        if (T < 0) throw shape_error("SkLinear::forward: negative token count");
+        void* ws = workspace(T, st);
+        check(sketched_linear_forward(&shape_, T, x, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(), bias_.get(), y,
+                                      saved, ws, ws_.bytes(), st));
+    }
+
+    // SkLinear::backward (nn_layers.cpp:78-101): gradients allocated here.
+    Grads backward(const void* x, const void* grad_out, int64_t T, const void* saved = nullptr,
+                   cudaStream_t st = nullptr) const {
+        Grads g{DeviceBuffer((size_t)(T * shape_.d_in) * elem_bytes(shape_.dtype)),
+                DeviceBuffer((size_t)(shape_.num_terms * shape_.low_rank * shape_.d_out) * 4),
+                DeviceBuffer((size_t)(shape_.num_terms * shape_.low_rank * shape_.d_in) * 4),
+                DeviceBuffer((size_t)shape_.d_out * 4)};
+        backward_into(x, grad_out, T, saved, g.grad_x.get(), g.grad_u1.as<float>(), g.grad_u2.as<float>(),
+                      g.grad_b.as<float>(), st);
+        return g;
+    }
+
+    // Allocation-free backward into caller buffers (e.g. one contiguous
+    // dU1s | dU2s | db bucket for the NCCL all-reduce).  grad_x / grad_b nullable.
+    void backward_into(const void* x, const void* grad_out, int64_t T, const void* saved, void* grad_x, float* dU1s,
+                       float* dU2s, float* db, cudaStream_t st = nullptr) const {
+        if (T < 0) throw shape_error("SkLinear::backward: negative token count");
+        void* ws = workspace(T, st);
+        check(sketched_linear_backward(&shape_, T, grad_out, x, saved, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(),
+                                       grad_x, dU1s, dU2s, db, ws, ws_.bytes(), st));
+    }
+
+    // Host-buffer convenience (the reference's value-semantics call):
+    // x_host [T, d_in] in the variant's element type -> y_host [T, d_out].
+    std::vector<uint8_t> forward_host(const void* x_host, int64_t T, cudaStream_t st = nullptr) const {
+        const size_t e = elem_bytes(shape_.dtype);
+        DeviceBuffer x((size_t)(T * shape_.d_in) * e), y((size_t)(T * shape_.d_out) * e);
+        x.upload(x_host, x.bytes(), st);
+        forward(x.get(), T, y.get(), nullptr, st);
+        std::vector<uint8_t> out(y.bytes());
+        y.download(out.data(), out.size(), st);
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        return out;
+    }
+
+  private:
+    SkLinear(int64_t d_in, int64_t d_out, int64_t l, int64_t k, skl_dtype dtype) {
+        if (l < 1 || k < 1) throw parameter_error("SkLinear: l and k must be >= 1");  // nn_layers.cpp:116
+        if (d_in < 1 || d_out < 1) throw shape_error("SkLinear: d_in and d_out must be >= 1");
+        shape_ = skl_shape{d_in, d_out, l, k, dtype};
+        const size_t e = elem_bytes(dtype);
+        S1s_ = DeviceBuffer((size_t)(l * d_in * k) * e);
+        U2s_ = DeviceBuffer((size_t)(l * d_in * k) * e);
+        U1s_ = DeviceBuffer((size_t)(l * k * d_out) * e);
+        S2s_ = DeviceBuffer((size_t)(l * k * d_out) * e);
+        bias_ = DeviceBuffer((size_t)d_out * e);
+    }
+
+    void* workspace(int64_t T, cudaStream_t st) const {
+        size_t f = 0, b = 0;
+        check(skl_workspace_size(&shape_, T, &f, &b));
+        const size_t need = f > b ? f : b;
+        if (ws_.bytes() < need) {
+            check_cuda(cudaStreamSynchronize(st), "sync");  // the old workspace may still be in use
+            ws_ = DeviceBuffer(need);
+        }
+        return ws_.get();
+    }
+
+    skl_shape shape_{};
+    DeviceBuffer S1s_, S2s_, U1s_, U2s_, bias_;
+    mutable DeviceBuffer ws_;
+};
+
+}  // namespace skl
+
+#endif  // SKL_HPP_
