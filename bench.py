@@ -10,7 +10,10 @@ of synthetic tokens, through the C-ABI of libskl.so:
     d_in=768, d_out=3072, L=2, k=128, 32768 tokens per GPU, bf16.
 Multi-GPU: token sharding (weak scaling, 32768 tokens per GPU); forward needs
 no communication; the backward all-reduces the fp32 gradient bucket
-(dU1s | dU2s | db) with NCCL.  Rank 0 prints one JSON line.
+(dU1s | db | dU2s) with NCCL, the dU1s | db part overlapped with the dX kernel.
+Rank 0 prints one JSON line.  At N=1 the line also carries "workloads": the
+other BASELINE.json configs (c1, c2-TF32, c3, c4 sweep) measured briefly, each
+with its own binding-roofline fraction.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/librnla_ref.so: the unmodified reference sources, timed by the
@@ -37,6 +40,7 @@ SEED = 42
 WORKLOAD = (f"c2: SKLinear fwd+bwd d_in={D_IN} d_out={D_OUT} L={L} k={K_RANK}, "
             f"{T_GPU} tokens per GPU (BERT-base FFN shape)")
 CPU_SAMPLE_T = 1024  # tokens per reference CPU step (bounded sample of the same workload)
+RESERVED_SMS = 8     # SMs left to NCCL when N > 1 (NCCL_MAX_CTAS matches)
 
 
 def peaks():
@@ -138,6 +142,83 @@ def cpu_baseline_reference(t_sample=CPU_SAMPLE_T, trials=3, warmup=1):
                       f"(bench::time_op), {mean_ms:.1f} ms/step"}
 
 
+# Other BASELINE.json configs (parity-tested in tests/; reported, not the headline):
+#   name, d_in, d_out, L, k, tokens, dtype
+SWEEP = [
+    ("c1 fp32/TF32 1024->1024 L1 k64 T64", 1024, 1024, 1, 64, 64, "tf32"),
+    ("c2 TF32 768->3072 L2 k128 T32768", 768, 3072, 2, 128, 32768, "tf32"),
+    ("c3 bf16 4096->4096 L3 k256 T65536", 4096, 4096, 3, 256, 65536, "bf16"),
+    ("c4 bf16 4096 L1 k16 T131072", 4096, 4096, 1, 16, 131072, "bf16"),
+    ("c4 bf16 4096 L2 k32 T131072", 4096, 4096, 2, 32, 131072, "bf16"),
+    ("c4 bf16 4096 L4 k64 T131072", 4096, 4096, 4, 64, 131072, "bf16"),
+    ("c4 TF32 4096 L1 k16 T131072", 4096, 4096, 1, 16, 131072, "tf32"),
+    ("c4 TF32 4096 L2 k64 T131072", 4096, 4096, 2, 64, 131072, "tf32"),
+]
+
+
+def roofline_time(d_in, d_out, l, k, T, ebytes, peak_tf, peak_bw):
+    """Binding roofline of one fwd+bwd step (SURVEY §8d): FLOPs 5·R·D per token;
+    algorithmic bytes (2D + d_in + 2Lk)·e per token (fwd: X, Y, saved; bwd: G,
+    X, saved, dX) -- params/grads are per-call and negligible."""
+    R, D = 2 * l * k, d_in + d_out
+    flops = 5 * R * D * T
+    bytes_ = (2 * D + d_in + 2 * l * k) * ebytes * T
+    t_tensor, t_hbm = flops / (peak_tf * 1e12), bytes_ / (peak_bw * 1e9)
+    return max(t_tensor, t_hbm), ("tensor" if t_tensor >= t_hbm else "hbm"), flops, bytes_
+
+
+def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=10, warmup=3, phased=False):
+    kind = skl.BF16 if dtype == "bf16" else skl.F32_TF32
+    td = torch.bfloat16 if dtype == "bf16" else torch.float32
+    s = skl.shape(d_in, d_out, l, k, kind)
+    S1s = torch.empty(l, d_in, k, dtype=td, device=dev)
+    S2s = torch.empty(l, k, d_out, dtype=td, device=dev)
+    U1s = torch.empty(l, k, d_out, dtype=td, device=dev)
+    U2s = torch.empty(l, d_in, k, dtype=td, device=dev)
+    skl.generate_sketches(s, skl.GAUSSIAN, SEED, S1s, S2s)
+    skl.init_params(s, SEED, U1s, U2s)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(7)
+    bias = torch.randn(d_out, device=dev, generator=gen).to(td)
+    X = torch.randn(T, d_in, device=dev, generator=gen).to(td)
+    G = torch.randn(T, d_out, device=dev, generator=gen).to(td)
+    Y = torch.empty(T, d_out, dtype=td, device=dev)
+    GX = torch.empty(T, d_in, dtype=td, device=dev)
+    saved = torch.empty(l * k, (T + 7) // 8 * 8, dtype=td, device=dev)
+    du1 = torch.empty(l, k, d_out, device=dev)
+    du2 = torch.empty(l, d_in, k, device=dev)
+    db = torch.empty(d_out, device=dev)
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device=dev)
+
+    def step():
+        skl.forward(s, X, S1s, S2s, U1s, U2s, bias, Y, saved, ws)
+        if phased:
+            skl.backward_phase(s, skl.BWD_DU1_DB, G, X, saved, S1s, S2s, U1s, U2s, None, du1, None, db, ws)
+            skl.backward_phase(s, skl.BWD_DX_DU2, G, X, saved, S1s, S2s, U1s, U2s, GX, None, du2, None, ws)
+        else:
+            skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, GX, du1, du2, db, ws)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    peak_bf16, peak_bw, _ = peaks()
+    peak_tf = peak_bf16 if dtype == "bf16" else peak_bf16 / 2  # TF32 dense = bf16 / 2 (not separately measured)
+    t_roof, bound, flops, bytes_ = roofline_time(d_in, d_out, l, k, T, 2 if dtype == "bf16" else 4, peak_tf, peak_bw)
+    return {"workload": name, "dtype": dtype, "tokens": T, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3),
+            "bound": bound, "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
+            "tflops": flops / (ms / 1e3) / 1e12, "hbm_gbs_alg": bytes_ / (ms / 1e3) / 1e9,
+            "fused": bool((2 * l * k + 63) // 64 * 64 <= (512 if dtype == "bf16" else 256)),
+            "peak_tflops_used": peak_tf, "phased_backward": phased}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -161,6 +242,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the other-config workloads at N=1")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup) if args.impl == "ours" else args.warmup
 
@@ -179,6 +261,7 @@ def main():
 
     torch.cuda.set_device(local_rank)
     if world > 1:
+        os.environ.setdefault("NCCL_MAX_CTAS", str(RESERVED_SMS))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream()
@@ -201,18 +284,21 @@ def main():
     Y = torch.empty(T, D_OUT, dtype=bf, device=dev)
     saved = torch.empty(L * K_RANK, (T + 7) // 8 * 8, dtype=bf, device=dev)  # Savedᵀ [L*k][round8(T)]
     GX = torch.empty(T, D_IN, dtype=bf, device=dev)
-    n1, n2 = L * K_RANK * D_OUT, L * D_IN * K_RANK
-    bucket = torch.empty(n1 + n2 + D_OUT, dtype=torch.float32, device=dev)  # dU1s | dU2s | db
-    dU1s = bucket[:n1].view(L, K_RANK, D_OUT)
-    dU2s = bucket[n1:n1 + n2].view(L, D_IN, K_RANK)
-    db = bucket[n1 + n2:]
+    from paper_2601_15473_b200.dp import GradBucket, backward_overlapped
+    gb = GradBucket.allocate(D_IN, D_OUT, L, K_RANK, device=dev)  # dU1s | db | dU2s (fp32)
+    bucket = gb.flat
     ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device=dev)
+    if world > 1:
+        # leave SMs for the NCCL kernel that runs concurrently with the dX kernel
+        skl.set_reserved_sms(RESERVED_SMS)
 
     def step(x=X, g=G):
         skl.forward(s, x, S1s, S2s, U1s, U2s, bias, Y, saved, ws)
-        skl.backward(s, g, x, saved, S1s, S2s, U1s, U2s, GX, dU1s, dU2s, db, ws)
-        if world > 1:
-            dist.all_reduce(bucket)
+        if world > 1:  # phased backward: all-reduce of dU1s|db overlaps the dX kernel
+            for w in backward_overlapped(skl, s, g, x, saved, S1s, S2s, U1s, U2s, GX, gb, ws):
+                w.wait()
+        else:
+            skl.backward(s, g, x, saved, S1s, S2s, U1s, U2s, GX, gb.dU1s, gb.dU2s, gb.db, ws)
 
     def barrier():
         if world > 1:
@@ -304,6 +390,22 @@ def main():
            "h2d_bytes_per_step": Xh.numel() * 2 + Gh.numel() * 2, "d2h_bytes_per_step": out_h.numel() * 4,
            "ms_per_step": ms_e2e, "path": "pinned host X,G -> sketched_linear_forward/backward -> grads to host"}
 
+    workloads = None
+    if world == 1 and not args.no_sweep:
+        workloads = []
+        for (name, di, do, l, k, tt, dt) in SWEEP:
+            try:
+                workloads.append(measure_workload(skl, torch, dev, name, di, do, l, k, tt, dt))
+            except Exception as e:  # report, never fake
+                workloads.append({"workload": name, "error": str(e)[:200]})
+            torch.cuda.empty_cache()
+        try:  # the DP schedule's phased backward (two dU launches, 8 SMs left to NCCL), no collective
+            skl.set_reserved_sms(RESERVED_SMS)
+            workloads.append(measure_workload(skl, torch, dev, "c2 bf16, DP-phased backward (8 SMs reserved)",
+                                              D_IN, D_OUT, L, K_RANK, T_GPU, "bf16", phased=True))
+        finally:
+            skl.set_reserved_sms(0)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -321,12 +423,14 @@ def main():
             "data": "synthetic (seeded Gaussian activations; sketches/U from the reference seed chain)",
             "config": {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
                        "tokens_per_gpu": T, "global_tokens": world * T,
-                       "parallelism": f"dp{world} (token sharding, NCCL all-reduce of dU1s|dU2s|db)",
+                       "parallelism": f"dp{world} (token sharding; NCCL all-reduce of dU1s|db overlapped with "
+                                      f"the dX kernel, then dU2s)",
                        "l2": "inputs larger than L2 (X 50 MB + G 201 MB read, Y 201 MB written per step)"},
             "roofline": roof,
             "step_tflops": step_roof, "step_roofline_frac": step_roof / peak_tf,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
             "kernels": per_kernel,
+            "workloads": workloads,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -34,8 +34,9 @@ ABI_SYMBOLS = (
     "skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed", "skl_params", "skl_exceeds_dense",
     "skl_generate_sketches", "skl_init_params", "skl_realize_sketch", "skl_workspace_size",
     "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads", "skl_launch_count",
-    "skl_profile_enable", "skl_profile_collect",
+    "skl_profile_enable", "skl_profile_collect", "sketched_linear_backward_phase", "skl_set_reserved_sms",
 )
+BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
 
 
 class SklError(RuntimeError):
@@ -108,6 +109,8 @@ def lib() -> ctypes.CDLL:
     L.skl_workspace_size.argtypes = [sp, i64, ctypes.POINTER(sz), ctypes.POINTER(sz)]
     L.sketched_linear_forward.argtypes = [sp, i64] + [vp] * 9 + [sz, vp]
     L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 12 + [sz, vp]
+    L.sketched_linear_backward_phase.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 12 + [sz, vp]
+    L.skl_set_reserved_sms.argtypes = [ctypes.c_int]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
     L.skl_launch_count.restype = u64
     L.skl_profile_enable.argtypes = [ctypes.c_int]
@@ -202,6 +205,22 @@ def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db,
                                           _ptr(U1s), _ptr(U2s), _ptr(grad_x), _ptr(dU1s), _ptr(dU2s), _ptr(db),
                                           _ptr(workspace), workspace.numel() if workspace is not None else 0,
                                           _stream(stream)))
+
+
+def backward_phase(s: _Shape, phases, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace,
+                   stream=None):
+    """sketched_linear_backward_phase: BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s)."""
+    T = x.shape[0]
+    _check(lib().sketched_linear_backward_phase(ctypes.byref(s), T, phases, _ptr(g), _ptr(x), _ptr(saved),
+                                                _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s), _ptr(grad_x),
+                                                _ptr(dU1s), _ptr(dU2s), _ptr(db), _ptr(workspace),
+                                                workspace.numel() if workspace is not None else 0,
+                                                _stream(stream)))
+
+
+def set_reserved_sms(n: int):
+    """Leave n SMs free for a concurrent NCCL kernel (skl_set_reserved_sms)."""
+    _check(lib().skl_set_reserved_sms(int(n)))
 
 
 @dataclass

@@ -70,10 +70,15 @@ DevInfo dev_info() {
     return d;
 }
 
+// SMs left free for concurrently running communication kernels (NCCL) --
+// skl_set_reserved_sms; kept even so CTA pairs still tile the grid.
+int g_reserved_sms = 0;
+
 skl_status check_device(DevInfo& di) {
     di = dev_info();
     if (di.sms == 0) return fail(SKL_ERR_CUDA, "no CUDA device available (libskl has no CPU fallback)");
     if (di.major != 10) return fail(SKL_ERR_CUDA, "libskl requires an sm_100 (B200) device, found sm_%d", di.major);
+    di.sms = std::max(2, (di.sms - g_reserved_sms) & ~1);
     return SKL_OK;
 }
 
@@ -363,13 +368,13 @@ int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
 struct DuShape {
     int m0, n0t, m1, n1t, tiles, splits, kb;
 };
-DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind) {
+DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) {
     DuShape s;
     s.m0 = (int)((d.Lk + 255) / 256);
     s.n0t = (int)((d.d_out + 255) / 256);
     s.m1 = (int)((d.Lk + 255) / 256);
     s.n1t = (int)((d.d_in + 255) / 256);
-    s.tiles = s.m0 * s.n0t + s.m1 * s.n1t;
+    s.tiles = ((which & 1) ? s.m0 * s.n0t : 0) + ((which & 2) ? s.m1 * s.n1t : 0);
     const int bkt = kind == 0 ? 64 : 32;  // tokens per k-block
     s.kb = (int)std::max<int64_t>(1, (T + bkt - 1) / bkt);
     s.splits = std::max(1, std::min((sms / 2) / s.tiles, std::max(1, s.kb / 2)));
@@ -411,6 +416,81 @@ template <typename Tp>
 Tp* at(void* ws, size_t off) {
     return reinterpret_cast<Tp*>(reinterpret_cast<uint8_t*>(ws) + off);
 }
+
+// dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
+// ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.  `which`:
+// bit 0 = dU1s (+ db), bit 1 = dU2s; one grouped persistent launch.
+skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* saved, const void* grad_y,
+                  const void* p2t, const void* x, float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
+                  const Plan& p, int sms, cudaStream_t st) {
+    const int eb = kind == 0 ? 2 : 4;
+    const int64_t ldt = t8(T);
+    const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    struct DevInfoLite { int sms; } di{sms};
+    const DuShape u = du_shape(d, T, sms, kind, which);
+    DuArgs a = {};
+    a.k_blocks = u.kb;
+    a.splits = u.splits;
+    a.num_tiles = u.tiles;
+    const DuProblem pu1{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
+                        (long long)1 << 40, 0, (long long)d.d_out, 1, grad_bias};
+    const DuProblem pu2{(int)d.Lk, (int)d.d_in, u.m1, u.n1t, (which & 1) ? u.m0 * u.n0t : 0, 0, inv, grad_U2s,
+                        (long long)d.k, (long long)(d.d_in * d.k), 1, (long long)d.k, nullptr};
+    const DuProblem none{0, 0, 0, 0, 1 << 30, 0, 0.f, nullptr, 1, 0, 0, 0, nullptr};
+    a.p[0] = (which & 1) ? pu1 : pu2;
+    a.p[1] = (which & 1) && (which & 2) ? pu2 : none;
+    const bool colsum = (which & 1) && grad_bias;
+    if (!(which & 1)) saved = p2t;      // unused map, any valid tensor
+    if (!(which & 2)) p2t = saved;
+    a.part = at<float>(workspace, p.du_part);
+    a.cpart = at<float>(workspace, p.du_cpart);
+    a.tickets = at<int>(workspace, p.du_tickets);
+    const int bkt = 128 / eb;  // tokens per k-block (= columns per MN-major block)
+    CUtensorMap ta0, tb0, ta1, tb1;
+    SKL_TRY(make_tmap(&ta0, saved, eb, T, d.Lk, ldt, bkt, 128));            // Savedᵀ, K-major
+    // MN-major TF32 tiles use the 32-B-atom 128B swizzle (UMMA layout SWIZZLE_128B_BASE32B)
+    const CUtensorMapSwizzle mn_swz = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    SKL_TRY(make_tmap(&tb0, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));  // G, MN-major
+    SKL_TRY(make_tmap(&ta1, p2t, eb, T, d.Lk, ldt, bkt, 128));                    // P_S2ᵀ, K-major
+    SKL_TRY(make_tmap(&tb1, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));         // X, MN-major
+    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
+    auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
+    static bool attr_set[2] = {false, false};
+    if (!attr_set[kind]) {
+        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
+        attr_set[kind] = true;
+    }
+    const int units = u.tiles * u.splits;  // CTA pairs
+    a.relay = colsum ? 1 : 0;
+    static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
+    a.coop = (!no_coop && 2 * units <= di.sms) ? 1 : 0;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * (a.coop ? units : std::min(di.sms / 2, units)));
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = dev::kDuSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeCooperative;
+    attr[1].val.cooperative = a.coop;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    ProfScope ps_("du_fused", st);
+    cudaError_t le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
+    if (le != cudaSuccess && a.coop) {  // cooperative + cluster refused: last-CTA reduction instead
+        (void)cudaGetLastError();
+        a.coop = 0;
+        attr[1].val.cooperative = 0;
+        cfg.gridDim = dim3(2 * std::min(di.sms / 2, units));
+        le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
+    }
+    SKL_CUDA(le);
+    return SKL_OK;
+}
+
 
 }  // namespace
 }  // namespace skl
@@ -566,10 +646,21 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
                                     const void* saved_proj, const void* S1s, const void* S2s, const void* U1s,
                                     const void* U2s, void* grad_x, float* grad_U1s, float* grad_U2s,
                                     float* grad_bias, void* workspace, size_t ws_bytes, void* stream) {
+    return sketched_linear_backward_phase(s, T, SKL_BWD_ALL, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x,
+                                          grad_U1s, grad_U2s, grad_bias, workspace, ws_bytes, stream);
+}
+
+skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigned phases, const void* grad_y,
+                                          const void* x, const void* saved_proj, const void* S1s, const void* S2s,
+                                          const void* U1s, const void* U2s, void* grad_x, float* grad_U1s,
+                                          float* grad_U2s, float* grad_bias, void* workspace, size_t ws_bytes,
+                                          void* stream) {
     SklDims d;
     SKL_TRY(get_dims(s, d));
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::backward: T must be >= 0");
-    if (!grad_y || !x || !S1s || !S2s || !U1s || !U2s || !grad_U1s || !grad_U2s)
+    if (phases == 0 || (phases & ~(unsigned)SKL_BWD_ALL)) return fail(SKL_ERR_PARAM, "bad phase mask %u", phases);
+    const bool ph_u1 = (phases & SKL_BWD_DU1_DB) != 0, ph_data = (phases & SKL_BWD_DX_DU2) != 0;
+    if (!grad_y || !x || !S1s || !S2s || !U1s || !U2s || (ph_u1 && !grad_U1s) || (ph_data && !grad_U2s))
         return fail(SKL_ERR_PARAM, "null tensor argument");
     SKL_TRY(check_alignment(d, s->dtype));
     DevInfo di;
@@ -579,9 +670,9 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         return fail(SKL_ERR_WORKSPACE, "backward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
     cudaStream_t st = (cudaStream_t)stream;
     if (T == 0) {  // empty batch: all gradients are zero (sums over no tokens)
-        SKL_CUDA(cudaMemsetAsync(grad_U1s, 0, (size_t)d.Lk * d.d_out * 4, st));
-        SKL_CUDA(cudaMemsetAsync(grad_U2s, 0, (size_t)d.Lk * d.d_in * 4, st));
-        if (grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
+        if (ph_u1) SKL_CUDA(cudaMemsetAsync(grad_U1s, 0, (size_t)d.Lk * d.d_out * 4, st));
+        if (ph_data) SKL_CUDA(cudaMemsetAsync(grad_U2s, 0, (size_t)d.Lk * d.d_in * 4, st));
+        if (ph_u1 && grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
         return SKL_OK;
     }
     const int elem = elem_of(s->dtype);
@@ -596,13 +687,15 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
     void* p2t = at<void>(workspace, p.p2t);
     const bool fused = use_fused(d, s->dtype);
     const bool bwd_direct = fused && grad_x != nullptr && direct_ok(d, s->dtype);
-    if (!bwd_direct || !saved_proj)
-        SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, acat, bcat, saved_proj ? nullptr : acatT, nullptr, nullptr,
-                              nullptr, st));
+    const bool need_saved = ph_u1 && !saved_proj;
+    if ((ph_data && !bwd_direct) || need_saved)
+        SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, (ph_data && !bwd_direct) ? acat : nullptr,
+                              (ph_data && !bwd_direct) ? bcat : nullptr, need_saved ? acatT : nullptr, nullptr,
+                              nullptr, nullptr, st));
 
     // Savedᵀ = (x·S1)ᵀ, recomputed only when the caller did not keep it.
     const void* saved = saved_proj;
-    if (!saved) {
+    if (need_saved) {
         void* sv = at<void>(workspace, p.saved);
         GemmArgs g = {};
         g.alpha = 1.f;
@@ -618,6 +711,10 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         saved = sv;
     }
 
+    // Phase DU1_DB alone runs first in a data-parallel step so the all-reduce of
+    // dU1s | db overlaps the dX kernel.
+    if (ph_u1 && !ph_data)
+        return run_du(d, T, kind, 1, saved, grad_y, nullptr, x, grad_U1s, nullptr, grad_bias, workspace, p, di.sms, st);
     // P = G·Bcatᵀ (P_S2ᵀ leaves the chip) and dX = inv·P·Acatᵀ
     if (fused && grad_x) {
         B2BArgs a = {};
@@ -667,63 +764,14 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
         }
     }
 
-    // dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
-    // ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.
-    const DuShape u = du_shape(d, T, di.sms, kind);
-    DuArgs a = {};
-    a.k_blocks = u.kb;
-    a.splits = u.splits;
-    a.num_tiles = u.tiles;
-    a.p[0] = DuProblem{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
-                       (long long)1 << 40, 0, (long long)d.d_out, 1, grad_bias};
-    a.p[1] = DuProblem{(int)d.Lk, (int)d.d_in, u.m1, u.n1t, u.m0 * u.n0t, 0, inv, grad_U2s,
-                       (long long)d.k, (long long)(d.d_in * d.k), 1, (long long)d.k, nullptr};
-    a.part = at<float>(workspace, p.du_part);
-    a.cpart = at<float>(workspace, p.du_cpart);
-    a.tickets = at<int>(workspace, p.du_tickets);
-    const int bkt = 128 / eb;  // tokens per k-block (= columns per MN-major block)
-    CUtensorMap ta0, tb0, ta1, tb1;
-    SKL_TRY(make_tmap(&ta0, saved, eb, T, d.Lk, ldt, bkt, 128));            // Savedᵀ, K-major
-    // MN-major TF32 tiles use the 32-B-atom 128B swizzle (UMMA layout SWIZZLE_128B_BASE32B)
-    const CUtensorMapSwizzle mn_swz = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-    SKL_TRY(make_tmap(&tb0, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));  // G, MN-major
-    SKL_TRY(make_tmap(&ta1, p2t, eb, T, d.Lk, ldt, bkt, 128));                    // P_S2ᵀ, K-major
-    SKL_TRY(make_tmap(&tb1, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));         // X, MN-major
-    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
-    auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[kind]) {
-        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
-        attr_set[kind] = true;
-    }
-    const int units = u.tiles * u.splits;  // CTA pairs
-    a.relay = grad_bias ? 1 : 0;
-    static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
-    a.coop = (!no_coop && 2 * units <= di.sms) ? 1 : 0;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (a.coop ? units : std::min(di.sms / 2, units)));
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = dev::kDuSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    attr[1].id = cudaLaunchAttributeCooperative;
-    attr[1].val.cooperative = a.coop;
-    cfg.attrs = attr;
-    cfg.numAttrs = 2;
-    ProfScope ps_("du_fused", st);
-    cudaError_t le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
-    if (le != cudaSuccess && a.coop) {  // cooperative + cluster refused: last-CTA reduction instead
-        (void)cudaGetLastError();
-        a.coop = 0;
-        attr[1].val.cooperative = 0;
-        cfg.gridDim = dim3(2 * std::min(di.sms / 2, units));
-        le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
-    }
-    SKL_CUDA(le);
+
+    return run_du(d, T, kind, ph_u1 ? 3 : 2, saved, grad_y, p2t, x, grad_U1s, grad_U2s, grad_bias, workspace, p,
+                  di.sms, st);
+}
+
+skl_status skl_set_reserved_sms(int n) {
+    if (n < 0 || n > 64) return fail(SKL_ERR_PARAM, "reserved SMs must be in [0, 64], got %d", n);
+    g_reserved_sms = n;
     return SKL_OK;
 }
 

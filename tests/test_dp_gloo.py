@@ -40,16 +40,19 @@ def _worker(rank, world, port, q):
     lo, hi = shard_range(T, rank, world)
     gx, gu1, gu2, gb = o.backward(p, x[:, lo:hi].copy(), g[:, lo:hi].copy())
     _, du1, du2, db = oracle.grads_to_abi(gx, gu1, gu2, gb)
-    bucket = GradBucket.allocate(d_in, d_out, L, k, device="cpu")
-    bucket.flat = bucket.flat.double()
-    n1, n2 = L * k * d_out, L * d_in * k
-    bucket.flat[:n1] = torch.from_numpy(du1.ravel())
-    bucket.flat[n1:n1 + n2] = torch.from_numpy(du2.ravel())
-    bucket.flat[n1 + n2:] = torch.from_numpy(db)
-    bucket.allreduce_()
+    bucket = GradBucket.allocate(d_in, d_out, L, k, device="cpu", dtype=torch.float64)
+    # phase DU1_DB writes dU1s | db, its all-reduce is issued async; phase
+    # DX_DU2 writes dU2s, then the tail all-reduce (the overlapped DP schedule)
+    bucket.dU1s.copy_(torch.from_numpy(du1))
+    bucket.db.copy_(torch.from_numpy(db))
+    w1 = bucket.allreduce_head(async_op=True)
+    bucket.dU2s.copy_(torch.from_numpy(du2))
+    w2 = bucket.allreduce_tail(async_op=True)
+    w1.wait()
+    w2.wait()
     if rank == 0:
         full = oracle.grads_to_abi(*o.backward(p, x, g))
-        ref = np.concatenate([full[1].ravel(), full[2].ravel(), full[3]])
+        ref = np.concatenate([full[1].ravel(), full[3], full[2].ravel()])  # dU1s | db | dU2s
         q.put(float(np.max(np.abs(bucket.flat.numpy() - ref)) / np.max(np.abs(ref))))
     dist.destroy_process_group()
 
