@@ -401,11 +401,17 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.inter = take(!fused ? (size_t)T * d.R_pad * e : 0);
     p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
     p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
-    if (bwd) {
-        const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1);
-        p.du_part = take((size_t)u.tiles * u.splits * 256 * 256 * 4);
-        p.du_cpart = take((size_t)u.n0t * u.splits * 256 * 4);
-        p.du_tickets = take((size_t)u.tiles * 4);
+    if (bwd) {  // sized for every phase split (a lone dU1 / dU2 launch uses more T splits)
+        size_t part = 0, cpart = 0, tickets = 0;
+        for (int which = 1; which <= 3; ++which) {
+            const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1, which);
+            part = std::max(part, (size_t)u.tiles * u.splits * 256 * 256 * 4);
+            cpart = std::max(cpart, (size_t)u.n0t * u.splits * 256 * 4);
+            tickets = std::max(tickets, (size_t)u.tiles * 4);
+        }
+        p.du_part = take(part);
+        p.du_cpart = take(cpart);
+        p.du_tickets = take(tickets);
     }
     p.colsum = take(0);
     p.total = off;
@@ -440,19 +446,27 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     a.p[0] = (which & 1) ? pu1 : pu2;
     a.p[1] = (which & 1) && (which & 2) ? pu2 : none;
     const bool colsum = (which & 1) && grad_bias;
-    if (!(which & 1)) saved = p2t;      // unused map, any valid tensor
-    if (!(which & 2)) p2t = saved;
+    if (!(which & 2)) p2t = saved;  // unused slot-1 maps: any valid tensor
     a.part = at<float>(workspace, p.du_part);
     a.cpart = at<float>(workspace, p.du_cpart);
     a.tickets = at<int>(workspace, p.du_tickets);
     const int bkt = 128 / eb;  // tokens per k-block (= columns per MN-major block)
     CUtensorMap ta0, tb0, ta1, tb1;
-    SKL_TRY(make_tmap(&ta0, saved, eb, T, d.Lk, ldt, bkt, 128));            // Savedᵀ, K-major
     // MN-major TF32 tiles use the 32-B-atom 128B swizzle (UMMA layout SWIZZLE_128B_BASE32B)
     const CUtensorMapSwizzle mn_swz = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
-    SKL_TRY(make_tmap(&tb0, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));  // G, MN-major
-    SKL_TRY(make_tmap(&ta1, p2t, eb, T, d.Lk, ldt, bkt, 128));                    // P_S2ᵀ, K-major
-    SKL_TRY(make_tmap(&tb1, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));         // X, MN-major
+    // Problem slot 0 reads (tmA0, tmB0), slot 1 (tmA1, tmB1).  dU1: Savedᵀ (K-major) x G
+    // (MN-major); dU2ᵀ: P_S2ᵀ (K-major) x X (MN-major).  A lone dU2 launch sits in slot 0.
+    CUtensorMap tu1a, tu1b, tu2a, tu2b;
+    if (which & 1) {
+        SKL_TRY(make_tmap(&tu1a, saved, eb, T, d.Lk, ldt, bkt, 128));
+        SKL_TRY(make_tmap(&tu1b, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));
+    }
+    SKL_TRY(make_tmap(&tu2a, p2t, eb, T, d.Lk, ldt, bkt, 128));
+    SKL_TRY(make_tmap(&tu2b, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));
+    ta0 = (which & 1) ? tu1a : tu2a;
+    tb0 = (which & 1) ? tu1b : tu2b;
+    ta1 = tu2a;
+    tb1 = tu2b;
     SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
     auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
     static bool attr_set[2] = {false, false};

@@ -66,7 +66,7 @@ class GradBucket:
     @staticmethod
     def _reduce(t, group, async_op):
         import torch.distributed as dist
-        if not dist.is_initialized() or dist.get_world_size(group) == 1:
+        if not dist.is_initialized():
             return None
         return dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group, async_op=async_op)
 

@@ -224,3 +224,72 @@ def test_backward_is_deterministic(skl, port):
     torch.cuda.synchronize()
     for a, b in zip(*outs):
         assert torch.equal(a, b)
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_phased_backward_matches_oracle(skl, port, dtype_name):
+    """sketched_linear_backward_phase(DU1_DB) then (DX_DU2), with SMs reserved
+    for a concurrent collective, gives the same gradients (within the gates)."""
+    import oracle
+    from tests._util import check_close
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    d_in, d_out, L, k, T = 768, 3072, 2, 128, 1000
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, dtype)
+    td = skl.torch_dtype(dtype)
+    y = torch.empty(T, d_out, dtype=td, device="cuda")
+    saved = torch.empty(L * k, (T + 7) // 8 * 8, dtype=td, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.set_reserved_sms(8)
+    try:
+        skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+        gx = torch.empty(T, d_in, dtype=td, device="cuda")
+        du1 = torch.empty(L, k, d_out, device="cuda")
+        du2 = torch.empty(L, d_in, k, device="cuda")
+        db = torch.empty(d_out, device="cuda")
+        skl.backward_phase(s, skl.BWD_DU1_DB, G, X, saved, S1s, S2s, U1s, U2s, None, du1, None, db, ws)
+        skl.backward_phase(s, skl.BWD_DX_DU2, G, X, saved, S1s, S2s, U1s, U2s, gx, None, du2, None, ws)
+        torch.cuda.synchronize()
+    finally:
+        skl.set_reserved_sms(0)
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    check_close("grad_x(phased)", _np(gx), rgx, dtype_name)
+    check_close("dU1s(phased)", _np(du1), rgu1, dtype_name)
+    check_close("dU2s(phased)", _np(du2), rgu2, dtype_name)
+    check_close("db(phased)", _np(db), rgb, dtype_name)
+
+
+def test_dp_overlapped_step_over_nccl(skl, port):
+    """The DP schedule bench.py runs at N > 1 (dp.backward_overlapped: async
+    NCCL all-reduce of dU1s|db issued before the dX kernel), on a world-1 NCCL
+    group: the collectives run and the bucket equals the plain backward."""
+    import socket
+    import torch.distributed as dist
+    from paper_2601_15473_b200.dp import GradBucket, backward_overlapped
+    d_in, d_out, L, k, T = 768, 3072, 2, 128, 2048
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port_ = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
+        saved = torch.empty(L * k, T, dtype=torch.bfloat16, device="cuda")
+        ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+        skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+        gb = GradBucket.allocate(d_in, d_out, L, k)
+        gx = torch.empty(T, d_in, dtype=torch.bfloat16, device="cuda")
+        works = backward_overlapped(skl, s, G, X, saved, S1s, S2s, U1s, U2s, gx, gb, ws)
+        assert len(works) == 2
+        for w in works:
+            w.wait()
+        ref = GradBucket.allocate(d_in, d_out, L, k)
+        gx2 = torch.empty_like(gx)
+        skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx2, ref.dU1s, ref.dU2s, ref.db, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(gx, gx2)
+        rel = (gb.flat - ref.flat).norm() / ref.flat.norm()
+        assert rel < 1e-5, rel
+    finally:
+        dist.destroy_process_group()
