@@ -21,7 +21,8 @@ import os
 from dataclasses import dataclass
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libskl.so")
+# SKL_LIB overrides the library path (A/B timing of two builds); default: in-tree build.
+LIB_PATH = os.environ.get("SKL_LIB") or os.path.join(_HERE, "libskl.so")
 
 SKL_OK = 0
 STATUS = {0: "SKL_OK", 1: "SKL_ERR_SHAPE", 2: "SKL_ERR_PARAM", 3: "SKL_ERR_CUDA", 4: "SKL_ERR_NCCL",

@@ -5,10 +5,10 @@
 //     sign bit, bit-exact integer chain of the reference stream
 //     (rng.hpp:13-69, sketch.cpp:34-49, nn_layers.cpp:124-145)
 //   * parameter packing: pawX [L,d,k] stacks -> the K-major operand panels the
-//     tcgen05 kernels stream (Acat / Bcat and their transposes), with TF32
+//     tcgen05 kernels stream when they cannot read the stacks in place
+//     (Acat / Bcat and their transposes, one tiled launch), with TF32
 //     round-to-nearest for the fp32 variant
-//   * deterministic split-K reduction (fixed order) + layout scatter
-//   * deterministic column sum (db = row_sums(G), nn_layers.cpp:23-30,99)
+// (db and the dU reductions are fused into the du kernel, du.cuh.)
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -146,138 +146,6 @@ __device__ __forceinline__ float ld_f(const void* p, uint64_t i) {
     else return reinterpret_cast<const float*>(p)[i];
 }
 
-// Acat [d_in][R_pad]: column r < Lk -> S1s[r/k][c][r%k], Lk <= r < 2Lk ->
-// U2s[..], zero padding.  Bcat [R_pad][d_out]: row r < Lk -> U1s[r/k][r%k][:],
-// then S2s, zero padding.  Operand element type: bf16 copy, or fp32 rounded
-// to TF32 (cvt.rna) for the tf32 variant.
-template <typename T>
-__global__ void pack_cat_kernel(const void* S1s, const void* U2s, const void* U1s, const void* S2s, int64_t L,
-                                int64_t k, int64_t d_in, int64_t d_out, int64_t R_pad, void* Acat, void* Bcat) {
-    const int64_t Lk = L * k;
-    const uint64_t na = (uint64_t)d_in * R_pad, nb = (uint64_t)R_pad * d_out;
-    for (uint64_t idx = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; idx < na + nb;
-         idx += (uint64_t)gridDim.x * blockDim.x) {
-        float v = 0.f;
-        uint64_t o = idx;
-        if (idx < na) {
-            const int64_t c = idx / R_pad, r = idx % R_pad;
-            if (r < Lk) v = ld_f<T>(S1s, ((r / k) * d_in + c) * k + r % k);
-            else if (r < 2 * Lk) v = ld_f<T>(U2s, (((r - Lk) / k) * d_in + c) * k + (r - Lk) % k);
-        } else {
-            o = idx - na;
-            const int64_t r = o / d_out, c = o % d_out;
-            if (r < Lk) v = ld_f<T>(U1s, r * d_out + c);
-            else if (r < 2 * Lk) v = ld_f<T>(S2s, (r - Lk) * d_out + c);
-        }
-        if constexpr (sizeof(T) == 2) {
-            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(idx < na ? Acat : Bcat);
-            dst[o] = __float2bfloat16_rn(v);
-        } else {
-            float* dst = reinterpret_cast<float*>(idx < na ? Acat : Bcat);
-            dst[o] = dev::tf32_rna(v);
-        }
-    }
-}
-
-// out[c][r] = in[r][c], in is [rows][cols]; 32x32 smem tiles.
-template <typename T>
-__global__ void transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows, int64_t cols) {
-    __shared__ T tile[32][33];
-    const int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int64_t r = r0 + i, c = c0 + threadIdx.x;
-        if (r < rows && c < cols) tile[i][threadIdx.x] = in[r * cols + c];
-    }
-    __syncthreads();
-    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
-        const int64_t c = c0 + i, r = r0 + threadIdx.x;
-        if (r < rows && c < cols) out[c * rows + r] = tile[threadIdx.x][i];
-    }
-}
-
-template <typename T>
-__global__ void to_f32_kernel(const void* in, float* out, int64_t n) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        out[i] = in ? ld_f<T>(in, i) : 0.f;
-}
-
-// ---------------------------------------------------------------- reductions
-// out[(n / nb) * blk + m * ldm + n % nb] = alpha * sum_{s=0..S-1} part[s][m][n]
-__global__ void reduce_partials_kernel(const float* __restrict__ part, int S, int64_t M, int64_t N, float alpha,
-                                       float* __restrict__ out, int64_t nb, int64_t blk, int64_t ldm) {
-    const int64_t MN = M * N;
-    if ((N & 3) == 0 && (nb & 3) == 0 && (ldm & 3) == 0 && (blk & 3) == 0) {
-        // 4 consecutive n per thread (never straddle an nb block)
-        for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) * 4; i < MN;
-             i += (int64_t)gridDim.x * blockDim.x * 4) {
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s = 0; s < S; ++s) {
-                const float4 v = __ldg(reinterpret_cast<const float4*>(part + s * MN + i));
-                acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-            }
-            const int64_t m = i / N, n = i % N;
-            *reinterpret_cast<float4*>(out + (n / nb) * blk + m * ldm + n % nb) =
-                make_float4(acc.x * alpha, acc.y * alpha, acc.z * alpha, acc.w * alpha);
-        }
-        return;
-    }
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < MN; i += (int64_t)gridDim.x * blockDim.x) {
-        float acc = 0.f;
-        for (int s = 0; s < S; ++s) acc += part[s * MN + i];
-        const int64_t m = i / N, n = i % N;
-        out[(n / nb) * blk + m * ldm + n % nb] = acc * alpha;
-    }
-}
-
-// Column sums of G [T][N] in two fixed-order stages: chunk c sums rows
-// [c*rows_per, (c+1)*rows_per) into part[c][N]; then part is reduced.
-// Each thread owns 8 consecutive columns (one 16-B load per row for bf16,
-// two for fp32), rows in ascending order: fixed summation order.
-// Block = 8 warps x 32 lanes over 256 columns: lane owns 8 columns, warp w
-// takes rows r0+w, r0+w+8, ...; the 8 warp partials are then added in warp
-// order through shared memory (fixed order -> deterministic).
-template <typename T>
-__global__ void __launch_bounds__(256) colsum_partial_kernel(const void* G, int64_t rows, int64_t N,
-                                                             int64_t rows_per, float* part) {
-    __shared__ float sh[8][256];
-    const int64_t c = blockIdx.y;
-    const int64_t r0 = c * rows_per, r1 = min(rows, r0 + rows_per);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int64_t n0 = blockIdx.x * 256 + lane * 8;
-    float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if (n0 + 8 <= N && (N & 7) == 0) {
-#pragma unroll 4
-        for (int64_t r = r0 + w; r < r1; r += 8) {
-            if constexpr (sizeof(T) == 2) {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(G) + r * N + n0));
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const float2 f = __bfloat1622float2(h[i]);
-                    acc[2 * i] += f.x;
-                    acc[2 * i + 1] += f.y;
-                }
-            } else {
-                const float4* p = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(G) + r * N + n0);
-                const float4 a = __ldg(p), b = __ldg(p + 1);
-                acc[0] += a.x; acc[1] += a.y; acc[2] += a.z; acc[3] += a.w;
-                acc[4] += b.x; acc[5] += b.y; acc[6] += b.z; acc[7] += b.w;
-            }
-        }
-    } else if (n0 < N) {
-        for (int64_t r = r0 + w; r < r1; r += 8)
-            for (int i = 0; i < 8 && n0 + i < N; ++i) acc[i] += ld_f<T>(G, r * N + n0 + i);
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i) sh[w][lane * 8 + i] = acc[i];
-    __syncthreads();
-    const int64_t col = blockIdx.x * 256 + threadIdx.x;
-    float s = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) s += sh[i][threadIdx.x];
-    if (col < N) part[c * N + col] = s;
-}
-
 inline int grid_for(uint64_t n, int block = 256) {
     uint64_t g = (n + block - 1) / block;
     if (g > 148ull * 16) g = 148ull * 16;
@@ -405,72 +273,6 @@ cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void
         pack_tiles_kernel<float><<<grid, 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out, d.R_pad, Acat,
                                                        Bcat, AcatT, BcatT, bias, bias32);
     return cudaGetLastError();
-}
-
-cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
-                        const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, cudaStream_t st) {
-    const uint64_t n = (uint64_t)d.R_pad * (d.d_in + d.d_out);
-    {
-    ProfScope ps_("pack", st);
-    if (elem == ELEM_BF16)
-        pack_cat_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
-                                                                    d.R_pad, Acat, Bcat);
-    else
-        pack_cat_kernel<float><<<grid_for(n), 256, 0, st>>>(S1s, U2s, U1s, S2s, d.L, d.k, d.d_in, d.d_out,
-                                                            d.R_pad, Acat, Bcat);
-    }
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    dim3 blk(32, 8);
-    if (AcatT) {
-        ProfScope ps_("transpose", st);
-        dim3 g((d.R_pad + 31) / 32, (d.d_in + 31) / 32);
-        if (elem == ELEM_BF16)
-            transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Acat, (__nv_bfloat16*)AcatT,
-                                                               d.d_in, d.R_pad);
-        else
-            transpose_kernel<float><<<g, blk, 0, st>>>((const float*)Acat, (float*)AcatT, d.d_in, d.R_pad);
-    }
-    if (BcatT) {
-        ProfScope ps_("transpose", st);
-        dim3 g((d.d_out + 31) / 32, (d.R_pad + 31) / 32);
-        if (elem == ELEM_BF16)
-            transpose_kernel<__nv_bfloat16><<<g, blk, 0, st>>>((const __nv_bfloat16*)Bcat, (__nv_bfloat16*)BcatT,
-                                                               d.R_pad, d.d_out);
-        else
-            transpose_kernel<float><<<g, blk, 0, st>>>((const float*)Bcat, (float*)BcatT, d.R_pad, d.d_out);
-    }
-    return cudaGetLastError();
-}
-
-cudaError_t launch_to_f32(const void* in, int elem, float* out, int64_t n, cudaStream_t st) {
-    ProfScope ps_("bias_f32", st);
-    if (elem == ELEM_BF16) to_f32_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(in, out, n);
-    else to_f32_kernel<float><<<grid_for(n), 256, 0, st>>>(in, out, n);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_reduce_partials(const float* part, int S, int64_t M, int64_t N, float alpha, float* out,
-                                   int64_t nb, int64_t blk, int64_t ldm, cudaStream_t st) {
-    ProfScope ps_("reduce", st);
-    reduce_partials_kernel<<<grid_for((uint64_t)M * N), 256, 0, st>>>(part, S, M, N, alpha, out, nb, blk, ldm);
-    return cudaGetLastError();
-}
-
-int64_t colsum_chunks(int64_t rows) { return rows < 256 ? 1 : (rows + 255) / 256 < 512 ? (rows + 255) / 256 : 512; }
-
-cudaError_t launch_colsum(const void* G, int elem, int64_t rows, int64_t N, float* part, float* out,
-                          cudaStream_t st) {
-    const int64_t chunks = colsum_chunks(rows);
-    const int64_t rows_per = (rows + chunks - 1) / chunks;
-    dim3 g((unsigned)((N + 255) / 256), (unsigned)chunks);
-    ProfScope* ps_ = new ProfScope("colsum", st);
-    if (elem == ELEM_BF16) colsum_partial_kernel<__nv_bfloat16><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
-    else colsum_partial_kernel<float><<<g, 256, 0, st>>>(G, rows, N, rows_per, part);
-    delete ps_;
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return launch_reduce_partials(part, (int)chunks, 1, N, 1.0f, out, N, 0, N, st);
 }
 
 }  // namespace skl

@@ -2,25 +2,23 @@
 //
 //   D[m, n] = alpha * sum_k A(m, k) * B(n, k)   (+ bias[n])
 //
-// Used by the SKLinear path for every contraction that does not run inside
-// the fused back-to-back kernel (b2b.cuh):
-//   * dU1s = inv * Savedᵀ·G     (split-K over tokens, A and B MN-major)
-//   * dU2s = inv * Xᵀ·P_S2      (split-K over tokens, A and B MN-major)
-//   * the unfused H = X·Acat / Y = H·Bcat (+b) / P / dX chain when the
-//     rank R = 2Lk is too large for the on-chip intermediate (R > 512).
+// Used by the SKLinear path for the contractions that do not run inside the
+// fused back-to-back kernel (b2b.cuh): the unfused H = x·Acat / y = H·Bcat
+// (+b) / P = G·Bcatᵀ / dX = P·Acatᵀ chain when the rank R = 2Lk is too large
+// for the on-chip intermediate (bf16 R > 512, TF32 R > 256), and the saved-
+// projection recompute.  Both operands are K-major.
 //
-// Structure (one CTA per SM, or one CTA pair per TPC when kCG == 2):
+// Structure (one CTA pair per two SMs, cta_group::2):
 //   warp 0      TMA producer   (one elected lane)  smem ring of kStages
 //   warp 1      MMA issuer     (one elected lane, leader CTA only)
 //   warp 2      TMEM allocator (512 columns = 2 accumulator stages)
-//   warps 4..7  epilogue       TMEM -> registers -> alpha/bias -> global
-// Operands are staged with 128B-swizzled TMA tiles; accumulators live in TMEM
-// (double-buffered so the epilogue of tile i overlaps the MMAs of tile i+1).
-// With kCG == 2 the pair runs cta_group::2 MMAs (M = 256, each CTA holds its
-// 128 rows of A and half of the N rows of B), halving per-SM operand traffic.
-//
-// Split-K writes raw fp32 partials [split][M][N]; reduce_partials (aux.cu)
-// sums them in a fixed order (deterministic) and applies alpha / layout.
+//   warps 4..7  epilogue       TMEM -> registers -> alpha/bias -> swizzled
+//                              smem -> TMA bulk store (coalesced, async)
+// The pair runs M = 256 (each CTA keeps its 128 rows of A and half of the
+// kBN rows of B), so per SM one 128x256x16 MMA reads 8 KB of smem per 64
+// cycles -- exactly the 128 B/clk smem port -- where a single CTA would need
+// 12 KB and be smem-bound at 2/3 of the tensor peak.  Accumulators are
+// double-buffered in TMEM so the epilogue of tile i overlaps tile i+1.
 #pragma once
 
 #include "sm100.cuh"
@@ -29,10 +27,10 @@ namespace skl {
 
 struct GemmArgs {
     int M, N, K;
-    int num_m_tiles, num_n_tiles, splits, k_blocks;
+    int num_m_tiles, num_n_tiles, k_blocks;
     float alpha;
-    const float* bias;  // [N] fp32, nullable (direct mode only)
-    // direct mode (partial == nullptr): all columns -> out (nullable); columns
+    const float* bias;  // [N] fp32, nullable
+    // all columns -> out through the tmOut tensor map (nullable); columns
     // [out2_c0, out2_c1) are additionally written transposed to out2
     // (out2[(n - out2_c0) * ldo2 + m]) -- the layout the dU kernel reads.
     void* out;
@@ -40,10 +38,8 @@ struct GemmArgs {
     void* out2;
     long long ldo2;
     int out2_c0, out2_c1;
-    int out_f32;  // 1: fp32 output, 0: bf16 output
-    int round_tf32;  // 1: round direct-mode outputs to TF32 (cvt.rna) -- they feed a TF32 GEMM
-    // split-K mode
-    float* partial;  // [splits][M][N] fp32
+    int out_f32;     // 1: fp32 output, 0: bf16 output
+    int round_tf32;  // 1: round outputs to TF32 (cvt.rna) -- they feed a TF32 GEMM
 };
 
 namespace dev {
@@ -59,34 +55,37 @@ struct KindTraits<1> {  // tf32 (fp32 words)
     static constexpr int kElem = 4, kBK = 32, kUK = 8;
 };
 
-template <int kCG, int kKind, bool kAMN, bool kBMN, int kBN, int kStages>
+template <int kCG, int kKind, int kBN, int kStages>
 struct GemmCfg {
     static constexpr int kBK = KindTraits<kKind>::kBK;
     static constexpr int kUK = KindTraits<kKind>::kUK;
     static constexpr int kElem = KindTraits<kKind>::kElem;
     static constexpr int kBM = 128;           // rows per CTA
     static constexpr int kNcta = kBN / kCG;   // B rows staged per CTA
-    static constexpr int kABytes = kBM * 128; // one 128-B row per M row (K-major) / BK rows x 128 B x 2 blocks
+    static constexpr int kABytes = kBM * 128; // one 128-B row (one k-block) per M row
     static constexpr int kBBytes = kNcta * 128;
     static constexpr int kStageBytes = kABytes + kBBytes;
     static constexpr int kTmemCols = 512;
-    static constexpr int kSmem = kStages * kStageBytes + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int kOutBytes = 16384;   // one [128 rows x 128 B] output box
+    static constexpr int kSmem = kStages * kStageBytes + 2 * kOutBytes + 1024 /*align*/ + 256 /*barriers*/;
     static_assert(kBN % (16 * kCG) == 0 && kBN <= 256 && kBN >= 16 * kCG, "bad BLOCK_N");
-    static_assert(!kBMN || kNcta % 64 == 0, "MN-major B needs 64-wide blocks");
-    static_assert(!(kKind == 1 && (kAMN || kBMN)), "MN-major TF32 operands are not supported");
+    static_assert(kBN % 64 == 0, "epilogue stores 64-column (bf16) / 32-column (fp32) boxes");
     static_assert(2 * kBN <= kTmemCols, "two accumulator stages must fit TMEM");
+    static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
-template <int kCG, int kKind, bool kAMN, bool kBMN, int kBN, int kStages>
+template <int kCG, int kKind, int kBN, int kStages>
 __global__ void __launch_bounds__(256, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs args) {
-    using C = GemmCfg<kCG, kKind, kAMN, kBMN, kBN, kStages>;
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                const __grid_constant__ CUtensorMap tmOut, GemmArgs args) {
+    using C = GemmCfg<kCG, kKind, kBN, kStages>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
     uint8_t* sA = smem;
     uint8_t* sB = smem + kStages * C::kABytes;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kStages * C::kStageBytes);
+    uint8_t* sOut = smem + kStages * C::kStageBytes;  // 2 x 16 KB output staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sOut + 2 * C::kOutBytes);
     uint64_t* full = bars;
     uint64_t* empty = bars + kStages;
     uint64_t* tfull = bars + 2 * kStages;
@@ -100,6 +99,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0 && elect_one()) {
         prefetch_tmap(&tmA);
         prefetch_tmap(&tmB);
+        if (args.out) prefetch_tmap(&tmOut);
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], kCG);
             mbar_init(&empty[s], 1);
@@ -119,19 +119,17 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int num_tiles = args.num_m_tiles * args.num_n_tiles * args.splits;
+    const int num_tiles = args.num_m_tiles * args.num_n_tiles;
     const int cluster_id = blockIdx.x / kCG;
     const int num_clusters = gridDim.x / kCG;
 
-    auto decode = [&](int t, int& m0, int& n0, int& kb0, int& kb1, int& split) {
-        const int mt = t % args.num_m_tiles;
-        const int rest = t / args.num_m_tiles;
-        const int nt = rest % args.num_n_tiles;
-        split = rest / args.num_n_tiles;
-        m0 = mt * (C::kBM * kCG);
-        n0 = nt * kBN;
-        kb0 = (int)(((long long)split * args.k_blocks) / args.splits);
-        kb1 = (int)(((long long)(split + 1) * args.k_blocks) / args.splits);
+    // n fastest: the clusters working at the same time share one A row panel
+    // (activations, large -- read from HBM once) and sweep the B panel
+    // (parameters, a few MB -- L2-resident).  m-fastest order re-read A once
+    // per N tile (ncu: 542 MB read vs 73 MB algorithmic for the c2 TF32 y GEMM).
+    auto decode = [&](int t, int& m0, int& n0) {
+        m0 = (t / args.num_n_tiles) * (C::kBM * kCG);
+        n0 = (t % args.num_n_tiles) * kBN;
     };
 
     if (warp == 0) {
@@ -140,33 +138,19 @@ __global__ void __launch_bounds__(256, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int t = cluster_id; t < num_tiles; t += num_clusters) {
-                int m0, n0, kb0, kb1, split;
-                decode(t, m0, n0, kb0, kb1, split);
+                int m0, n0;
+                decode(t, m0, n0);
                 const int am = m0 + (int)rank * C::kBM;
                 const int bn = n0 + (int)rank * C::kNcta;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    uint8_t* a_dst = sA + stage * C::kABytes;
-                    uint8_t* b_dst = sB + stage * C::kBBytes;
                     const int k0 = kb * C::kBK;
                     if (leader)
                         mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kCG);
                     else
                         mbar_arrive_cluster(&full[stage], 0);
-                    if constexpr (!kAMN) {
-                        tma_load_2d<kCG>(&tmA, &full[stage], a_dst, k0, am);
-                    } else {
-                        // two 64-wide M blocks, each [BK rows x 128 B]
-                        tma_load_2d<kCG>(&tmA, &full[stage], a_dst, am, k0);
-                        tma_load_2d<kCG>(&tmA, &full[stage], a_dst + C::kBK * 128, am + 64, k0);
-                    }
-                    if constexpr (!kBMN) {
-                        tma_load_2d<kCG>(&tmB, &full[stage], b_dst, k0, bn);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < C::kNcta / 64; ++j)
-                            tma_load_2d<kCG>(&tmB, &full[stage], b_dst + j * C::kBK * 128, bn + 64 * j, k0);
-                    }
+                    tma_load_2d<kCG>(&tmA, &full[stage], sA + stage * C::kABytes, k0, am);
+                    tma_load_2d<kCG>(&tmB, &full[stage], sB + stage * C::kBBytes, k0, bn);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -174,35 +158,25 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer
         if (leader && elect_one()) {
-            constexpr uint32_t idesc = make_idesc(kKind, C::kBM * kCG, kBN, kAMN ? 1 : 0, kBMN ? 1 : 0);
+            constexpr uint32_t idesc = make_idesc(kKind, C::kBM * kCG, kBN, 0, 0);
             int stage = 0;
             uint32_t phase = 0;
             int iter = 0;
             for (int t = cluster_id; t < num_tiles; t += num_clusters, ++iter) {
-                int m0, n0, kb0, kb1, split;
-                decode(t, m0, n0, kb0, kb1, split);
                 const int acc = iter & 1;
                 mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kBN;
-                for (int kb = kb0; kb < kb1; ++kb) {
+                for (int kb = 0; kb < args.k_blocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * C::kABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * C::kBBytes);
 #pragma unroll
-                    for (int k = 0; k < C::kBK / C::kUK; ++k) {
-                        uint64_t ad, bd;
-                        if constexpr (!kAMN)
-                            ad = make_sdesc(a_addr + k * C::kUK * C::kElem, 0, 1024);
-                        else
-                            ad = make_sdesc(a_addr + k * C::kUK * 128, C::kBK * 128, 1024);
-                        if constexpr (!kBMN)
-                            bd = make_sdesc(b_addr + k * C::kUK * C::kElem, 0, 1024);
-                        else
-                            bd = make_sdesc(b_addr + k * C::kUK * 128, C::kBK * 128, 1024);
-                        mma_ss<kCG, kKind>(d_tmem, ad, bd, idesc, (kb > kb0 || k > 0) ? 1u : 0u);
-                    }
+                    for (int k = 0; k < C::kBK / C::kUK; ++k)
+                        mma_ss<kCG, kKind>(d_tmem, make_sdesc(a_addr + k * C::kUK * C::kElem, 0, 1024),
+                                           make_sdesc(b_addr + k * C::kUK * C::kElem, 0, 1024), idesc,
+                                           (kb > 0 || k > 0) ? 1u : 0u);
                     mma_commit<kCG>(&empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
@@ -211,84 +185,74 @@ __global__ void __launch_bounds__(256, 1)
         }
     } else if (warp >= 4) {
         // ------------------------------------------------------------ epilogue
+        // Thread = one accumulator row (TMEM lane).  Each 128-B column slice
+        // (64 bf16 / 32 fp32 columns) goes TMEM -> registers -> alpha/bias
+        // (/TF32 rounding) -> 128B-swizzled smem box -> one TMA bulk store
+        // (two boxes in flight).
         const uint32_t q = warp & 3;  // TMEM lane quarter
         const uint32_t lane = lane_id();
-        int iter = 0;
+        const uint32_t srow = q * 32 + lane;
+        const bool issuer = (q == 0 && lane == 0);
+        const int ecols = args.out_f32 ? 32 : 64;
+        int iter = 0, nbox = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++iter) {
-            int m0, n0, kb0, kb1, split;
-            decode(t, m0, n0, kb0, kb1, split);
+            int m0, n0;
+            decode(t, m0, n0);
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
-            const int row = m0 + (int)rank * C::kBM + (int)(q * 32 + lane);
+            const int row0 = m0 + (int)rank * C::kBM;
+            const int row = row0 + (int)srow;
             const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kBN;
 #pragma unroll 1
-            for (int c = 0; c < kBN; c += 16) {
-                uint32_t r[16];
-                tmem_ld16(t_row + c, r);
-                tmem_ld_wait();
+            for (int c = 0; c < kBN; c += ecols) {
                 const int n = n0 + c;
-                if (row >= args.M || n >= args.N) continue;
-                float v[16];
+                if (n >= args.N) break;  // uniform across the CTA
+                uint32_t ra[32], rb[32];
+                tmem_ld32(t_row + c, ra);
+                if (!args.out_f32) tmem_ld32(t_row + c + 32, rb);
+                tmem_ld_wait();
+                float v[64];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
-                if (args.partial) {
-                    float* dst = args.partial + ((long long)split * args.M + row) * args.N + n;
-                    if (n + 16 <= args.N && (args.N & 3) == 0) {
-#pragma unroll
-                        for (int j = 0; j < 16; j += 4)
-                            *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                    } else {
-                        for (int j = 0; j < 16 && n + j < args.N; ++j) dst[j] = v[j];
-                    }
-                    continue;
+                for (int j = 0; j < 64; ++j) {
+                    if (j >= ecols) break;
+                    const uint32_t bits = j < 32 ? ra[j] : rb[j - 32];
+                    const float b = (args.bias != nullptr && n + j < args.N) ? __ldg(args.bias + n + j) : 0.f;
+                    v[j] = fmaf(__uint_as_float(bits), args.alpha, b);
+                    if (args.round_tf32) v[j] = tf32_rna(v[j]);
                 }
-                float bv[16];
-                load_bias16(args.bias, n, args.N, bv);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] = fmaf(v[j], args.alpha, bv[j]);
-                if (args.round_tf32) {
-#pragma unroll
-                    for (int j = 0; j < 16; ++j) v[j] = tf32_rna(v[j]);
-                }
-                const int nvalid = min(16, args.N - n);
                 // columns [out2_c0, out2_c1) also go out transposed: out2[(n - c0) * ldo2 + row]
-                if (args.out2 && n + 16 > args.out2_c0 && n < args.out2_c1) {
-                    for (int j = 0; j < 16; ++j) {
+                if (args.out2 && row < args.M && n + ecols > args.out2_c0 && n < args.out2_c1) {
+#pragma unroll
+                    for (int j = 0; j < 64; ++j) {
                         const int nn = n + j;
-                        if (nn < args.out2_c0 || nn >= args.out2_c1 || nn >= args.N) continue;
+                        if (j >= ecols || nn < args.out2_c0 || nn >= args.out2_c1 || nn >= args.N) continue;
                         const long long o = (long long)(nn - args.out2_c0) * args.ldo2 + row;
                         if (args.out_f32) reinterpret_cast<float*>(args.out2)[o] = v[j];
                         else reinterpret_cast<__nv_bfloat16*>(args.out2)[o] = __float2bfloat16_rn(v[j]);
                     }
                 }
-                if (args.out) {
-                    void* obase = args.out;
-                    const long long ld = args.ldo;
-                    const int nv = nvalid;
-                    if (args.out_f32) {
-                        float* dst = reinterpret_cast<float*>(obase) + (long long)row * ld + n;
-                        if (nv == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+                if (!args.out) continue;
+                uint8_t* buf = sOut + (nbox & 1) * C::kOutBytes;
+                if (issuer) bulk_wait_read<1>();  // the store that last used `buf` has read it
+                named_bar_sync(1, 128);
+                const uint32_t row_addr = smem_u32(buf) + srow * 128;
 #pragma unroll
-                            for (int j = 0; j < 16; j += 4)
-                                *reinterpret_cast<float4*>(dst + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-                        } else {
-                            for (int j = 0; j < nv; ++j) dst[j] = v[j];
-                        }
-                    } else {
-                        __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(obase) + (long long)row * ld + n;
-                        if (nv == 16 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-                            uint4 w0 = make_uint4(pack_bf16x2(v[0], v[1]), pack_bf16x2(v[2], v[3]),
-                                                  pack_bf16x2(v[4], v[5]), pack_bf16x2(v[6], v[7]));
-                            uint4 w1 = make_uint4(pack_bf16x2(v[8], v[9]), pack_bf16x2(v[10], v[11]),
-                                                  pack_bf16x2(v[12], v[13]), pack_bf16x2(v[14], v[15]));
-                            reinterpret_cast<uint4*>(dst)[0] = w0;
-                            reinterpret_cast<uint4*>(dst)[1] = w1;
-                        } else {
-                            for (int j = 0; j < nv; ++j) dst[j] = __float2bfloat16_rn(v[j]);
-                        }
-                    }
+                for (int ch = 0; ch < 8; ++ch) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        w[i] = args.out_f32 ? __float_as_uint(v[4 * ch + i])
+                                            : pack_bf16x2(v[8 * ch + 2 * i], v[8 * ch + 2 * i + 1]);
+                    st_shared_v4(row_addr + ((uint32_t)(ch ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
                 }
+                fence_proxy_async_smem();
+                named_bar_sync(1, 128);
+                if (issuer) {
+                    tma_store_2d(&tmOut, buf, n, row0);  // rows >= M / cols >= N are clipped
+                    bulk_commit();
+                }
+                ++nbox;
             }
             tc_fence_before();
             __syncwarp();
@@ -297,6 +261,7 @@ __global__ void __launch_bounds__(256, 1)
                 else mbar_arrive_cluster(&tempty[acc], 0);
             }
         }
+        if (issuer) bulk_wait<0>();
     }
 
     tc_fence_before();

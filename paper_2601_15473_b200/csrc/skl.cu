@@ -128,30 +128,30 @@ struct View {
     int64_t rows, cols, ld;
 };
 
-template <int kCG, int kKind, bool kAMN, bool kBMN, int kBN, int kStages>
+template <int kCG, int kKind, int kBN, int kStages>
 skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N, int K, GemmArgs args, int sms,
                     cudaStream_t st) {
-    using C = dev::GemmCfg<kCG, kKind, kAMN, kBMN, kBN, kStages>;
+    using C = dev::GemmCfg<kCG, kKind, kBN, kStages>;
     const int eb = dev::KindTraits<kKind>::kElem;
     const int bk = C::kBK;
-    CUtensorMap ta, tb;
-    // A(m,k): K-major storage [M][K] or MN-major storage [K][M]
-    if (!kAMN) SKL_TRY(make_tmap(&ta, A.ptr, eb, K, M, A.ld, bk, 128));
-    else SKL_TRY(make_tmap(&ta, A.ptr, eb, M, K, A.ld, 128 / eb, bk));
-    if (!kBMN) SKL_TRY(make_tmap(&tb, B.ptr, eb, K, N, B.ld, bk, C::kNcta));
-    else SKL_TRY(make_tmap(&tb, B.ptr, eb, N, K, B.ld, 128 / eb, bk));
+    CUtensorMap ta, tb, to;
+    SKL_TRY(make_tmap(&ta, A.ptr, eb, K, M, A.ld, bk, 128));          // A [M][K], K-major
+    SKL_TRY(make_tmap(&tb, B.ptr, eb, K, N, B.ld, bk, C::kNcta));     // B [N][K], K-major
+    if (args.out) {
+        const int ob = args.out_f32 ? 4 : 2;
+        SKL_TRY(make_tmap(&to, args.out, ob, N, M, args.ldo, 128 / ob, 128));
+    } else {
+        to = ta;  // unused
+    }
     args.M = M;
     args.N = N;
     args.K = K;
     args.num_m_tiles = (M + 128 * kCG - 1) / (128 * kCG);
     args.num_n_tiles = (N + kBN - 1) / kBN;
     args.k_blocks = (K + bk - 1) / bk;
-    if (args.splits < 1) args.splits = 1;
-    if (args.splits > args.k_blocks) args.splits = std::max(1, args.k_blocks);
-    const int tiles = args.num_m_tiles * args.num_n_tiles * args.splits;
-    int grid = std::min(sms / kCG, tiles) * kCG;
-    if (grid < kCG) grid = kCG;
-    auto kern = dev::gemm_kernel<kCG, kKind, kAMN, kBMN, kBN, kStages>;
+    const int tiles = args.num_m_tiles * args.num_n_tiles;
+    int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
+    auto kern = dev::gemm_kernel<kCG, kKind, kBN, kStages>;
     static bool attr_set = false;
     if (!attr_set) {
         SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -170,15 +170,15 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     ProfScope ps_(name, st);
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, args));
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, args));
     return SKL_OK;
 }
 
 // K-major x K-major GEMM in the variant's MMA kind (0 bf16, 1 tf32).
 skl_status gemm_any(int kind, const char* name, const View& A, const View& B, int M, int N, int K, GemmArgs args,
                     int sms, cudaStream_t st) {
-    if (kind == 0) return run_gemm<1, 0, false, false, 256, 4>(name, A, B, M, N, K, args, sms, st);
-    return run_gemm<1, 1, false, false, 256, 4>(name, A, B, M, N, K, args, sms, st);
+    if (kind == 0) return run_gemm<2, 0, 256, 6>(name, A, B, M, N, K, args, sms, st);
+    return run_gemm<2, 1, 256, 6>(name, A, B, M, N, K, args, sms, st);
 }
 
 // Operand sources of the fused kernel.  kMode 0: b1 / b2 are packed panels.
@@ -363,8 +363,14 @@ struct Plan {
 int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
 
 // Tiling of the fused dU kernel (du.cuh): problem 0 = dU1 [Lk, d_out],
-// problem 1 = dU2ᵀ [Lk, d_in]; 256 x 256 pair tiles; T split so ~one unit
-// per CTA pair.
+// problem 1 = dU2ᵀ [Lk, d_in]; 256 x 256 pair tiles; T split S ways so the
+// units fill the pairs in ONE wave (cooperative launch, slice-parallel
+// reduction).  Units run split-major: the pairs active together sweep the
+// same token window, so the rank operand (Savedᵀ / P_S2ᵀ, reused by every N
+// tile) is served from L2.  Measured alternatives, both slower at c2/c3: a
+// stream-K partition with staggered token offsets (+36-62 %: the rank operand
+// falls out of L2) and multi-wave splits with last-CTA reduction (+3x at c2:
+// serial reductions).
 struct DuShape {
     int m0, n0t, m1, n1t, tiles, splits, kb;
 };
@@ -377,7 +383,9 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     s.tiles = ((which & 1) ? s.m0 * s.n0t : 0) + ((which & 2) ? s.m1 * s.n1t : 0);
     const int bkt = kind == 0 ? 64 : 32;  // tokens per k-block
     s.kb = (int)std::max<int64_t>(1, (T + bkt - 1) / bkt);
-    s.splits = std::max(1, std::min((sms / 2) / s.tiles, std::max(1, s.kb / 2)));
+    static const int force = getenv("SKL_DU_SPLITS") ? atoi(getenv("SKL_DU_SPLITS")) : 0;  // experiments
+    s.splits = force > 0 ? std::min(force, s.kb)
+                         : std::max(1, std::min((sms / 2) / std::max(1, s.tiles), std::max(1, s.kb / 2)));
     return s;
 }
 
@@ -401,7 +409,7 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.inter = take(!fused ? (size_t)T * d.R_pad * e : 0);
     p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
     p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
-    if (bwd) {  // sized for every phase split (a lone dU1 / dU2 launch uses more T splits)
+    if (bwd) {  // sized for every phase's split choice
         size_t part = 0, cpart = 0, tickets = 0;
         for (int which = 1; which <= 3; ++which) {
             const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1, which);
@@ -432,7 +440,6 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     const int eb = kind == 0 ? 2 : 4;
     const int64_t ldt = t8(T);
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
-    struct DevInfoLite { int sms; } di{sms};
     const DuShape u = du_shape(d, T, sms, kind, which);
     DuArgs a = {};
     a.k_blocks = u.kb;
@@ -474,12 +481,14 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
         attr_set[kind] = true;
     }
-    const int units = u.tiles * u.splits;  // CTA pairs
+    const int units = u.tiles * u.splits;  // CTA-pair work units
     a.relay = colsum ? 1 : 0;
     static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
-    a.coop = (!no_coop && 2 * units <= di.sms) ? 1 : 0;
+    // one wave: cooperative launch, slice-parallel reduction; several waves:
+    // persistent grid, the last CTA of each tile reduces it
+    a.coop = (!no_coop && 2 * units <= sms) ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(2 * (a.coop ? units : std::min(di.sms / 2, units)));
+    cfg.gridDim = dim3(2 * (a.coop ? units : std::min(sms / 2, units)));
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = dev::kDuSmem;
     cfg.stream = st;
@@ -498,7 +507,7 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         (void)cudaGetLastError();
         a.coop = 0;
         attr[1].val.cooperative = 0;
-        cfg.gridDim = dim3(2 * std::min(di.sms / 2, units));
+        cfg.gridDim = dim3(2 * std::min(sms / 2, units));
         le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
     }
     SKL_CUDA(le);
@@ -641,8 +650,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g1.out2_c1 = (int)d.Lk;
     g1.out_f32 = eb == 4;
     g1.round_tf32 = eb == 4;  // H feeds a TF32 GEMM: round-to-nearest instead of hardware truncation
-    g1.splits = 1;
-    View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+        View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
     SKL_TRY(gemm_any(eb == 4, "gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st));
     GemmArgs g2 = {};
     g2.alpha = inv;
@@ -650,8 +658,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     g2.out = y;
     g2.ldo = d.d_out;
     g2.out_f32 = eb == 4;
-    g2.splits = 1;
-    View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
+        View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
     SKL_TRY(gemm_any(eb == 4, "gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st));
     return SKL_OK;
 }
@@ -719,8 +726,7 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
         g.out2_c1 = (int)d.Lk;
         g.out_f32 = eb == 4;
         g.round_tf32 = kind;
-        g.splits = 1;
-        View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+                View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
         SKL_TRY(gemm_any(kind, "gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st));
         saved = sv;
     }
@@ -763,8 +769,7 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
         g.out2_c1 = (int)(2 * d.Lk);
         g.out_f32 = eb == 4;
         g.round_tf32 = kind;
-        g.splits = 1;
-        View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
+                View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
         SKL_TRY(gemm_any(kind, "gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st));
         if (grad_x) {
             GemmArgs g2 = {};
@@ -772,8 +777,7 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
             g2.out = grad_x;
             g2.ldo = d.d_in;
             g2.out_f32 = eb == 4;
-            g2.splits = 1;
-            View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
+                        View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
             SKL_TRY(gemm_any(kind, "gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st));
         }
     }

@@ -22,16 +22,8 @@ cudaError_t launch_gen_sketches(int dist, uint64_t seed, const SklDims& d, int e
 cudaError_t launch_init_u(uint64_t seed, const SklDims& d, int elem, void* U1s, void* U2s, cudaStream_t st);
 cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int unit_var, int transpose, int elem,
                            void* out, cudaStream_t st);
-cudaError_t launch_pack(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
-                        const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, cudaStream_t st);
+
 cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
                          const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, const void* bias,
                          float* bias32, cudaStream_t st);
-cudaError_t launch_to_f32(const void* in, int elem, float* out, int64_t n, cudaStream_t st);
-cudaError_t launch_reduce_partials(const float* part, int S, int64_t M, int64_t N, float alpha, float* out,
-                                   int64_t nb, int64_t blk, int64_t ldm, cudaStream_t st);
-int64_t colsum_chunks(int64_t rows);
-cudaError_t launch_colsum(const void* G, int elem, int64_t rows, int64_t N, float* part, float* out,
-                          cudaStream_t st);
-
 }  // namespace skl
