@@ -219,6 +219,60 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
             "peak_tflops_used": peak_tf, "phased_backward": phased}
 
 
+def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers=12):
+    """BASELINE config 5: the 12-layer BERT-base stack of SKLinear FFN/proj
+    layers (paper_2601_15473_b200.model.bert_ffn_stack: 72 SKLinear layers,
+    ReLU fused), fwd + bwd of T tokens per GPU; at N > 1 every layer's dU
+    bucket is all-reduced (NCCL) overlapped with the layers below it."""
+    import torch.distributed as dist
+    from paper_2601_15473_b200.model import bert_ffn_stack, wait_all
+    chain = bert_ffn_stack(num_layers=num_layers, device=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(11)
+    x = torch.randn(T, 768, device=dev, generator=gen).to(torch.bfloat16)
+    g = torch.randn(T, 768, device=dev, generator=gen).to(torch.bfloat16)
+    buckets = chain.allocate_grads(dev)
+
+    def step():
+        chain.forward(x)
+        _, works = chain.backward(g, buckets=buckets, need_grad_x=False, overlap=world > 1)
+        wait_all(works)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    e0.record(st)
+    for _ in range(steps):
+        step()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    peak_bf16, peak_bw, _ = peaks()
+    t_roof = 0.0
+    flops = 0
+    for stp in chain.steps:
+        L = stp.layer
+        tr, _, f, _ = roofline_time(L.d_in, L.d_out, L.num_terms, L.low_rank, T, 2, peak_bf16, peak_bw)
+        t_roof += tr
+        flops += f
+    del chain, buckets
+    torch.cuda.empty_cache()
+    return {"workload": f"c5 BERT-base {num_layers}-layer SKLinear FFN/proj stack ({6 * num_layers} SKLinear, "
+                        f"fused ReLU), fwd+bwd, {T} tokens per GPU" + (f", dp{world} overlapped all-reduce"
+                                                                        if world > 1 else ""),
+            "dtype": "bf16", "tokens": T * world, "ms_per_step": ms, "tokens_per_s": world * T / (ms / 1e3),
+            "bound": "tensor", "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
+            "tflops": flops / (ms / 1e3) / 1e12, "n_gpus": world}
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -391,6 +445,11 @@ def main():
            "ms_per_step": ms_e2e, "path": "pinned host X,G -> sketched_linear_forward/backward -> grads to host"}
 
     workloads = None
+    if world > 1 and not args.no_sweep:  # the stack exercises the per-layer overlapped all-reduce
+        try:
+            workloads = [measure_stack(skl, torch, dev, world)]
+        except Exception as e:
+            workloads = [{"workload": "c5 stack", "error": str(e)[:200]}]
     if world == 1 and not args.no_sweep:
         workloads = []
         for (name, di, do, l, k, tt, dt) in SWEEP:
@@ -399,6 +458,10 @@ def main():
             except Exception as e:  # report, never fake
                 workloads.append({"workload": name, "error": str(e)[:200]})
             torch.cuda.empty_cache()
+        try:
+            workloads.append(measure_stack(skl, torch, dev, world))
+        except Exception as e:
+            workloads.append({"workload": "c5 stack", "error": str(e)[:200]})
         try:  # the DP schedule's phased backward (two dU launches, 8 SMs left to NCCL), no collective
             skl.set_reserved_sms(RESERVED_SMS)
             workloads.append(measure_workload(skl, torch, dev, "c2 bf16, DP-phased backward (8 SMs reserved)",

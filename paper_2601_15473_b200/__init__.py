@@ -36,8 +36,10 @@ ABI_SYMBOLS = (
     "skl_generate_sketches", "skl_init_params", "skl_realize_sketch", "skl_workspace_size",
     "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads", "skl_launch_count",
     "skl_profile_enable", "skl_profile_collect", "sketched_linear_backward_phase", "skl_set_reserved_sms",
+    "sketched_linear_forward_ex", "sketched_linear_backward_ex",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
+FUSE_RELU_OUT, FUSE_RELU_IN = 1, 2
 
 
 class SklError(RuntimeError):
@@ -112,6 +114,8 @@ def lib() -> ctypes.CDLL:
     L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 12 + [sz, vp]
     L.sketched_linear_backward_phase.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 12 + [sz, vp]
     L.skl_set_reserved_sms.argtypes = [ctypes.c_int]
+    L.sketched_linear_forward_ex.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 9 + [sz, vp]
+    L.sketched_linear_backward_ex.argtypes = [sp, i64, ctypes.c_uint, ctypes.c_uint] + [vp] * 12 + [sz, vp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
     L.skl_launch_count.restype = u64
     L.skl_profile_enable.argtypes = [ctypes.c_int]
@@ -193,11 +197,12 @@ def init_params(s: _Shape, seed, U1s, U2s, stream=None):
     _check(lib().skl_init_params(ctypes.byref(s), seed, _ptr(U1s), _ptr(U2s), _stream(stream)))
 
 
-def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None):
+def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None, fuse=0):
+    """sketched_linear_forward(_ex): fuse = FUSE_RELU_OUT applies the following ReLU."""
     T = x.shape[0]
-    _check(lib().sketched_linear_forward(ctypes.byref(s), T, _ptr(x), _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s),
-                                         _ptr(bias), _ptr(y), _ptr(saved), _ptr(workspace),
-                                         workspace.numel() if workspace is not None else 0, _stream(stream)))
+    _check(lib().sketched_linear_forward_ex(ctypes.byref(s), T, fuse, _ptr(x), _ptr(S1s), _ptr(S2s), _ptr(U1s),
+                                            _ptr(U2s), _ptr(bias), _ptr(y), _ptr(saved), _ptr(workspace),
+                                            workspace.numel() if workspace is not None else 0, _stream(stream)))
 
 
 def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace, stream=None):
@@ -209,14 +214,15 @@ def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db,
 
 
 def backward_phase(s: _Shape, phases, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace,
-                   stream=None):
-    """sketched_linear_backward_phase: BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s)."""
+                   stream=None, fuse=0):
+    """sketched_linear_backward_ex: phases BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s) / BWD_ALL;
+    fuse = FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward)."""
     T = x.shape[0]
-    _check(lib().sketched_linear_backward_phase(ctypes.byref(s), T, phases, _ptr(g), _ptr(x), _ptr(saved),
-                                                _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s), _ptr(grad_x),
-                                                _ptr(dU1s), _ptr(dU2s), _ptr(db), _ptr(workspace),
-                                                workspace.numel() if workspace is not None else 0,
-                                                _stream(stream)))
+    _check(lib().sketched_linear_backward_ex(ctypes.byref(s), T, phases, fuse, _ptr(g), _ptr(x), _ptr(saved),
+                                             _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s), _ptr(grad_x),
+                                             _ptr(dU1s), _ptr(dU2s), _ptr(db), _ptr(workspace),
+                                             workspace.numel() if workspace is not None else 0,
+                                             _stream(stream)))
 
 
 def set_reserved_sms(n: int):

@@ -49,6 +49,11 @@ struct B2BArgs {
                         // matter: per-SM TMA ingest grows ~2.5x from 4 KB to 16 KB boxes)
     int dbg;            // perf-bisection switches (SKL_B2B_DEBUG): 1 skip GEMM2 epilogue math/stores, 4 skip GEMM2 MMAs
     long long ld_save;
+    // Fused neighbours of the layer in a Linear/ReLU chain (nn_model.cpp:111-122):
+    int relu;           // forward: out = max(0, ·)  (Relu::forward, nn_layers.cpp:341-345)
+    const void* mask;   // backward: out *= (mask > 0), mask = the layer input [T, N2] that a ReLU
+                        // produced (Relu::backward, nn_layers.cpp:347-354); nullable
+    long long ld_mask;
 };
 
 namespace dev {
@@ -141,7 +146,9 @@ struct B2BCfg {
 //          [L*k][d_out] (MN-major tiles).  No packing pass.
 // kMode 2: backward straight from the stacks: B1 = U1s|S2s [L*k][d_out]
 //          (K-major), B2 = S1s|U2s [L*d_in][k] (K-major, per-term row offset).
-template <int kCG, int kMode, int kKind>
+// kPost: the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
+// mask); a separate instantiation so the plain layer keeps its register budget.
+template <int kCG, int kMode, int kKind, bool kPost>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
@@ -542,6 +549,12 @@ __global__ void __launch_bounds__(384, 1)
                 SKL_TIMED(3, named_bar_sync(1 + wg, 128));
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
                 const long long tm0 = clock64();
+                // 16-B chunk of the ReLU mask (the layer input) for columns [col, col + 16 B)
+                auto mask_chunk = [&](int col) -> uint4 {
+                    if (args.mask == nullptr || !row_ok || col >= args.N2) return make_uint4(0u, 0u, 0u, 0u);
+                    return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(args.mask) +
+                                                                ((long long)row * args.ld_mask + col) * C::kElem));
+                };
                 if constexpr (kKind == 1) {
                     // fp32 output: the group's 64 columns are two [128 x 32] fp32 boxes
 #pragma unroll
@@ -549,11 +562,23 @@ __global__ void __launch_bounds__(384, 1)
                         const float4 b4 = reinterpret_cast<const float4*>(bias_g + s * 64)[c];
                         const uint32_t* src = (c < 8) ? ra : rb;
                         const int o = (c & 7) * 4;
+                        float v[4] = {fmaf(__uint_as_float(src[o]), alpha, b4.x),
+                                      fmaf(__uint_as_float(src[o + 1]), alpha, b4.y),
+                                      fmaf(__uint_as_float(src[o + 2]), alpha, b4.z),
+                                      fmaf(__uint_as_float(src[o + 3]), alpha, b4.w)};
+                        if (kPost && args.relu) {
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) v[i] = fmaxf(v[i], 0.f);
+                        }
+                        if (kPost && args.mask) {
+                            const uint4 mk = mask_chunk(n0 + 4 * c);
+                            const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(m[i]) > 0.f ? v[i] : 0.f;
+                        }
                         st_shared_v4(row_addr + (c >> 3) * 16384 + ((uint32_t)((c & 7) ^ (srow & 7)) << 4),
-                                     __float_as_uint(fmaf(__uint_as_float(src[o]), alpha, b4.x)),
-                                     __float_as_uint(fmaf(__uint_as_float(src[o + 1]), alpha, b4.y)),
-                                     __float_as_uint(fmaf(__uint_as_float(src[o + 2]), alpha, b4.z)),
-                                     __float_as_uint(fmaf(__uint_as_float(src[o + 3]), alpha, b4.w)));
+                                     __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
+                                     __float_as_uint(v[3]));
                     }
                     fence_proxy_async_smem();
                     named_bar_sync(1 + wg, 128);
@@ -572,11 +597,26 @@ __global__ void __launch_bounds__(384, 1)
                     const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                     const uint32_t* src = (c < 4) ? ra : rb;
                     const int o = (c & 3) * 8;
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) v[i] = fmaf(__uint_as_float(src[o + i]), alpha, bv[i]);
+                    if (kPost && args.relu) {
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
+                    }
+                    if (kPost && args.mask) {
+                        const uint4 mk = mask_chunk(n0 + 8 * c);
+                        const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&m[i]));
+                            v[2 * i] = f.x > 0.f ? v[2 * i] : 0.f;
+                            v[2 * i + 1] = f.y > 0.f ? v[2 * i + 1] : 0.f;
+                        }
+                    }
                     uint32_t w[4];
 #pragma unroll
-                    for (int i = 0; i < 4; ++i)
-                        w[i] = pack_bf16x2(fmaf(__uint_as_float(src[o + 2 * i]), alpha, bv[2 * i]),
-                                           fmaf(__uint_as_float(src[o + 2 * i + 1]), alpha, bv[2 * i + 1]));
+                    for (int i = 0; i < 4; ++i) w[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
                     st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
                 }
                 fence_proxy_async_smem();

@@ -40,6 +40,9 @@ struct GemmArgs {
     int out2_c0, out2_c1;
     int out_f32;     // 1: fp32 output, 0: bf16 output
     int round_tf32;  // 1: round outputs to TF32 (cvt.rna) -- they feed a TF32 GEMM
+    int relu;        // out = max(0, ·)            (fused Relu::forward)
+    const void* mask;  // out *= (mask > 0), mask [M][ld_mask] in the output type (fused Relu::backward)
+    long long ld_mask;
 };
 
 namespace dev {
@@ -219,7 +222,37 @@ __global__ void __launch_bounds__(256, 1)
                     const uint32_t bits = j < 32 ? ra[j] : rb[j - 32];
                     const float b = (args.bias != nullptr && n + j < args.N) ? __ldg(args.bias + n + j) : 0.f;
                     v[j] = fmaf(__uint_as_float(bits), args.alpha, b);
+                    if (args.relu) v[j] = fmaxf(v[j], 0.f);
                     if (args.round_tf32) v[j] = tf32_rna(v[j]);
+                }
+                if (args.mask && row < args.M) {
+                    // 128 B of the ReLU mask row (the layer input) covering these columns
+                    const uint8_t* mrow = reinterpret_cast<const uint8_t*>(args.mask) +
+                                          ((long long)row * args.ld_mask + n) * (args.out_f32 ? 4 : 2);
+                    if (args.out_f32) {
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch) {
+                            if (n + 4 * ch >= args.N) break;
+                            const uint4 mk = __ldg(reinterpret_cast<const uint4*>(mrow + ch * 16));
+                            const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                if (__uint_as_float(m[i]) <= 0.f) v[4 * ch + i] = 0.f;
+                        }
+                    } else {
+#pragma unroll
+                        for (int ch = 0; ch < 8; ++ch) {
+                            if (n + 8 * ch >= args.N) break;
+                            const uint4 mk = __ldg(reinterpret_cast<const uint4*>(mrow + ch * 16));
+                            const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
+#pragma unroll
+                            for (int i = 0; i < 4; ++i) {
+                                const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&m[i]));
+                                if (f.x <= 0.f) v[8 * ch + 2 * i] = 0.f;
+                                if (f.y <= 0.f) v[8 * ch + 2 * i + 1] = 0.f;
+                            }
+                        }
+                    }
                 }
                 // columns [out2_c0, out2_c1) also go out transposed: out2[(n - c0) * ldo2 + row]
                 if (args.out2 && row < args.M && n + ecols > args.out2_c0 && n < args.out2_c1) {

@@ -190,7 +190,7 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode, int kKind>
+template <int kCG, int kMode, int kKind, bool kPost = false>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     using C = dev::B2BCfg<kCG, kMode, kKind>;
     constexpr int eb = C::kElem, bk = C::kBK;
@@ -226,7 +226,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     }();
     if (grid_cap > 0) sms = std::min(sms, grid_cap);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
-    auto kern = dev::b2b_kernel<kCG, kMode, kKind>;
+    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost>;
     static bool attr_set = false;
     if (!attr_set) {
         SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
@@ -269,6 +269,13 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         };
         while (r > 8 && !ok(r)) r /= 2;
         a.b1rows = r;
+    }
+    if (a.relu || a.mask) {  // fused ReLU / ReLU-mask epilogue (CTA pairs only)
+        if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "fused ReLU needs the CTA-pair kernel (SKL_B2B_CG=2)");
+        if (kind == 1) return run_b2b_cg<2, 0, 1, true>(name, src, a, sms, st);
+        if (mode == 1) return run_b2b_cg<2, 1, 0, true>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2, 0, true>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0, 0, true>(name, src, a, sms, st);
     }
     if (kind == 1) {
         if (g_b2b_cg == 2) return run_b2b_cg<2, 0, 1>(name, src, a, sms, st);
@@ -592,6 +599,14 @@ skl_status skl_workspace_size(const skl_shape* s, int64_t T, size_t* fwd_bytes, 
 skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x, const void* S1s, const void* S2s,
                                    const void* U1s, const void* U2s, const void* bias, void* y, void* saved_proj,
                                    void* workspace, size_t ws_bytes, void* stream) {
+    return sketched_linear_forward_ex(s, T, 0, x, S1s, S2s, U1s, U2s, bias, y, saved_proj, workspace, ws_bytes,
+                                      stream);
+}
+
+skl_status sketched_linear_forward_ex(const skl_shape* s, int64_t T, unsigned fuse, const void* x, const void* S1s,
+                                      const void* S2s, const void* U1s, const void* U2s, const void* bias, void* y,
+                                      void* saved_proj, void* workspace, size_t ws_bytes, void* stream) {
+    if (fuse & ~(unsigned)SKL_FUSE_RELU_OUT) return fail(SKL_ERR_PARAM, "forward: unsupported fuse flags %u", fuse);
     SklDims d;
     SKL_TRY(get_dims(s, d));
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::forward: T must be >= 0");
@@ -622,6 +637,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
         a.R_pad = (int)d.R_pad;
         a.N2 = (int)d.d_out;
         a.alpha = inv;
+        a.relu = (fuse & SKL_FUSE_RELU_OUT) ? 1 : 0;
         a.bias = direct ? reinterpret_cast<const float*>(bias) : bias32;
         a.bias_bf16 = direct ? 1 : 0;
         a.out = y;
@@ -654,6 +670,7 @@ skl_status sketched_linear_forward(const skl_shape* s, int64_t T, const void* x,
     SKL_TRY(gemm_any(eb == 4, "gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st));
     GemmArgs g2 = {};
     g2.alpha = inv;
+    g2.relu = (fuse & SKL_FUSE_RELU_OUT) ? 1 : 0;
     g2.bias = bias32;
     g2.out = y;
     g2.ldo = d.d_out;
@@ -667,8 +684,8 @@ skl_status sketched_linear_backward(const skl_shape* s, int64_t T, const void* g
                                     const void* saved_proj, const void* S1s, const void* S2s, const void* U1s,
                                     const void* U2s, void* grad_x, float* grad_U1s, float* grad_U2s,
                                     float* grad_bias, void* workspace, size_t ws_bytes, void* stream) {
-    return sketched_linear_backward_phase(s, T, SKL_BWD_ALL, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x,
-                                          grad_U1s, grad_U2s, grad_bias, workspace, ws_bytes, stream);
+    return sketched_linear_backward_ex(s, T, SKL_BWD_ALL, 0, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x,
+                                       grad_U1s, grad_U2s, grad_bias, workspace, ws_bytes, stream);
 }
 
 skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigned phases, const void* grad_y,
@@ -676,6 +693,16 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
                                           const void* U1s, const void* U2s, void* grad_x, float* grad_U1s,
                                           float* grad_U2s, float* grad_bias, void* workspace, size_t ws_bytes,
                                           void* stream) {
+    return sketched_linear_backward_ex(s, T, phases, 0, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x, grad_U1s,
+                                       grad_U2s, grad_bias, workspace, ws_bytes, stream);
+}
+
+skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned phases, unsigned fuse,
+                                       const void* grad_y, const void* x, const void* saved_proj, const void* S1s,
+                                       const void* S2s, const void* U1s, const void* U2s, void* grad_x,
+                                       float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
+                                       size_t ws_bytes, void* stream) {
+    if (fuse & ~(unsigned)SKL_FUSE_RELU_IN) return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
     SklDims d;
     SKL_TRY(get_dims(s, d));
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::backward: T must be >= 0");
@@ -745,6 +772,8 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
         a.N2 = (int)d.d_in;
         a.alpha = inv;
         a.bias = nullptr;
+        a.mask = (fuse & SKL_FUSE_RELU_IN) ? x : nullptr;  // grad_x *= (x > 0): the preceding ReLU's backward
+        a.ld_mask = d.d_in;
         a.out = grad_x;
         a.ldo = d.d_in;
         a.save = p2t;  // P_S2ᵀ [Lk][T8]
@@ -774,6 +803,8 @@ skl_status sketched_linear_backward_phase(const skl_shape* s, int64_t T, unsigne
         if (grad_x) {
             GemmArgs g2 = {};
             g2.alpha = inv;
+            g2.mask = (fuse & SKL_FUSE_RELU_IN) ? x : nullptr;
+            g2.ld_mask = d.d_in;
             g2.out = grad_x;
             g2.ldo = d.d_in;
             g2.out_f32 = eb == 4;

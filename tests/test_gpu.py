@@ -293,3 +293,87 @@ def test_dp_overlapped_step_over_nccl(skl, port):
         assert rel < 1e-5, rel
     finally:
         dist.destroy_process_group()
+
+
+# --------------------------------------------------------------------------- Linear/ReLU chains
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_chain_with_fused_relu_matches_oracle(skl, port, dtype_name):
+    """model_forward over SKLinear / ReLU layers (nn_model.cpp:111-122) with the
+    ReLU fused into the neighbouring kernels, forward + training backward, vs
+    the layer-by-layer f64 oracle composition (Relu::forward/backward,
+    nn_layers.cpp:341-354) on the same rounded parameters and input."""
+    import oracle
+    from paper_2601_15473_b200.model import Relu, SkChain
+    from tests._util import check_close
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    dims = [(96, 160, 2, 32), (160, 128, 1, 64), (128, 64, 3, 16)]
+    T = 150
+    layers = []
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    for i, (di, do, L, k) in enumerate(dims):
+        lyr = skl.SkLinear(di, do, L, k, seed=100 + i, dtype=dtype)
+        lyr.bias.copy_((torch.randn(do, device="cuda", generator=gen) * 0.3).to(td))
+        layers.append(lyr)
+    chain = SkChain([layers[0], Relu(), layers[1], layers[2]])
+    x = torch.randn(T, 96, device="cuda", generator=gen).to(td)
+    g = torch.randn(T, 64, device="cuda", generator=gen).to(td)
+    y = chain.forward(x)
+    grads, works = chain.backward(g, overlap=False)
+    torch.cuda.synchronize()
+    # oracle, layer by layer on the device's own (rounded) layer inputs, so each
+    # fused kernel is checked at its own tolerance (an all-f64 composition
+    # would compound the rounding of the bf16 activations and flip ReLU masks
+    # at pre-activations within one rounding step of zero)
+    P = [oracle.from_abi(l.d_in, l.d_out, _np(l.S1s), _np(l.U1s), _np(l.U2s), _np(l.S2s)) for l in layers]
+    B = [_np(l.bias) for l in layers]
+    a0 = _np(x).T.copy()
+    a1 = _np(chain.steps[1].x).T.copy()
+    a2 = _np(chain.steps[2].x).T.copy()
+    check_close("chain relu(layer0)", a1, np.maximum(port.forward(P[0], B[0], a0), 0.0), dtype_name)
+    check_close("chain layer1", a2, port.forward(P[1], B[1], a1), dtype_name)
+    check_close("chain y", _np(y), port.forward(P[2], B[2], a2).T, dtype_name)
+    g3 = _np(g).T.copy()
+    gx3, *r3 = port.backward(P[2], a2, g3)
+    gx2, *r2 = port.backward(P[1], a1, gx3)
+    g1 = np.where(a1 > 0, gx2, 0.0)                      # Relu::backward
+    gx1, *r1 = port.backward(P[0], a0, g1)
+    check_close("chain grad_x", _np(grads.grad_x), gx1.T, dtype_name)
+    for i, r in enumerate((r1, r2, r3)):
+        _, du1, du2, db = oracle.grads_to_abi(np.zeros((1, 1)), *r)
+        b = grads.layers[i]
+        check_close(f"chain dU1s[{i}]", _np(b.dU1s), du1, dtype_name)
+        check_close(f"chain dU2s[{i}]", _np(b.dU2s), du2, dtype_name)
+        check_close(f"chain db[{i}]", _np(b.db), db, dtype_name)
+
+
+def test_bert_stack_overlapped_dp_step_runs(skl):
+    """Config 5 at reduced depth: the BERT FFN/proj stack with the phased,
+    per-layer all-reduce schedule on a world-1 NCCL group gives the same
+    gradients as the plain backward."""
+    import socket
+    import torch.distributed as dist
+    from paper_2601_15473_b200.model import bert_ffn_stack, wait_all
+    chain = bert_ffn_stack(num_layers=2)
+    T = 1024
+    x = torch.randn(T, 768, device="cuda").to(torch.bfloat16)
+    g = torch.randn(T, 768, device="cuda").to(torch.bfloat16)
+    chain.forward(x)
+    ref, _ = chain.backward(g, overlap=False)
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port_ = sock.getsockname()[1]
+    sock.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        got, works = chain.backward(g, overlap=True)
+        assert len(works) == 2 * len(chain.steps)
+        wait_all(works)
+        torch.cuda.synchronize()
+        assert torch.equal(got.grad_x, ref.grad_x)
+        for a, b in zip(got.layers, ref.layers):
+            rel = (a.flat - b.flat).norm() / b.flat.norm()
+            assert rel < 1e-5, rel
+    finally:
+        dist.destroy_process_group()
