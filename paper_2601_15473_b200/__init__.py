@@ -56,6 +56,10 @@ class ParameterError(SklError, ValueError):
     """rnla::parameter_error (errors.hpp:16-19)."""
 
 
+class LoadError(SklError):
+    """rnla::nn::load_error (errors.hpp:40-45): malformed or incompatible model file."""
+
+
 class _Shape(ctypes.Structure):
     _fields_ = [("d_in", ctypes.c_int64), ("d_out", ctypes.c_int64), ("num_terms", ctypes.c_int64),
                 ("low_rank", ctypes.c_int64), ("dtype", ctypes.c_int)]
@@ -248,7 +252,8 @@ class SkLinear:
     derive_seed(seed, 1000+i), zero bias -- all generated on the GPU.
     """
 
-    def __init__(self, d_in, d_out, num_terms, low_rank, seed=0, dist=GAUSSIAN, dtype=BF16, device="cuda"):
+    def __init__(self, d_in, d_out, num_terms, low_rank, seed=0, dist=GAUSSIAN, dtype=BF16, device="cuda",
+                 _fresh=True):
         import torch
         if num_terms < 1 or low_rank < 1:
             raise ParameterError(2, "SkLinear: num_terms and low_rank must be >= 1")
@@ -262,9 +267,49 @@ class SkLinear:
         self.U1s = torch.empty(L, k, d_out, dtype=td, device=device)
         self.U2s = torch.empty(L, d_in, k, dtype=td, device=device)
         self.bias = torch.zeros(d_out, dtype=td, device=device)
-        generate_sketches(self.shape, dist, seed, self.S1s, self.S2s)
-        init_params(self.shape, seed, self.U1s, self.U2s)
+        # sketch descriptors in reference order [s1_0, s2_0, s1_1, ...] (dist, rows, cols, seed):
+        # what model_save serialises instead of the values (nn_model.cpp:250-265)
+        dname = "gaussian" if dist == GAUSSIAN else "rademacher"
+        self.sketches = [d for i in range(L) for d in ((dname, k, d_out, derive_seed(seed, 2 * i)),
+                                                         (dname, k, d_in, derive_seed(seed, 2 * i + 1)))]
+        if _fresh:
+            generate_sketches(self.shape, dist, seed, self.S1s, self.S2s)
+            init_params(self.shape, seed, self.U1s, self.U2s)
         self._ws = None
+
+    @classmethod
+    def from_parts(cls, d_in, d_out, num_terms, low_rank, sketches, u1, u2, bias, dtype=BF16, device="cuda"):
+        """A layer from sketch DESCRIPTORS plus explicit U / bias in the reference's
+        layout (sk_linear_from_json, nn_model.cpp:290-311): the sketches are
+        re-realised on the device from (dist, rows, cols, seed) -- bit-identical to
+        SketchOp::realized -- and u1 [L][k][d_in], u2 [L][d_out][k] are transposed
+        into the U2s / U1s stacks."""
+        import numpy as np
+        import torch
+        L, k = num_terms, low_rank
+        if len(sketches) != 2 * L:
+            raise ShapeError(1, "SKLinear: expected 2*num_terms sketches")
+        lyr = cls(d_in, d_out, L, k, seed=0, dtype=dtype, device=device, _fresh=False)
+        for i in range(L):
+            for j, (dname, rows, cols, seed) in enumerate(sketches[2 * i: 2 * i + 2]):
+                if dname not in ("gaussian", "rademacher"):
+                    raise ParameterError(2, f"SKLinear: sketch distribution {dname!r} is not on this path")
+                want = d_out if j == 0 else d_in
+                if rows != k or cols != want:
+                    raise ShapeError(1, f"SKLinear: sketch {2 * i + j} is {rows}x{cols}, expected {k}x{want}")
+                dist = GAUSSIAN if dname == "gaussian" else RADEMACHER
+                if j == 0:   # s1_i == S2s[i] [k, d_out]
+                    realize_sketch(dist, k, d_out, seed, lyr.S2s[i])
+                else:        # s2_i == S1s[i]ᵀ  [d_in, k]
+                    realize_sketch(dist, k, d_in, seed, lyr.S1s[i], transpose=True)
+        lyr.sketches = [tuple(s) for s in sketches]
+        td = torch_dtype(dtype)
+        u1 = np.asarray(u1, dtype=np.float64).reshape(L, k, d_in)
+        u2 = np.asarray(u2, dtype=np.float64).reshape(L, d_out, k)
+        lyr.U2s.copy_(torch.from_numpy(np.ascontiguousarray(u1.transpose(0, 2, 1))).to(device=device, dtype=td))
+        lyr.U1s.copy_(torch.from_numpy(np.ascontiguousarray(u2.transpose(0, 2, 1))).to(device=device, dtype=td))
+        lyr.bias.copy_(torch.from_numpy(np.asarray(bias, dtype=np.float64)).to(device=device, dtype=td))
+        return lyr
 
     def params(self):
         """SkLinear::params -> (learnable, total_stored, dense_equivalent)."""

@@ -79,6 +79,15 @@ class SkChain:
         self.dtype = self.steps[0].layer.dtype
         self._ws = None
 
+    def layers(self):
+        """The chain as a layer list (SkLinear / Relu), e.g. for model_save."""
+        out = []
+        for st in self.steps:
+            out.append(st.layer)
+            if st.relu_out:
+                out.append(Relu())
+        return out
+
     @property
     def d_in(self):
         return self.steps[0].layer.d_in
