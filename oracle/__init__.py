@@ -215,6 +215,18 @@ class Oracle:
 # Layout helpers: reference (column convention, per-term) <-> ABI (row
 # convention, pawX [L, d, k] stacks).  Pure data movement, exact.
 # ---------------------------------------------------------------------------
+def sk_linear_from_dense(o: "Oracle", W: np.ndarray, l: int, k: int, seed: int, dist: int = GAUSSIAN) -> Params:
+    """sk_linear_from_dense (nn_layers.cpp:149-160): sketches seeded like
+    sk_linear_shell (:124-127), u1_i = s1_i·W [k, d_in], u2_i = W·s2_iᵀ
+    [d_out, k] (f64 matmul; the reference's gemm_rows order is irrelevant at f64
+    against the bf16/TF32 gates)."""
+    d_out, d_in = W.shape
+    p = o.sk_linear_fresh(d_in, d_out, l, k, seed, dist)   # same sketches; U replaced below
+    u1 = np.stack([p.s1[i] @ W for i in range(l)])
+    u2 = np.stack([W @ p.s2[i].T for i in range(l)])
+    return Params(d_in, d_out, l, k, p.s1, u1, p.s2, u2)
+
+
 def to_abi(p: Params):
     """-> dict(S1s [L,d_in,k], U1s [L,k,d_out], U2s [L,d_in,k], S2s [L,k,d_out])."""
     return dict(

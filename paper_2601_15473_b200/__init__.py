@@ -36,7 +36,7 @@ ABI_SYMBOLS = (
     "skl_generate_sketches", "skl_init_params", "skl_realize_sketch", "skl_workspace_size",
     "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads", "skl_launch_count",
     "skl_profile_enable", "skl_profile_collect", "sketched_linear_backward_phase", "skl_set_reserved_sms",
-    "sketched_linear_forward_ex", "sketched_linear_backward_ex",
+    "sketched_linear_forward_ex", "sketched_linear_backward_ex", "skl_from_dense", "skl_from_dense_workspace_size",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
 FUSE_RELU_OUT, FUSE_RELU_IN = 1, 2
@@ -118,6 +118,8 @@ def lib() -> ctypes.CDLL:
     L.sketched_linear_backward.argtypes = [sp, i64] + [vp] * 12 + [sz, vp]
     L.sketched_linear_backward_phase.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 12 + [sz, vp]
     L.skl_set_reserved_sms.argtypes = [ctypes.c_int]
+    L.skl_from_dense_workspace_size.argtypes = [sp, ctypes.POINTER(sz)]
+    L.skl_from_dense.argtypes = [sp, ctypes.c_int, u64] + [vp] * 8 + [sz, vp]
     L.sketched_linear_forward_ex.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 9 + [sz, vp]
     L.sketched_linear_backward_ex.argtypes = [sp, i64, ctypes.c_uint, ctypes.c_uint] + [vp] * 12 + [sz, vp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
@@ -276,6 +278,26 @@ class SkLinear:
             generate_sketches(self.shape, dist, seed, self.S1s, self.S2s)
             init_params(self.shape, seed, self.U1s, self.U2s)
         self._ws = None
+
+    @classmethod
+    def from_dense(cls, W, bias, num_terms, low_rank, seed=0, dist=GAUSSIAN, dtype=BF16):
+        """sk_linear_from_dense (nn_layers.cpp:149-160), computed on the device:
+        W [d_out, d_in] (the reference's DenseLinear::w), bias [d_out] or None."""
+        import torch
+        d_out, d_in = W.shape
+        if bias is not None and bias.numel() != d_out:
+            raise ShapeError(1, "sk_linear_from_dense: bias length != d_out")
+        lyr = cls(d_in, d_out, num_terms, low_rank, seed=seed, dist=dist, dtype=dtype, device=W.device, _fresh=False)
+        td = torch_dtype(dtype)
+        Wd = W.to(td).contiguous()
+        bd = bias.to(td).contiguous() if bias is not None else None
+        n = ctypes.c_size_t()
+        _check(lib().skl_from_dense_workspace_size(ctypes.byref(lyr.shape), ctypes.byref(n)))
+        ws = torch.empty(n.value, dtype=torch.uint8, device=W.device)
+        _check(lib().skl_from_dense(ctypes.byref(lyr.shape), dist, seed, _ptr(Wd), _ptr(bd), _ptr(lyr.S1s),
+                                    _ptr(lyr.S2s), _ptr(lyr.U1s), _ptr(lyr.U2s), _ptr(lyr.bias), _ptr(ws), n.value,
+                                    _stream(None)))
+        return lyr
 
     @classmethod
     def from_parts(cls, d_in, d_out, num_terms, low_rank, sketches, u1, u2, bias, dtype=BF16, device="cuda"):

@@ -275,4 +275,40 @@ cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void
     return cudaGetLastError();
 }
 
+// out[c][r] = in[r][c] for a [rows][cols] matrix; 32x32 smem tiles (coalesced
+// both ways).  Used once per conversion by skl_from_dense (W -> Wᵀ).
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows,
+                                                        int64_t cols) {
+    __shared__ T tile[32][33];
+    const int64_t tr = (rows + 31) / 32, tc = (cols + 31) / 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int64_t b = blockIdx.x; b < tr * tc; b += gridDim.x) {
+        const int64_t r0 = (b / tc) * 32, c0 = (b % tc) * 32;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = r0 + ty + 8 * i, c = c0 + tx;
+            if (r < rows && c < cols) tile[ty + 8 * i][tx] = in[r * cols + c];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int64_t c = c0 + ty + 8 * i, r = r0 + tx;
+            if (r < rows && c < cols) out[c * rows + r] = tile[tx][ty + 8 * i];
+        }
+    }
+}
+
+cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st) {
+    ProfScope ps_("transpose", st);
+    const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
+    const int grid = (int)std::min<int64_t>(tiles, 148 * 8);
+    if (elem == ELEM_BF16)
+        transpose_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, rows, cols);
+    else
+        transpose_kernel<float><<<grid, 256, 0, st>>>((const float*)in, (float*)out, rows, cols);
+    return cudaGetLastError();
+}
+
 }  // namespace skl

@@ -818,6 +818,66 @@ skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned p
                   di.sms, st);
 }
 
+skl_status skl_from_dense_workspace_size(const skl_shape* s, size_t* bytes) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    const size_t e = ebytes(s->dtype);
+    *bytes = align_up((size_t)d.R_pad * d.d_in * e) + align_up((size_t)d.d_in * d.d_out * e);
+    return SKL_OK;
+}
+
+// sk_linear_from_dense (nn_layers.cpp:149-160) on the device.  Reference:
+// u1_i = s1_i·W [k, d_in], u2_i = W·s2_iᵀ [d_out, k].  In the ABI stacks
+// (S2s[i] = s1_i, S1s[i] = s2_iᵀ):  U1s[i] = u2_iᵀ = S1s[i]ᵀ·Wᵀ  and
+// U2s[i] = u1_iᵀ = Wᵀ·S2s[i]ᵀ -- two tcgen05 GEMMs (all terms of U1s in one).
+skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed, const void* W,
+                          const void* bias_in, void* S1s, void* S2s, void* U1s, void* U2s, void* bias_out,
+                          void* workspace, size_t ws_bytes, void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (!W || !S1s || !S2s || !U1s || !U2s) return fail(SKL_ERR_PARAM, "null tensor argument");
+    if (dist != SKL_DIST_GAUSSIAN && dist != SKL_DIST_RADEMACHER) return fail(SKL_ERR_PARAM, "unknown dist %d", dist);
+    SKL_TRY(check_alignment(d, s->dtype));
+    const int eb = ebytes(s->dtype), elem = elem_of(s->dtype), kind = s->dtype == SKL_BF16 ? 0 : 1;
+    if ((d.k * eb) % 16)
+        return fail(SKL_ERR_UNSUPPORTED, "sk_linear_from_dense: low_rank must be a multiple of %d", 16 / eb);
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    size_t need = 0;
+    SKL_TRY(skl_from_dense_workspace_size(s, &need));
+    if (!workspace || ws_bytes < need)
+        return fail(SKL_ERR_WORKSPACE, "from_dense workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    void* acatT = workspace;                                                        // rows < Lk: S1s[i]ᵀ
+    void* wT = at<void>(workspace, align_up((size_t)d.R_pad * d.d_in * eb));       // Wᵀ [d_in][d_out]
+    SKL_CUDA(launch_gen_sketches((int)dist, layer_seed, d, elem, S1s, S2s, st));  // sk_linear_shell seeds
+    SKL_CUDA(cudaMemsetAsync(U2s, 0, (size_t)d.Lk * d.d_in * eb, st));            // (pack reads the U2 half)
+    SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, nullptr, nullptr, nullptr, st));
+    SKL_CUDA(launch_transpose(W, elem, d.d_out, d.d_in, wT, st));
+    GemmArgs g = {};
+    g.alpha = 1.f;
+    g.out = U1s;  // [L*k][d_out]
+    g.ldo = d.d_out;
+    g.out_f32 = eb == 4;
+    View va{acatT, d.Lk, d.d_in, d.d_in}, vw{W, d.d_out, d.d_in, d.d_in};
+    SKL_TRY(gemm_any(kind, "from_dense_U1", va, vw, (int)d.Lk, (int)d.d_out, (int)d.d_in, g, di.sms, st));
+    for (int64_t i = 0; i < d.L; ++i) {
+        GemmArgs g2 = {};
+        g2.alpha = 1.f;
+        g2.out = static_cast<uint8_t*>(U2s) + (size_t)i * d.d_in * d.k * eb;  // U2s[i] [d_in][k]
+        g2.ldo = d.k;
+        g2.out_f32 = eb == 4;
+        View vwt{wT, d.d_in, d.d_out, d.d_out};
+        View vs2{static_cast<const uint8_t*>(S2s) + (size_t)i * d.k * d.d_out * eb, d.k, d.d_out, d.d_out};
+        SKL_TRY(gemm_any(kind, "from_dense_U2", vwt, vs2, (int)d.d_in, (int)d.k, (int)d.d_out, g2, di.sms, st));
+    }
+    if (bias_out) {
+        if (bias_in) SKL_CUDA(cudaMemcpyAsync(bias_out, bias_in, (size_t)d.d_out * eb, cudaMemcpyDeviceToDevice, st));
+        else SKL_CUDA(cudaMemsetAsync(bias_out, 0, (size_t)d.d_out * eb, st));
+    }
+    return SKL_OK;
+}
+
 skl_status skl_set_reserved_sms(int n) {
     if (n < 0 || n > 64) return fail(SKL_ERR_PARAM, "reserved SMs must be in [0, 64], got %d", n);
     g_reserved_sms = n;

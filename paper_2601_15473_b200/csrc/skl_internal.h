@@ -26,4 +26,5 @@ cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int u
 cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
                          const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, const void* bias,
                          float* bias32, cudaStream_t st);
+cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st);
 }  // namespace skl

@@ -377,3 +377,28 @@ def test_bert_stack_overlapped_dp_step_runs(skl):
             assert rel < 1e-5, rel
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("d_in,d_out,L,k", [(256, 384, 2, 64), (96, 160, 3, 16)])
+def test_from_dense_matches_oracle(skl, port, dtype_name, d_in, d_out, L, k):
+    """sk_linear_from_dense on device (tcgen05 GEMMs) == the reference algorithm
+    (u1 = s1·W, u2 = W·s2ᵀ, nn_layers.cpp:149-160) on the same rounded W."""
+    import oracle
+    from tests._util import check_close
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    W = (torch.randn(d_out, d_in, device="cuda", generator=gen) * 0.05).to(td)
+    b = torch.randn(d_out, device="cuda", generator=gen).to(td)
+    lyr = skl.SkLinear.from_dense(W, b, L, k, seed=77, dtype=dtype)
+    torch.cuda.synchronize()
+    P = oracle.sk_linear_from_dense(port, _np(W), L, k, 77)
+    abi = oracle.to_abi(P)
+    from tests._util import bf16_round, f32_round
+    rnd = bf16_round if dtype == skl.BF16 else f32_round   # direct f64 -> element rounding (no double rounding)
+    assert np.array_equal(_np(lyr.S2s), rnd(abi["S2s"]))   # sketches bit-exact
+    assert np.array_equal(_np(lyr.S1s), rnd(abi["S1s"]))
+    check_close("from_dense U1s", _np(lyr.U1s), abi["U1s"], dtype_name)
+    check_close("from_dense U2s", _np(lyr.U2s), abi["U2s"], dtype_name)
+    assert torch.equal(lyr.bias, b)
