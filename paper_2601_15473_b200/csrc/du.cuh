@@ -48,6 +48,7 @@ struct DuArgs {
     int* tickets;    // [num_tiles], zero on entry, left zero on exit
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
+    int dbg;         // SKL_DU_DEBUG=1: per-CTA cycle accounting into g_du_prof (perf analysis)
 };
 
 namespace dev {
@@ -67,6 +68,12 @@ struct DuKind {
     static constexpr int kW = 128 / kElem;    // columns per MN-major block
     static constexpr int kUK = kKind == 0 ? 16 : 8;  // K per MMA instruction
 };
+
+// Per-CTA cycle accounting (DuArgs::dbg): [0] producer waits on empty stages,
+// [1] producer total, [2] MMA waits on full stages, [3] MMA total, [4] epilogue
+// colsum phase, [5] epilogue waits on the accumulator, [6] partial write,
+// [7] reduction (ticket wait + sum).
+__device__ unsigned long long g_du_prof[296][8];
 
 template <int kKind>
 __global__ void __launch_bounds__(256, 1)
@@ -141,13 +148,21 @@ __global__ void __launch_bounds__(256, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            unsigned long long w_empty = 0;
+            const long long t_beg = clock64();
             for (int u = pair; u < units; u += npairs) {
                 const Unit x = decode(u);
                 const CUtensorMap* ma = x.p ? &tmA1 : &tmA0;
                 const CUtensorMap* mb = x.p ? &tmB1 : &tmB0;
                 const int m0 = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256 + (int)rank * 128;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (args.dbg) {
+                        const long long t0 = clock64();
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        w_empty += (unsigned long long)(clock64() - t0);
+                    } else {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                    }
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
                     const int k0 = kb * KT::kBK;
@@ -170,6 +185,10 @@ __global__ void __launch_bounds__(256, 1)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
+            if (args.dbg) {
+                g_du_prof[blockIdx.x][0] = w_empty;
+                g_du_prof[blockIdx.x][1] = (unsigned long long)(clock64() - t_beg);
+            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (leader)
@@ -178,6 +197,8 @@ __global__ void __launch_bounds__(256, 1)
             int stage = 0;
             uint32_t phase = 0;
             int iter = 0;
+            unsigned long long w_full = 0;
+            const long long t_beg = clock64();
             for (int u = pair; u < units; u += npairs, ++iter) {
                 const Unit x = decode(u);
                 const int acc = iter & 1;
@@ -185,7 +206,13 @@ __global__ void __launch_bounds__(256, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kDuBN;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                    mbar_wait(&full[stage], phase);
+                    if (args.dbg) {
+                        const long long t0 = clock64();
+                        mbar_wait(&full[stage], phase);
+                        w_full += (unsigned long long)(clock64() - t0);
+                    } else {
+                        mbar_wait(&full[stage], phase);
+                    }
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * kDuABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
@@ -201,6 +228,10 @@ __global__ void __launch_bounds__(256, 1)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
                 mma_commit<2>(&tfull[acc]);
+            }
+            if (args.dbg) {
+                g_du_prof[blockIdx.x][2] = w_full;
+                g_du_prof[blockIdx.x][3] = (unsigned long long)(clock64() - t_beg);
             }
         }
     } else if (warp == 3) {
@@ -224,10 +255,20 @@ __global__ void __launch_bounds__(256, 1)
         int stage = 0;
         uint32_t phase = 0;
         int iter = 0;
+        unsigned long long e_cs = 0, e_acc = 0, e_part = 0, e_red = 0;
+        long long e_t = clock64();
+        auto lap = [&](unsigned long long& slot) {
+            if (args.dbg) {
+                const long long now = clock64();
+                slot += (unsigned long long)(now - e_t);
+                e_t = now;
+            }
+        };
         for (int u = pair; u < units; u += npairs, ++iter) {
             const Unit x = decode(u);
             const DuProblem& P = args.p[x.p];
             const int m0 = x.mt * 256, n0 = x.nt * 256;
+            lap(e_red);
             if (x.colsum) {
                 // ---- column sums of this CTA's 128 staged G columns: thread ->
                 // one 16-B chunk (kCPC columns) of one kW-column block, 8 token rows.
@@ -282,10 +323,12 @@ __global__ void __launch_bounds__(256, 1)
                 for (int kb = x.kb0; kb < x.kb1; ++kb)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
             }
+            lap(e_cs);
             // ---- accumulator -> fp32 partial [tile][split][256][256], our 128 rows
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
+            lap(e_acc);
             {
                 float* prow = args.part + (((long long)x.tile * args.splits + x.split) * 256 + rank * 128 + t) * kDuBN;
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
@@ -308,6 +351,7 @@ __global__ void __launch_bounds__(256, 1)
                 else mbar_arrive_cluster(&tempty[acc], 0);
             }
 
+            lap(e_part);
             // ---- deterministic split reduction (sum in split order 0..S-1)
             __threadfence();
             named_bar_sync(2, 128);
@@ -381,8 +425,14 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
         }
+        lap(e_red);
+        if (args.dbg && warp == 4 && lane == 0) {
+            g_du_prof[blockIdx.x][4] = e_cs;
+            g_du_prof[blockIdx.x][5] = e_acc;
+            g_du_prof[blockIdx.x][6] = e_part;
+            g_du_prof[blockIdx.x][7] = e_red;
+        }
     }
-
     tc_fence_before();
     cluster_sync();
     if (warp == 2) {

@@ -490,6 +490,8 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     }
     const int units = u.tiles * u.splits;  // CTA-pair work units
     a.relay = colsum ? 1 : 0;
+    static const int du_dbg = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;  // perf analysis
+    a.dbg = du_dbg;
     static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
     // one wave: cooperative launch, slice-parallel reduction; several waves:
     // persistent grid, the last CTA of each tile reduces it
@@ -926,6 +928,13 @@ extern "C" int skl_debug_b2b_prof(unsigned long long* out, int n) {
     const int total = 296 * 8;
     if (n > total) n = total;
     if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_prof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
+extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
+    const int total = 296 * 8;
+    if (n > total) n = total;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_prof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
         return -1;
     return n;
 }
