@@ -74,6 +74,7 @@ struct DuKind {
 // colsum phase, [5] epilogue waits on the accumulator, [6] partial write,
 // [7] reduction (ticket wait + sum).
 __device__ unsigned long long g_du_prof[296][8];
+__device__ unsigned long long g_du_wait[296][4];  // [cta]: fence+ticket wait, +fence, +sum, +colsum/release
 
 template <int kKind>
 __global__ void __launch_bounds__(256, 1)
@@ -92,6 +93,7 @@ __global__ void __launch_bounds__(256, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* ticket_s = reinterpret_cast<int*>(tmem_slot + 1);
+    uint64_t* rbar = tempty + 3;  // (8-B slot after tmem_slot/ticket_s) reduction bulk-load barrier
     float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [8][128]
 
     const uint32_t warp = warp_id();
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(256, 1)
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 8);
         }
+        mbar_init(rbar, 1);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(256, 1)
         const int t = (int)(q * 32 + lane);  // 0..127
         int stage = 0;
         uint32_t phase = 0;
+        uint32_t red_phase = 0;
         int iter = 0;
         unsigned long long e_cs = 0, e_acc = 0, e_part = 0, e_red = 0;
         long long e_t = clock64();
@@ -370,6 +374,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
                 named_bar_sync(2, 128);
+                if (args.dbg && t == 0) g_du_wait[blockIdx.x][0] = (unsigned long long)(clock64() - e_t);
                 const int z = 2 * x.split + (int)rank;
                 row_lo = z * 256 / parts;
                 row_hi = (z + 1) * 256 / parts;
@@ -384,27 +389,86 @@ __global__ void __launch_bounds__(256, 1)
                 col_lo = 0; col_hi = last ? kDuBN : 0;
             }
             __threadfence();
+            if (args.dbg && t == 0) g_du_wait[blockIdx.x][1] = (unsigned long long)(clock64() - e_t);
             const float* pbase = args.part + (long long)x.tile * args.splits * 256 * kDuBN;
             const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
                              (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
-            for (int f = t; f < (row_hi - row_lo) * (kDuBN / 4); f += 128) {
-                const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
-                const int m = m0 + r, n = n0 + c;
-                if (m >= P.M || n >= P.N) continue;
-                float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (int sp = 0; sp < args.splits; ++sp) {
-                    const float4 v =
-                        __ldcg(reinterpret_cast<const float4*>(pbase + ((long long)sp * 256 + r) * kDuBN + c));
-                    sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+            if (args.coop) {
+                // Cooperative (one unit per pair): the operand ring is idle now, so the
+                // S partial slices of this CTA's rows (S x rows x 1 KB = 128 KB, since
+                // rows = 256 / 2S) are pulled into smem with bulk copies -- all in flight
+                // at once -- and summed from smem.  (Register loads from far L2 were
+                // latency-bound: ~10 us for 128 KB.)
+                const int rows = row_hi - row_lo;
+                const uint32_t slice = (uint32_t)rows * kDuBN * 4;
+                if (t == 0 && rows > 0) {
+                    fence_proxy_async_global();  // partials were written by other CTAs' generic stores
+                    mbar_arrive_expect_tx(rbar, slice * (uint32_t)args.splits);
+                    for (int sp = 0; sp < args.splits; ++sp)
+                        bulk_load_1d(smem + (size_t)sp * slice, pbase + ((long long)sp * 256 + row_lo) * kDuBN, slice,
+                                     rbar);
                 }
-                const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
-                const long long mo = (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
-                if (vec && n + 4 <= P.N) {
-                    *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
-                } else {
-                    for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
+                if (rows > 0) mbar_wait(rbar, red_phase);
+                red_phase ^= 1u;
+                const float4* s4 = reinterpret_cast<const float4*>(smem);
+                for (int f = t; f < rows * (kDuBN / 4); f += 128) {
+                    const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
+                    const int m = m0 + r, n = n0 + c;
+                    float4 sum = s4[f];
+                    for (int sp = 1; sp < args.splits; ++sp) {
+                        const float4 v = s4[(size_t)sp * (slice / 16) + f];
+                        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+                    }
+                    if (m >= P.M || n >= P.N) continue;
+                    const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
+                    const long long mo = P.mb >= P.M ? (long long)m * P.ms : (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
+                    if (vec && n + 4 <= P.N) {
+                        *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
+                    } else {
+                        for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
+                    }
+                }
+            } else {
+            // Last-CTA reduction (non-cooperative): each thread gathers kU float4 outputs at once
+            // (kU x splits independent L2 loads in flight) before any store.
+            constexpr int kU = 8;
+            const int nf = (row_hi - row_lo) * (kDuBN / 4);
+            for (int f0 = t; f0 < nf; f0 += 128 * kU) {
+                float4 sum[kU];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) sum[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int sp = 0; sp < args.splits; ++sp) {
+                    float4 v[kU];
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        const int f = f0 + 128 * u;
+                        const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
+                        v[u] = f < nf ? __ldcg(reinterpret_cast<const float4*>(pbase + ((long long)sp * 256 + r) * kDuBN + c))
+                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int u = 0; u < kU; ++u) {
+                        sum[u].x += v[u].x; sum[u].y += v[u].y; sum[u].z += v[u].z; sum[u].w += v[u].w;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    const int f = f0 + 128 * u;
+                    if (f >= nf) break;
+                    const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
+                    const int m = m0 + r, n = n0 + c;
+                    if (m >= P.M || n >= P.N) continue;
+                    const float o[4] = {sum[u].x * P.alpha, sum[u].y * P.alpha, sum[u].z * P.alpha, sum[u].w * P.alpha};
+                    const long long mo = (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
+                    if (vec && n + 4 <= P.N) {
+                        *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
+                    } else {
+                        for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
+                    }
                 }
             }
+            }
+            if (args.dbg && t == 0) g_du_wait[blockIdx.x][2] = (unsigned long long)(clock64() - e_t);
             if (x.colsum) {
                 for (int c = col_lo + t; c < col_hi; c += 128) {
                     const int n = n0 + c;

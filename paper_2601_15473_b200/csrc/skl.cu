@@ -938,6 +938,12 @@ extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
         return -1;
     return n;
 }
+extern "C" int skl_debug_du_wait(unsigned long long* out, int n) {
+    if (n > 296 * 4) n = 296 * 4;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_wait, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
 extern "C" int skl_debug_b2b_eprof(unsigned long long* out, int n) {
     const int total = 296 * 8;
     if (n > total) n = total;

@@ -221,6 +221,20 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         : "r"(taddr));
 }
 
+// 1-D bulk copy global -> this CTA's smem, completion on `bar` (tx bytes).
+__device__ __forceinline__ void bulk_load_1d(void* smem, const void* gmem, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(smem)),
+        "l"(reinterpret_cast<uint64_t>(gmem)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Order this thread's prior generic-proxy view of global memory before its
+// subsequent async-proxy (TMA / bulk) accesses.
+__device__ __forceinline__ void fence_proxy_async_global() {
+    asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
 // ---------------------------------------------------------------- bulk stores
 // smem tile -> global through a tensor map (OOB rows/cols are clipped).
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void* smem, int32_t c0, int32_t c1) {
