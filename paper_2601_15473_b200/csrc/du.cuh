@@ -33,6 +33,8 @@ struct DuProblem {
     int M, N;             // output is M x N
     int m_tiles, n_tiles;  // 256 x 256 pair tiles
     int tile0;            // first global tile index of this problem
+    int splits;           // T split of this problem's tiles (per-problem: balances colsum vs plain tiles)
+    int unit0, slot0;     // first work unit / first partial slot of this problem
     int colsum;           // 1: also sum the B operand over K (db)
     float alpha;
     float* out;           // out[(m / mb) * mbs + (m % mb) * ms + n * ns]
@@ -41,10 +43,10 @@ struct DuProblem {
 };
 
 struct DuArgs {
-    int k_blocks, splits, num_tiles;
+    int k_blocks, num_units, num_tiles;
     DuProblem p[2];
-    float* part;     // [num_tiles][splits][256][256]
-    float* cpart;    // [p0.n_tiles][splits][256]
+    float* part;     // [slot0 + tile * splits + split][256][256] per problem
+    float* cpart;    // [p0.n_tiles][p0.splits][256]
     int* tickets;    // [num_tiles], zero on entry, left zero on exit
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
@@ -126,22 +128,27 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int units = args.num_tiles * args.splits;
+    const int units = args.num_units;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
     struct Unit {
-        int p, mt, nt, tile, split, kb0, kb1;
+        int p, mt, nt, tile, split, kb0, kb1, slot, nsplit;
         bool colsum;
     };
     auto decode = [&](int u) {
         Unit x;
-        x.split = u / args.num_tiles;
-        x.tile = u % args.num_tiles;
-        x.p = x.tile >= args.p[1].tile0 && args.p[1].m_tiles > 0 ? 1 : 0;
-        const int lt = x.tile - args.p[x.p].tile0;
-        x.mt = lt % args.p[x.p].m_tiles;
-        x.nt = lt / args.p[x.p].m_tiles;
-        x.kb0 = (int)(((long long)x.split * args.k_blocks) / args.splits);
-        x.kb1 = (int)(((long long)(x.split + 1) * args.k_blocks) / args.splits);
+        x.p = u >= args.p[1].unit0 && args.p[1].m_tiles > 0 ? 1 : 0;
+        const DuProblem& P = args.p[x.p];
+        const int ptiles = P.m_tiles * P.n_tiles;
+        const int lu = u - P.unit0;
+        x.split = lu / ptiles;  // split-major within the problem: concurrent units share a token window
+        const int lt = lu % ptiles;
+        x.tile = P.tile0 + lt;
+        x.slot = P.slot0 + lt * P.splits;
+        x.nsplit = P.splits;
+        x.mt = lt % P.m_tiles;
+        x.nt = lt / P.m_tiles;
+        x.kb0 = (int)(((long long)x.split * args.k_blocks) / P.splits);
+        x.kb1 = (int)(((long long)(x.split + 1) * args.k_blocks) / P.splits);
         x.colsum = args.p[x.p].colsum && x.mt == 0;
         return x;
     };
@@ -319,7 +326,7 @@ __global__ void __launch_bounds__(256, 1)
                     float s = 0.f;
 #pragma unroll
                     for (int g = 0; g < kGroups; ++g) s += csum_s[g * 128 + t];
-                    __stcg(args.cpart + ((long long)x.nt * args.splits + x.split) * kDuBN + rank * 128 + t, s);
+                    __stcg(args.cpart + ((long long)x.nt * x.nsplit + x.split) * kDuBN + rank * 128 + t, s);
                 }
                 named_bar_sync(2, 128);
             } else {
@@ -334,7 +341,7 @@ __global__ void __launch_bounds__(256, 1)
             tc_fence_after();
             lap(e_acc);
             {
-                float* prow = args.part + (((long long)x.tile * args.splits + x.split) * 256 + rank * 128 + t) * kDuBN;
+                float* prow = args.part + (((long long)x.slot + x.split) * 256 + rank * 128 + t) * kDuBN;
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
 #pragma unroll 1
                 for (int c = 0; c < kDuBN; c += 32) {
@@ -360,7 +367,7 @@ __global__ void __launch_bounds__(256, 1)
             __threadfence();
             named_bar_sync(2, 128);
             int* tk = args.tickets + x.tile;
-            const int parts = 2 * args.splits;  // CTAs contributing to this tile
+            const int parts = 2 * x.nsplit;  // CTAs contributing to this tile
             int row_lo, row_hi, col_lo, col_hi;
             if (args.coop) {
                 if (t == 0) {
@@ -390,7 +397,7 @@ __global__ void __launch_bounds__(256, 1)
             }
             __threadfence();
             if (args.dbg && t == 0) g_du_wait[blockIdx.x][1] = (unsigned long long)(clock64() - e_t);
-            const float* pbase = args.part + (long long)x.tile * args.splits * 256 * kDuBN;
+            const float* pbase = args.part + (long long)x.slot * 256 * kDuBN;
             const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
                              (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
             if (args.coop) {
@@ -403,8 +410,8 @@ __global__ void __launch_bounds__(256, 1)
                 const uint32_t slice = (uint32_t)rows * kDuBN * 4;
                 if (t == 0 && rows > 0) {
                     fence_proxy_async_global();  // partials were written by other CTAs' generic stores
-                    mbar_arrive_expect_tx(rbar, slice * (uint32_t)args.splits);
-                    for (int sp = 0; sp < args.splits; ++sp)
+                    mbar_arrive_expect_tx(rbar, slice * (uint32_t)x.nsplit);
+                    for (int sp = 0; sp < x.nsplit; ++sp)
                         bulk_load_1d(smem + (size_t)sp * slice, pbase + ((long long)sp * 256 + row_lo) * kDuBN, slice,
                                      rbar);
                 }
@@ -415,7 +422,7 @@ __global__ void __launch_bounds__(256, 1)
                     const int r = row_lo + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
                     const int m = m0 + r, n = n0 + c;
                     float4 sum = s4[f];
-                    for (int sp = 1; sp < args.splits; ++sp) {
+                    for (int sp = 1; sp < x.nsplit; ++sp) {
                         const float4 v = s4[(size_t)sp * (slice / 16) + f];
                         sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
                     }
@@ -437,7 +444,7 @@ __global__ void __launch_bounds__(256, 1)
                 float4 sum[kU];
 #pragma unroll
                 for (int u = 0; u < kU; ++u) sum[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (int sp = 0; sp < args.splits; ++sp) {
+                for (int sp = 0; sp < x.nsplit; ++sp) {
                     float4 v[kU];
 #pragma unroll
                     for (int u = 0; u < kU; ++u) {
@@ -474,8 +481,8 @@ __global__ void __launch_bounds__(256, 1)
                     const int n = n0 + c;
                     if (n >= P.N) continue;
                     float sum = 0.f;
-                    for (int sp = 0; sp < args.splits; ++sp)
-                        sum += __ldcg(args.cpart + ((long long)x.nt * args.splits + sp) * kDuBN + c);
+                    for (int sp = 0; sp < x.nsplit; ++sp)
+                        sum += __ldcg(args.cpart + ((long long)x.nt * x.nsplit + sp) * kDuBN + c);
                     P.db[n] = sum;
                 }
             }

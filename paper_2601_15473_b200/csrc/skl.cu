@@ -379,7 +379,8 @@ int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
 // falls out of L2) and multi-wave splits with last-CTA reduction (+3x at c2:
 // serial reductions).
 struct DuShape {
-    int m0, n0t, m1, n1t, tiles, splits, kb;
+    int m0, n0t, m1, n1t, t0, t1, s0, s1, kb, units;  // t*/s*: tiles / T splits of dU1 (0) and dU2 (1)
+    int tiles() const { return t0 + t1; }
 };
 DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) {
     DuShape s;
@@ -387,12 +388,33 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     s.n0t = (int)((d.d_out + 255) / 256);
     s.m1 = (int)((d.Lk + 255) / 256);
     s.n1t = (int)((d.d_in + 255) / 256);
-    s.tiles = ((which & 1) ? s.m0 * s.n0t : 0) + ((which & 2) ? s.m1 * s.n1t : 0);
+    s.t0 = (which & 1) ? s.m0 * s.n0t : 0;
+    s.t1 = (which & 2) ? s.m1 * s.n1t : 0;
     const int bkt = kind == 0 ? 64 : 32;  // tokens per k-block
     s.kb = (int)std::max<int64_t>(1, (T + bkt - 1) / bkt);
-    static const int force = getenv("SKL_DU_SPLITS") ? atoi(getenv("SKL_DU_SPLITS")) : 0;  // experiments
-    s.splits = force > 0 ? std::min(force, s.kb)
-                         : std::max(1, std::min((sms / 2) / std::max(1, s.tiles), std::max(1, s.kb / 2)));
+    const int pairs = std::max(1, sms / 2);
+    const int smax = std::max(1, s.kb / 2);  // keep >= 2 k-blocks per unit
+    // Per-problem splits, one wave: minimise the longest unit (dU2 units weighted
+    // by kW1 relative to dU1), then the number of partials.  At c2 the main loop
+    // is HBM-bound already (285 MB at ~6.5 TB/s), so 60 pairs are as fast as 72;
+    // small layers (768x768, L=1) gain 30 % from filling all pairs.
+    static const double kW1 = getenv("SKL_DU_W1") ? atof(getenv("SKL_DU_W1")) : 1.0;
+    double best = 1e30;
+    s.s0 = s.s1 = 1;
+    for (int a = (s.t0 ? 1 : 0); a <= (s.t0 ? smax : 0); ++a)
+        for (int b = (s.t1 ? 1 : 0); b <= (s.t1 ? smax : 0); ++b) {
+            if (s.t0 * a + s.t1 * b > pairs && (a > 1 || b > 1)) continue;
+            const double len = std::max(a ? std::ceil((double)s.kb / a) : 0.0,
+                                        b ? std::ceil((double)s.kb / b) * kW1 : 0.0);
+            const double cost = len + 1e-3 * (s.t0 * a + s.t1 * b);  // tie-break: fewer partials
+            if (cost < best) { best = cost; s.s0 = std::max(a, 1); s.s1 = std::max(b, 1); }
+        }
+    if (const char* e = getenv("SKL_DU_SPLITS")) {  // experiments: "S" or "S0,S1"
+        int a = 0, b = 0;
+        const int n = sscanf(e, "%d,%d", &a, &b);
+        if (n >= 1 && a > 0) s.s0 = std::min(a, s.kb), s.s1 = std::min(n == 2 && b > 0 ? b : a, s.kb);
+    }
+    s.units = s.t0 * s.s0 + s.t1 * s.s1;
     return s;
 }
 
@@ -420,9 +442,9 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
         size_t part = 0, cpart = 0, tickets = 0;
         for (int which = 1; which <= 3; ++which) {
             const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1, which);
-            part = std::max(part, (size_t)u.tiles * u.splits * 256 * 256 * 4);
-            cpart = std::max(cpart, (size_t)u.n0t * u.splits * 256 * 4);
-            tickets = std::max(tickets, (size_t)u.tiles * 4);
+            part = std::max(part, (size_t)u.units * 256 * 256 * 4);
+            cpart = std::max(cpart, (size_t)u.n0t * u.s0 * 256 * 4);
+            tickets = std::max(tickets, (size_t)u.tiles() * 4);
         }
         p.du_part = take(part);
         p.du_cpart = take(cpart);
@@ -450,13 +472,14 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     const DuShape u = du_shape(d, T, sms, kind, which);
     DuArgs a = {};
     a.k_blocks = u.kb;
-    a.splits = u.splits;
-    a.num_tiles = u.tiles;
-    const DuProblem pu1{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, grad_bias ? 1 : 0, inv, grad_U1s,
+    a.num_units = u.units;
+    a.num_tiles = u.tiles();
+    const int u1_units = (which & 1) ? u.t0 * u.s0 : 0;
+    const DuProblem pu1{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, u.s0, 0, 0, grad_bias ? 1 : 0, inv, grad_U1s,
                         (long long)1 << 40, 0, (long long)d.d_out, 1, grad_bias};
-    const DuProblem pu2{(int)d.Lk, (int)d.d_in, u.m1, u.n1t, (which & 1) ? u.m0 * u.n0t : 0, 0, inv, grad_U2s,
+    const DuProblem pu2{(int)d.Lk, (int)d.d_in, u.m1, u.n1t, u.t0, u.s1, u1_units, u1_units, 0, inv, grad_U2s,
                         (long long)d.k, (long long)(d.d_in * d.k), 1, (long long)d.k, nullptr};
-    const DuProblem none{0, 0, 0, 0, 1 << 30, 0, 0.f, nullptr, 1, 0, 0, 0, nullptr};
+    const DuProblem none{0, 0, 0, 0, 1 << 30, 1, 1 << 30, 0, 0, 0.f, nullptr, 1, 0, 0, 0, nullptr};
     a.p[0] = (which & 1) ? pu1 : pu2;
     a.p[1] = (which & 1) && (which & 2) ? pu2 : none;
     const bool colsum = (which & 1) && grad_bias;
@@ -481,14 +504,14 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     tb0 = (which & 1) ? tu1b : tu2b;
     ta1 = tu2a;
     tb1 = tu2b;
-    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles * 4, st));
+    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles() * 4, st));
     auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
     static bool attr_set[2] = {false, false};
     if (!attr_set[kind]) {
         SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
         attr_set[kind] = true;
     }
-    const int units = u.tiles * u.splits;  // CTA-pair work units
+    const int units = u.units;  // CTA-pair work units
     a.relay = colsum ? 1 : 0;
     static const int du_dbg = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;  // perf analysis
     a.dbg = du_dbg;
