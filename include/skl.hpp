@@ -116,6 +116,21 @@ class SkLinear {
         return s;
     }
 
+    // sk_linear_from_dense (nn_layers.cpp:149-160) on the device: W [d_out, d_in]
+    // and bias [d_out] (nullable) are DEVICE arrays in the variant's element type.
+    static SkLinear from_dense(const void* W, const void* bias, int64_t d_in, int64_t d_out, int64_t l, int64_t k,
+                               uint64_t seed, skl_dist dist = SKL_DIST_GAUSSIAN, skl_dtype dtype = SKL_BF16,
+                               cudaStream_t st = nullptr) {
+        SkLinear s(d_in, d_out, l, k, dtype);
+        size_t n = 0;
+        check(skl_from_dense_workspace_size(&s.shape_, &n));
+        DeviceBuffer ws(n);
+        check(skl_from_dense(&s.shape_, dist, seed, W, bias, s.S1s_.get(), s.S2s_.get(), s.U1s_.get(),
+                             s.U2s_.get(), s.bias_.get(), ws.get(), n, st));
+        check_cuda(cudaStreamSynchronize(st), "sync");  // ws is released on return
+        return s;
+    }
+
     // Explicit parameters (host arrays in the variant's element type, ABI
     // layouts) -- the analogue of SketchOp::with_realized (sketch.hpp:36-38).
     static SkLinear with_params(int64_t d_in, int64_t d_out, int64_t l, int64_t k, skl_dtype dtype,
@@ -160,11 +175,13 @@ class SkLinear {
 
     // SkLinear::forward (nn_layers.cpp:61-76), device pointers:
     // x [T, d_in] -> y [T, d_out]; saved (nullable) [L*k][round8(T)] keeps x·S1_i.
-    void forward(const void* x, int64_t T, void* y, void* saved = nullptr, cudaStream_t st = nullptr) const {
+    // fuse = SKL_FUSE_RELU_OUT applies a following ReLU in the epilogue.
+    void forward(const void* x, int64_t T, void* y, void* saved = nullptr, cudaStream_t st = nullptr,
+                 unsigned fuse = 0) const {
         if (T < 0) throw shape_error("SkLinear::forward: negative token count");
         void* ws = workspace(T, st);
-        check(sketched_linear_forward(&shape_, T, x, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(), bias_.get(), y,
-                                      saved, ws, ws_.bytes(), st));
+        check(sketched_linear_forward_ex(&shape_, T, fuse, x, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(),
+                                         bias_.get(), y, saved, ws, ws_.bytes(), st));
     }
 
     // SkLinear::backward (nn_layers.cpp:78-101): gradients allocated here.
@@ -181,12 +198,15 @@ class SkLinear {
 
     // Allocation-free backward into caller buffers (e.g. one contiguous
     // dU1s | dU2s | db bucket for the NCCL all-reduce).  grad_x / grad_b nullable.
+    // phases: SKL_BWD_ALL, or SKL_BWD_DU1_DB then SKL_BWD_DX_DU2 (data-parallel overlap);
+    // fuse = SKL_FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward).
     void backward_into(const void* x, const void* grad_out, int64_t T, const void* saved, void* grad_x, float* dU1s,
-                       float* dU2s, float* db, cudaStream_t st = nullptr) const {
+                       float* dU2s, float* db, cudaStream_t st = nullptr, unsigned phases = SKL_BWD_ALL,
+                       unsigned fuse = 0) const {
         if (T < 0) throw shape_error("SkLinear::backward: negative token count");
         void* ws = workspace(T, st);
-        check(sketched_linear_backward(&shape_, T, grad_out, x, saved, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(),
-                                       grad_x, dU1s, dU2s, db, ws, ws_.bytes(), st));
+        check(sketched_linear_backward_ex(&shape_, T, phases, fuse, grad_out, x, saved, S1s_.get(), S2s_.get(),
+                                          U1s_.get(), U2s_.get(), grad_x, dU1s, dU2s, db, ws, ws_.bytes(), st));
     }
 
     // Host-buffer convenience (the reference's value-semantics call):

@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <dlfcn.h>
+
 #include "skl.hpp"
 
 extern "C" {
@@ -396,6 +398,94 @@ void test_params() {
     report("params / exceeds_dense closed forms", ok);
 }
 
+void test_from_dense() {
+    // sk_linear_from_dense (nn_layers.cpp:149-160): u1_i = s1_i·W, u2_i = W·s2_iᵀ
+    const int64_t d_in = 96, d_out = 160, l = 2, k = 16;
+    const skl_dtype t = SKL_F32_TF32;
+    vec W(d_out * d_in), b(d_out);
+    orc_gaussian_matrix(d_out, d_in, 21, W.data());
+    orc_gaussian_matrix(1, d_out, 22, b.data());
+    for (double& v : W) v *= 0.05;
+    const auto Wh = to_dev(W, t), bh = to_dev(b, t);
+    skl::DeviceBuffer Wd(Wh.size()), bd(bh.size());
+    Wd.upload(Wh.data(), Wh.size());
+    bd.upload(bh.data(), bh.size());
+    skl::SkLinear L = skl::SkLinear::from_dense(Wd.get(), bd.get(), d_in, d_out, l, k, 33, SKL_DIST_GAUSSIAN, t);
+    const RefParams P = ref_from_layer(L);  // device sketches (bit-exact) and device U
+    const vec Wr = from_dev(Wh.data(), W.size(), t);
+    vec u1(l * k * d_in, 0.0), u2(l * d_out * k, 0.0), u1d, u2d;
+    for (int64_t i = 0; i < l; ++i)
+        for (int64_t j = 0; j < k; ++j) {
+            for (int64_t c = 0; c < d_in; ++c) {
+                double acc = 0;
+                for (int64_t o = 0; o < d_out; ++o) acc += P.s1[(i * k + j) * d_out + o] * Wr[o * d_in + c];
+                u1[(i * k + j) * d_in + c] = acc;
+            }
+            for (int64_t o = 0; o < d_out; ++o) {
+                double acc = 0;
+                for (int64_t c = 0; c < d_in; ++c) acc += Wr[o * d_in + c] * P.s2[(i * k + j) * d_in + c];
+                u2[(i * d_out + o) * k + j] = acc;
+            }
+        }
+    std::string d1, d2;
+    const bool ok1 = gate(P.u1, u1, t, d1), ok2 = gate(P.u2, u2, t, d2);
+    report("from_dense u1 = s1·W (tcgen05)", ok1, d1);
+    report("from_dense u2 = W·s2ᵀ (tcgen05)", ok2, d2);
+    const vec bias = download(L.bias(), d_out, t), br = from_dev(bh.data(), d_out, t);
+    report("from_dense bias copied", bias == br);
+}
+
+void test_fused_relu_forward() {
+    // SKL_FUSE_RELU_OUT == max(0, plain forward), bitwise
+    const int64_t d_in = 128, d_out = 192, l = 2, k = 64, T = 200;
+    skl::SkLinear L = skl::SkLinear::fresh(d_in, d_out, l, k, 5, SKL_DIST_GAUSSIAN, SKL_BF16);
+    vec xv(T * d_in), bv(d_out);
+    orc_gaussian_matrix(T, d_in, 6, xv.data());
+    orc_gaussian_matrix(1, d_out, 7, bv.data());
+    const auto xh = to_dev(xv, SKL_BF16), bh = to_dev(bv, SKL_BF16);
+    skl::check_cuda(cudaMemcpy(L.bias(), bh.data(), bh.size(), cudaMemcpyHostToDevice), "bias");
+    skl::DeviceBuffer X(xh.size()), Y(T * d_out * 2), R(T * d_out * 2);
+    X.upload(xh.data(), xh.size());
+    L.forward(X.get(), T, Y.get());
+    L.forward(X.get(), T, R.get(), nullptr, nullptr, SKL_FUSE_RELU_OUT);
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+    const vec y = download(Y.get(), T * d_out, SKL_BF16), r = download(R.get(), T * d_out, SKL_BF16);
+    bool ok = true;
+    for (size_t i = 0; i < y.size(); ++i) ok &= r[i] == (y[i] > 0 ? y[i] : 0.0);
+    report("fused ReLU forward == max(0, forward) bitwise", ok);
+}
+
+void test_nccl_allreduce_world1() {
+    // skl_allreduce_grads over a real ncclComm_t (one rank): the C-ABI entry a
+    // C++ data-parallel host calls on the gradient bucket.
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        std::printf("SKIP nccl (libnccl.so.2 not loadable)\n");
+        return;
+    }
+    using init_all_fn = int (*)(void**, int, const int*);
+    using destroy_fn = int (*)(void*);
+    auto init_all = reinterpret_cast<init_all_fn>(dlsym(h, "ncclCommInitAll"));
+    auto destroy = reinterpret_cast<destroy_fn>(dlsym(h, "ncclCommDestroy"));
+    void* comm = nullptr;
+    const int dev0 = 0;
+    bool ok = init_all && destroy && init_all(&comm, 1, &dev0) == 0;
+    const size_t n = 1000;
+    std::vector<float> hv(n);
+    for (size_t i = 0; i < n; ++i) hv[i] = 0.5f * (float)i - 7.f;
+    skl::DeviceBuffer B(n * 4);
+    B.upload(hv.data(), n * 4);
+    if (ok) ok = skl_allreduce_grads(comm, B.as<float>(), n, nullptr) == SKL_OK;
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+    std::vector<float> back(n);
+    B.download(back.data(), n * 4);
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+    ok = ok && back == hv;  // sum over one rank
+    ok = ok && skl_allreduce_grads(nullptr, B.as<float>(), n, nullptr) == SKL_ERR_PARAM;
+    if (comm) destroy(comm);
+    report("skl_allreduce_grads over an NCCL communicator (world 1)", ok);
+}
+
 }  // namespace
 
 int main() {
@@ -416,6 +506,9 @@ int main() {
         test_batch_additivity();
         test_errors();
         test_params();
+        test_from_dense();
+        test_fused_relu_forward();
+        test_nccl_allreduce_world1();
     } catch (const std::exception& e) {
         std::printf("FAIL uncaught exception: %s\n", e.what());
         ++g_fail;
