@@ -32,6 +32,10 @@
 
 #include "sm100.cuh"
 
+#ifndef SKL_FWD_SINGLE_PASS
+#define SKL_FWD_SINGLE_PASS 0  // measured: 99 -> 116 us at c2 (3 stages starve GEMM2)
+#endif
+
 namespace skl {
 
 struct B2BArgs {
@@ -124,13 +128,13 @@ struct B2BCfg {
     // The backward's GEMM1 (K = d_out, 80% of its MMAs) runs single-pass: one
     // A1 tile feeds both 256-wide chunks, so G is read once instead of twice;
     // its stages therefore hold A1 + B1 for all of R (48 KB).
-    static constexpr bool kSinglePassG1 = kMode == 2 && kCG == 2;
+    static constexpr bool kSinglePassG1 = (kMode == 2 || (kMode == 1 && SKL_FWD_SINGLE_PASS)) && kCG == 2;
     static constexpr int kStageBytes = (kCG == 1 || kSinglePassG1) ? 48 * 1024 : 32 * 1024;
     // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
     static constexpr int kBiasTabBytes = kMode == 1 ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages = kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0) - kKind;
+    static constexpr int kStages = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0) - kKind;
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
