@@ -24,6 +24,7 @@
 
 #include "../../include/skl.h"
 #include "b2b.cuh"
+#include "b2b_tf32.cuh"
 #include "du.cuh"
 #include "gemm.cuh"
 #include "prof.h"
@@ -249,6 +250,40 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     return SKL_OK;
 }
 
+// TF32 with 256 < R_pad <= 512: H split between TMEM and SMEM (b2b_tf32.cuh).
+template <bool kSP>
+skl_status run_b2b_tf32_wide(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
+    using C = dev::B2BT32Cfg<kSP>;
+    auto kern = dev::b2b_tf32_kernel<kSP>;
+    CUtensorMap ta, tb1, tb2, ty;
+    SKL_TRY(make_tmap(&ta, src.a1, 4, a.K1, a.T, a.K1, C::kBK, 128));
+    SKL_TRY(make_tmap(&tb1, src.b1, 4, a.K1, a.R_pad, a.K1, C::kBK, a.b1rows));
+    SKL_TRY(make_tmap(&tb2, src.b2, 4, a.R_pad, a.N2, a.R_pad, C::kBK, C::kB2Rows));
+    SKL_TRY(make_tmap(&ty, a.out, 4, a.N2, a.T, a.ldo, C::kBK, 128));
+    const int tiles = (a.T + 255) / 256;
+    const int grid = std::max(1, std::min(sms / 2, tiles)) * 2;
+    static bool attr_set = false;
+    if (!attr_set) {
+        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(384);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    ProfScope ps_(name, st);
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, ty, a));
+    return SKL_OK;
+}
+
 int g_b2b_cg = 2;       // CTA-group width of the fused kernel (SKL_B2B_CG=1 forces single-CTA MMAs)
 int g_b2b_direct = 1;   // read the ABI stacks directly when k % 64 == 0 (SKL_B2B_PACKED=1 disables)
 
@@ -269,6 +304,12 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         };
         while (r > 8 && !ok(r)) r /= 2;
         a.b1rows = r;
+    }
+    if (kind == 1 && b2b_tf32_wide_supported(a.R_pad)) {
+        if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "the wide-rank TF32 kernel needs CTA pairs");
+        // single-pass GEMM1 when its A operand is long (the backward's G, K1 = d_out)
+        if (a.K1 >= 2048) return run_b2b_tf32_wide<true>(name, src, a, sms, st);
+        return run_b2b_tf32_wide<false>(name, src, a, sms, st);
     }
     if (a.relu || a.mask) {  // fused ReLU / ReLU-mask epilogue (CTA pairs only)
         if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "fused ReLU needs the CTA-pair kernel (SKL_B2B_CG=2)");
@@ -357,7 +398,10 @@ bool use_fused(const SklDims& d, skl_dtype t) {
         const char* e = getenv("SKL_FORCE_UNFUSED");
         return e && atoi(e) != 0;
     }();
-    return !force_unfused && b2b_supported(d.R_pad, t == SKL_BF16 ? 0 : 1);
+    static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
+    if (force_unfused) return false;
+    if (t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad)) return g_b2b_cg == 2;
+    return b2b_supported(d.R_pad, t == SKL_BF16 ? 0 : 1);
 }
 
 struct Plan {
