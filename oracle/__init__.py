@@ -227,6 +227,37 @@ def sk_linear_from_dense(o: "Oracle", W: np.ndarray, l: int, k: int, seed: int, 
     return Params(d_in, d_out, l, k, p.s1, u1, p.s2, u2)
 
 
+def skconv_forward(ref: "Oracle", geo, p: Params, bias, x):
+    """The REFERENCE's SkConv2d::forward (nn_layers.cpp:226-244, via oracle/_ref)
+    on explicit parameters.  geo = (c_in, c_out, kh, kw, stride, padding); x NCHW."""
+    B, C, H, W = x.shape
+    c_in, c_out, kh, kw, st, pad = geo
+    oh, ow = (H + 2 * pad - kh) // st + 1, (W + 2 * pad - kw) // st + 1
+    y = np.empty((B, c_out, oh, ow))
+    g = np.array(geo, dtype=np.uint64)
+    f = ref.lib.ref_skconv_forward
+    f.argtypes = [_up, _u64, _u64] + [_dp] * 5 + [_u64] * 3 + [_dp, _dp]
+    ref._check(f(g.ctypes.data_as(_up), p.l, p.k, _p(p.s1), _p(p.u1), _p(p.s2), _p(p.u2), _p(np.ascontiguousarray(bias)),
+                 B, H, W, _p(np.ascontiguousarray(x)), _p(y)), "skconv_forward")
+    return y
+
+
+def skconv_backward(ref: "Oracle", geo, p: Params, x, g):
+    """The REFERENCE's SkConv2d::backward (nn_layers.cpp:280-314) -> (grad_x, gu1, gu2, gb)."""
+    B, C, H, W = x.shape
+    gx = np.empty_like(x)
+    gu1 = np.empty((p.l, p.k, p.d_in))
+    gu2 = np.empty((p.l, p.d_out, p.k))
+    gb = np.empty(p.d_out)
+    geo_a = np.array(geo, dtype=np.uint64)
+    f = ref.lib.ref_skconv_backward
+    f.argtypes = [_up, _u64, _u64] + [_dp] * 4 + [_u64] * 3 + [_dp] * 6
+    ref._check(f(geo_a.ctypes.data_as(_up), p.l, p.k, _p(p.s1), _p(p.u1), _p(p.s2), _p(p.u2), B, H, W,
+                 _p(np.ascontiguousarray(x)), _p(np.ascontiguousarray(g)), _p(gx), _p(gu1), _p(gu2), _p(gb)),
+               "skconv_backward")
+    return gx, gu1, gu2, gb
+
+
 def to_abi(p: Params):
     """-> dict(S1s [L,d_in,k], U1s [L,k,d_out], U2s [L,d_in,k], S2s [L,k,d_out])."""
     return dict(

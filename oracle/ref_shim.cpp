@@ -206,3 +206,59 @@ int ref_max_threads(void) {
 }
 
 }  // extern "C"
+
+// ---- SkConv2d (nn_layers.cpp:226-314) on explicit parameters -------------------
+namespace {
+rnla::nn::SkConv2d make_conv(const std::uint64_t* geo, std::uint64_t l, std::uint64_t k, const double* s1,
+                             const double* u1, const double* s2, const double* u2, const double* bias) {
+    rnla::nn::SkConv2d c;
+    c.shape.c_in = geo[0];
+    c.shape.c_out = geo[1];
+    c.shape.kernel_h = geo[2];
+    c.shape.kernel_w = geo[3];
+    c.shape.stride = geo[4];
+    c.shape.padding = geo[5];
+    c.inner = make_layer(c.shape.lowered_d_in(), c.shape.c_out, l, k, s1, u1, s2, u2, bias);
+    return c;
+}
+rnla::nn::ImageBatch make_images(std::uint64_t B, std::uint64_t C, std::uint64_t H, std::uint64_t W, const double* p) {
+    rnla::nn::ImageBatch x;
+    x.batch = B;
+    x.channels = C;
+    x.height = H;
+    x.width = W;
+    x.data.assign(p, p + B * C * H * W);
+    return x;
+}
+}  // namespace
+
+extern "C" {
+// geo = {c_in, c_out, kernel_h, kernel_w, stride, padding}; x NCHW [B, c_in, H, W]; y [B, c_out, oh, ow]
+int ref_skconv_forward(const std::uint64_t* geo, std::uint64_t l, std::uint64_t k, const double* s1,
+                       const double* u1, const double* s2, const double* u2, const double* bias, std::uint64_t B,
+                       std::uint64_t H, std::uint64_t W, const double* x, double* y) {
+    return guard([&] {
+        const auto c = make_conv(geo, l, k, s1, u1, s2, u2, bias);
+        const auto out = c.forward(make_images(B, geo[0], H, W, x));
+        std::memcpy(y, out.data.data(), out.data.size() * sizeof(double));
+    });
+}
+
+int ref_skconv_backward(const std::uint64_t* geo, std::uint64_t l, std::uint64_t k, const double* s1,
+                        const double* u1, const double* s2, const double* u2, std::uint64_t B, std::uint64_t H,
+                        std::uint64_t W, const double* x, const double* g, double* gx, double* gu1, double* gu2,
+                        double* gb) {
+    return guard([&] {
+        const auto c = make_conv(geo, l, k, s1, u1, s2, u2, nullptr);
+        const std::uint64_t oh = c.shape.out_h(H), ow = c.shape.out_w(W);
+        const auto gr = c.backward(make_images(B, geo[0], H, W, x), make_images(B, geo[1], oh, ow, g));
+        std::memcpy(gx, gr.grad_x.data.data(), gr.grad_x.data.size() * sizeof(double));
+        const std::uint64_t d_in = c.shape.lowered_d_in(), d_out = c.shape.c_out;
+        for (std::uint64_t i = 0; i < l; ++i) {
+            std::memcpy(gu1 + i * k * d_in, gr.grad_u1[i].data(), k * d_in * sizeof(double));
+            std::memcpy(gu2 + i * d_out * k, gr.grad_u2[i].data(), d_out * k * sizeof(double));
+        }
+        std::memcpy(gb, gr.grad_b.data(), d_out * sizeof(double));
+    });
+}
+}  // extern "C"

@@ -37,6 +37,7 @@ ABI_SYMBOLS = (
     "sketched_linear_forward", "sketched_linear_backward", "skl_allreduce_grads", "skl_launch_count",
     "skl_profile_enable", "skl_profile_collect", "sketched_linear_backward_phase", "skl_set_reserved_sms",
     "sketched_linear_forward_ex", "sketched_linear_backward_ex", "skl_from_dense", "skl_from_dense_workspace_size",
+    "skl_conv_workspace_size", "sketched_conv2d_forward", "sketched_conv2d_backward",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
 FUSE_RELU_OUT, FUSE_RELU_IN = 1, 2

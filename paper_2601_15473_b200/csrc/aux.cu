@@ -311,4 +311,128 @@ cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t col
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- convolution lowering
+// SkConv2d (nn_layers.cpp:176-314) = im2col + SkLinear + reshape.  Token t =
+// b*oh*ow + oy*ow + ox; lowered feature f = ch*kh*kw + kr*kw + kc (im2col's
+// row order, nn_layers.cpp:176-200).  All kernels are gathers (each output
+// element written once, fixed summation order): deterministic, no atomics.
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_tokens_kernel(const T* __restrict__ img, T* __restrict__ cols,
+                                                            ConvGeom g) {
+    const int64_t d = (int64_t)g.c * g.kh * g.kw;
+    const int64_t n = (int64_t)g.B * g.oh * g.ow * d;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / d, f = i % d;
+        const int64_t b = t / ((int64_t)g.oh * g.ow), p = t % ((int64_t)g.oh * g.ow);
+        const int oy = (int)(p / g.ow), ox = (int)(p % g.ow);
+        const int ch = (int)(f / (g.kh * g.kw)), kr = (int)((f / g.kw) % g.kh), kc = (int)(f % g.kw);
+        const int iy = oy * g.stride + kr - g.pad, ix = ox * g.stride + kc - g.pad;
+        cols[i] = (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w)
+                      ? img[(((int64_t)b * g.c + ch) * g.h + iy) * g.w + ix]
+                      : T(0.f);
+    }
+}
+
+// col2im (nn_layers.cpp:202-224) as a gather: input pixel (b, ch, iy, ix)
+// sums the patch entries that read it, in (kr, kc) order.
+template <typename T>
+__global__ void __launch_bounds__(256) col2im_gather_kernel(const T* __restrict__ cols, T* __restrict__ img,
+                                                            ConvGeom g) {
+    const int64_t d = (int64_t)g.c * g.kh * g.kw;
+    const int64_t n = (int64_t)g.B * g.c * g.h * g.w;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int ix = (int)(i % g.w), iy = (int)((i / g.w) % g.h);
+        const int ch = (int)((i / ((int64_t)g.w * g.h)) % g.c);
+        const int64_t b = i / ((int64_t)g.w * g.h * g.c);
+        float acc = 0.f;
+        for (int kr = 0; kr < g.kh; ++kr) {
+            const int ty = iy + g.pad - kr;
+            if (ty < 0 || ty % g.stride) continue;
+            const int oy = ty / g.stride;
+            if (oy >= g.oh) continue;
+            for (int kc = 0; kc < g.kw; ++kc) {
+                const int tx = ix + g.pad - kc;
+                if (tx < 0 || tx % g.stride) continue;
+                const int ox = tx / g.stride;
+                if (ox >= g.ow) continue;
+                const int64_t t = (b * g.oh + oy) * g.ow + ox;
+                acc += (float)cols[t * d + ((int64_t)ch * g.kh + kr) * g.kw + kc];
+            }
+        }
+        img[i] = T(acc);
+    }
+}
+
+// [B*P, C] token rows <-> [B, C, P] planes (P = oh*ow): 32x32 smem tiles per image.
+template <typename T>
+__global__ void __launch_bounds__(256) tokens_planes_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t B,
+                                                            int64_t P, int64_t C, int to_planes) {
+    __shared__ float tile[32][33];
+    const int64_t tp = (P + 31) / 32, tc = (C + 31) / 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    for (int64_t blk = blockIdx.x; blk < B * tp * tc; blk += gridDim.x) {
+        const int64_t b = blk / (tp * tc), r = blk % (tp * tc);
+        const int64_t p0 = (r / tc) * 32, c0 = (r % tc) * 32;
+        __syncthreads();
+        if (to_planes) {  // in [b*P + p][c] -> out [b][c][p]
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t p = p0 + ty + 8 * i, c = c0 + tx;
+                if (p < P && c < C) tile[ty + 8 * i][tx] = (float)in[(b * P + p) * C + c];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t c = c0 + ty + 8 * i, p = p0 + tx;
+                if (p < P && c < C) out[(b * C + c) * P + p] = T(tile[tx][ty + 8 * i]);
+            }
+        } else {          // in [b][c][p] -> out [b*P + p][c]
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t c = c0 + ty + 8 * i, p = p0 + tx;
+                if (p < P && c < C) tile[tx][ty + 8 * i] = (float)in[(b * C + c) * P + p];
+            }
+            __syncthreads();
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int64_t p = p0 + ty + 8 * i, c = c0 + tx;
+                if (p < P && c < C) out[(b * P + p) * C + c] = T(tile[ty + 8 * i][tx]);
+            }
+        }
+    }
+}
+
+cudaError_t launch_im2col(const void* img, int elem, const ConvGeom& g, void* cols, cudaStream_t st) {
+    ProfScope ps_("im2col", st);
+    const uint64_t n = (uint64_t)g.B * g.oh * g.ow * g.c * g.kh * g.kw;
+    if (elem == ELEM_BF16)
+        im2col_tokens_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)img, (__nv_bfloat16*)cols, g);
+    else
+        im2col_tokens_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)img, (float*)cols, g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_col2im(const void* cols, int elem, const ConvGeom& g, void* img, cudaStream_t st) {
+    ProfScope ps_("col2im", st);
+    const uint64_t n = (uint64_t)g.B * g.c * g.h * g.w;
+    if (elem == ELEM_BF16)
+        col2im_gather_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)cols, (__nv_bfloat16*)img, g);
+    else
+        col2im_gather_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)cols, (float*)img, g);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tokens_planes(const void* in, int elem, int64_t B, int64_t P, int64_t C, void* out, int to_planes,
+                                 cudaStream_t st) {
+    ProfScope ps_(to_planes ? "to_planes" : "to_tokens", st);
+    const int64_t blocks = B * ((P + 31) / 32) * ((C + 31) / 32);
+    const int grid = (int)std::min<int64_t>(blocks, 148 * 8);
+    if (elem == ELEM_BF16)
+        tokens_planes_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, B, P, C,
+                                                                  to_planes);
+    else
+        tokens_planes_kernel<float><<<grid, 256, 0, st>>>((const float*)in, (float*)out, B, P, C, to_planes);
+    return cudaGetLastError();
+}
+
 }  // namespace skl

@@ -947,6 +947,111 @@ skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed
     return SKL_OK;
 }
 
+// ---------------------------------------------------------------- SkConv2d
+// SkConv2d::forward / backward (nn_layers.cpp:226-314): im2col lowering +
+// the SKLinear path (inner layer d_in = c_in*kh*kw, d_out = c_out) + NCHW
+// reshapes, all on the device.  T = B*oh*ow patches are the tokens.
+namespace skl {
+namespace {
+skl_status conv_geom(const skl_shape* s, const skl_conv_shape* cs, int64_t B, int64_t H, int64_t W, ConvGeom& g) {
+    if (!s || !cs) return fail(SKL_ERR_PARAM, "null shape");
+    if (cs->c_in < 1 || cs->c_out < 1 || cs->kernel_h < 1 || cs->kernel_w < 1 || cs->stride < 1 || cs->padding < 0)
+        return fail(SKL_ERR_PARAM, "conv: invalid ConvShape");
+    if (s->d_in != cs->c_in * cs->kernel_h * cs->kernel_w || s->d_out != cs->c_out)
+        return fail(SKL_ERR_SHAPE, "SKConv2d: inner dims disagree with conv shape");  // nn_model.cpp:500
+    if (B < 0 || H < 1 || W < 1) return fail(SKL_ERR_SHAPE, "conv: bad image size");
+    const int64_t ph = H + 2 * cs->padding, pw = W + 2 * cs->padding;
+    if (ph < cs->kernel_h) return fail(SKL_ERR_SHAPE, "conv: kernel taller than padded image");  // nn_layers.cpp:166
+    if (pw < cs->kernel_w) return fail(SKL_ERR_SHAPE, "conv: kernel wider than padded image");   // :172
+    g = ConvGeom{(int)B, (int)cs->c_in, (int)H, (int)W, (int)cs->kernel_h, (int)cs->kernel_w, (int)cs->stride,
+                 (int)cs->padding, (int)((ph - cs->kernel_h) / cs->stride + 1),
+                 (int)((pw - cs->kernel_w) / cs->stride + 1)};
+    return SKL_OK;
+}
+struct ConvPlan {
+    size_t cols, ytok, gtok, dcols, inner, total;
+};
+ConvPlan conv_plan(const skl_shape* s, const ConvGeom& g, bool bwd) {
+    const size_t e = s->dtype == SKL_BF16 ? 2 : 4;
+    const int64_t T = (int64_t)g.B * g.oh * g.ow;
+    ConvPlan p = {};
+    size_t off = 0;
+    auto take = [&](size_t b) { size_t o = off; off += align_up(b ? b : 1); return o; };
+    p.cols = take((size_t)T * s->d_in * e);    // im2col patches [T, d_in] (recomputed when not kept)
+    p.ytok = take(bwd ? 0 : (size_t)T * s->d_out * e);
+    p.gtok = take(bwd ? (size_t)T * s->d_out * e : 0);
+    p.dcols = take(bwd ? (size_t)T * s->d_in * e : 0);
+    size_t f = 0, b = 0;
+    skl_workspace_size(s, T, &f, &b);
+    p.inner = take(bwd ? b : f);
+    p.total = off;
+    return p;
+}
+}  // namespace
+}  // namespace skl
+
+skl_status skl_conv_workspace_size(const skl_shape* s, const skl_conv_shape* cs, int64_t B, int64_t H, int64_t W,
+                                   size_t* fwd_bytes, size_t* bwd_bytes) {
+    ConvGeom g;
+    SKL_TRY(conv_geom(s, cs, B, H, W, g));
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (fwd_bytes) *fwd_bytes = conv_plan(s, g, false).total;
+    if (bwd_bytes) *bwd_bytes = conv_plan(s, g, true).total;
+    return SKL_OK;
+}
+
+skl_status sketched_conv2d_forward(const skl_shape* s, const skl_conv_shape* cs, int64_t B, int64_t H, int64_t W,
+                                   unsigned fuse, const void* x, const void* S1s, const void* S2s, const void* U1s,
+                                   const void* U2s, const void* bias, void* y, void* cols_out, void* saved_proj,
+                                   void* workspace, size_t ws_bytes, void* stream) {
+    ConvGeom g;
+    SKL_TRY(conv_geom(s, cs, B, H, W, g));
+    if (!x || !y) return fail(SKL_ERR_PARAM, "null tensor argument");
+    const ConvPlan p = conv_plan(s, g, false);
+    if (!workspace || ws_bytes < p.total)
+        return fail(SKL_ERR_WORKSPACE, "conv forward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
+    const int64_t T = (int64_t)g.B * g.oh * g.ow;
+    if (T == 0) return SKL_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int elem = elem_of(s->dtype);
+    void* cols = cols_out ? cols_out : at<void>(workspace, p.cols);
+    void* ytok = at<void>(workspace, p.ytok);
+    SKL_CUDA(launch_im2col(x, elem, g, cols, st));
+    SKL_TRY(sketched_linear_forward_ex(s, T, fuse, cols, S1s, S2s, U1s, U2s, bias, ytok, saved_proj,
+                                       at<void>(workspace, p.inner), p.total - p.inner, stream));
+    SKL_CUDA(launch_tokens_planes(ytok, elem, g.B, (int64_t)g.oh * g.ow, s->d_out, y, 1, st));
+    return SKL_OK;
+}
+
+skl_status sketched_conv2d_backward(const skl_shape* s, const skl_conv_shape* cs, int64_t B, int64_t H, int64_t W,
+                                    const void* grad_y, const void* x, const void* cols_in, const void* saved_proj,
+                                    const void* S1s, const void* S2s, const void* U1s, const void* U2s, void* grad_x,
+                                    float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
+                                    size_t ws_bytes, void* stream) {
+    ConvGeom g;
+    SKL_TRY(conv_geom(s, cs, B, H, W, g));
+    if (!grad_y || (!x && !cols_in)) return fail(SKL_ERR_PARAM, "null tensor argument");
+    const ConvPlan p = conv_plan(s, g, true);
+    if (!workspace || ws_bytes < p.total)
+        return fail(SKL_ERR_WORKSPACE, "conv backward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
+    const int64_t T = (int64_t)g.B * g.oh * g.ow;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int elem = elem_of(s->dtype);
+    const void* cols = cols_in;
+    if (!cols) {
+        SKL_CUDA(launch_im2col(x, elem, g, at<void>(workspace, p.cols), st));
+        cols = at<void>(workspace, p.cols);
+    }
+    void* gtok = at<void>(workspace, p.gtok);
+    void* dcols = grad_x ? at<void>(workspace, p.dcols) : nullptr;
+    if (T > 0) SKL_CUDA(launch_tokens_planes(grad_y, elem, g.B, (int64_t)g.oh * g.ow, s->d_out, gtok, 0, st));
+    SKL_TRY(sketched_linear_backward(s, T, gtok, cols, saved_proj, S1s, S2s, U1s, U2s, dcols, grad_U1s, grad_U2s,
+                                     grad_bias, at<void>(workspace, p.inner), p.total - p.inner, stream));
+    if (grad_x) SKL_CUDA(launch_col2im(dcols, elem, g, grad_x, st));
+    return SKL_OK;
+}
+
 skl_status skl_set_reserved_sms(int n) {
     if (n < 0 || n > 64) return fail(SKL_ERR_PARAM, "reserved SMs must be in [0, 64], got %d", n);
     g_reserved_sms = n;

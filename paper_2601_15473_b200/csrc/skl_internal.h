@@ -26,5 +26,13 @@ cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int u
 cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void* U2s, const void* U1s,
                          const void* S2s, void* Acat, void* Bcat, void* AcatT, void* BcatT, const void* bias,
                          float* bias32, cudaStream_t st);
+// Convolution geometry of one SkConv2d call (ConvShape, layers.hpp:96-107).
+struct ConvGeom {
+    int B, c, h, w, kh, kw, stride, pad, oh, ow;
+};
+cudaError_t launch_im2col(const void* img, int elem, const ConvGeom& g, void* cols, cudaStream_t st);
+cudaError_t launch_col2im(const void* cols, int elem, const ConvGeom& g, void* img, cudaStream_t st);
+cudaError_t launch_tokens_planes(const void* in, int elem, int64_t B, int64_t P, int64_t C, void* out, int to_planes,
+                                 cudaStream_t st);
 cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st);
 }  // namespace skl

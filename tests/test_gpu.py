@@ -402,3 +402,40 @@ def test_from_dense_matches_oracle(skl, port, dtype_name, d_in, d_out, L, k):
     check_close("from_dense U1s", _np(lyr.U1s), abi["U1s"], dtype_name)
     check_close("from_dense U2s", _np(lyr.U2s), abi["U2s"], dtype_name)
     assert torch.equal(lyr.bias, b)
+
+
+# --------------------------------------------------------------------------- SkConv2d
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("stride,pad", [(1, 1), (2, 0)])
+def test_skconv2d_matches_reference(skl, ref, dtype_name, stride, pad):
+    """SkConv2d forward/backward on device (im2col -> SKLinear -> NCHW, col2im)
+    vs the REFERENCE's own SkConv2d (oracle/_ref) on the same parameters."""
+    import oracle
+    from paper_2601_15473_b200.conv import ConvShape, SkConv2d
+    from tests._util import check_close
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    cs = ConvShape(c_in=8, c_out=24, kernel_h=3, kernel_w=3, stride=stride, padding=pad)
+    conv = SkConv2d(cs, 2, 16, seed=9, dtype=dtype)
+    gen = torch.Generator(device="cuda").manual_seed(4)
+    conv.inner.bias.copy_((torch.randn(24, device="cuda", generator=gen) * 0.2).to(td))
+    B, H, W = 3, 10, 11
+    x = torch.randn(B, 8, H, W, device="cuda", generator=gen).to(td)
+    keep = {}
+    y = conv.forward(x, keep=keep)
+    g = torch.randn_like(y.float()).to(td)
+    gr = conv.backward(x, g, keep=keep)
+    gr2 = conv.backward(x, g)                       # recompute path (no kept patches)
+    torch.cuda.synchronize()
+    s = conv.inner
+    P = oracle.from_abi(s.d_in, s.d_out, _np(s.S1s), _np(s.U1s), _np(s.U2s), _np(s.S2s))
+    geo = (cs.c_in, cs.c_out, cs.kernel_h, cs.kernel_w, cs.stride, cs.padding)
+    y_ref = oracle.skconv_forward(ref, geo, P, _np(s.bias), _np(x))
+    check_close("conv y", _np(y), y_ref, dtype_name)
+    gx, gu1, gu2, gb = oracle.skconv_backward(ref, geo, P, _np(x), _np(g))
+    _, du1, du2, db = oracle.grads_to_abi(np.zeros((1, 1)), gu1, gu2, gb)
+    for tag, G in (("kept", gr), ("recompute", gr2)):
+        check_close(f"conv grad_x ({tag})", _np(G.grad_x), gx, dtype_name)
+        check_close(f"conv dU1s ({tag})", _np(G.grad_u1), du1, dtype_name)
+        check_close(f"conv dU2s ({tag})", _np(G.grad_u2), du2, dtype_name)
+        check_close(f"conv db ({tag})", _np(G.grad_b), db, dtype_name)
