@@ -105,6 +105,14 @@ __device__ unsigned long long g_b2b_prof[296][8];
 // buffer reuse, [2]/[3] epilogue named barriers, [4] waits on GEMM1 chunks,
 // [5] epilogue total.
 __device__ unsigned long long g_b2b_eprof[296][8];
+// SKL_B2B_DEBUG & 64: %globaltimer (ns) per CTA at [0] entry, [1] after the
+// prologue, [2] epilogue done (stores drained), [3] exit.
+__device__ unsigned long long g_b2b_ts[296][4];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 #define SKL_TIMED(slot, call)                                                  \
     do {                                                                       \
         if (args.dbg & 32) {                                                   \
@@ -158,6 +166,7 @@ __global__ void __launch_bounds__(384, 1)
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
     using C = B2BCfg<kCG, kMode, kKind>;
+    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][0] = gtimer();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(384, 1)
     if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][1] = gtimer();
 
     const int tile_rows = 128 * kCG;
     const int num_tiles = (args.T + tile_rows - 1) / tile_rows;
@@ -464,7 +474,11 @@ __global__ void __launch_bounds__(384, 1)
                                     dst[(long long)(col + i - args.save_col0) * args.ld_save] = __uint_as_float(r[i]);
                         }
                     }
-                } else
+                } else {
+                if (args.save) {  // buf doubles as the transpose scratch: the last store must have left it
+                    if (issuer) bulk_wait_read<0>();
+                    named_bar_sync(1 + wg, 128);
+                }
 #pragma unroll 1
                 for (int rd = 0; rd < 2; ++rd) {
                     const int qi = 2 * rd + (int)wg;
@@ -490,18 +504,33 @@ __global__ void __launch_bounds__(384, 1)
                         tmem_st8(tmem_base + lane_base + 128 * c + cl / 2, p);
                         const int col = 256 * c + cl;  // H column (R order)
                         // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
-                        // ld_save >= T): the token-reduction GEMMs then read them K-major.
-                        // Lanes are consecutive tokens, so each store is 64 contiguous bytes.
-                        if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
-                            __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(args.save) + row;
+                        // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
+                        // The warp's [32 tokens x 16 cols] block is transposed through a 1 KB
+                        // smem scratch so every lane writes two 16-B chunks (8 tokens of one
+                        // column) instead of 16 scattered 2-B stores (8 % of the kernel).
+                        if (args.save && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
                             const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
+                            __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(buf + q * 1024);  // [16 cols][32 tokens]
 #pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols)
-                                    dst[(long long)(col + i - args.save_col0) * args.ld_save] = pb[i];
+                            for (int i = 0; i < 16; ++i) scr[i * 32 + lane] = pb[i];
+                            __syncwarp();
+                            const long long tok0 = (long long)t * tile_rows + (int)rank * 128 + q * 32;
+#pragma unroll
+                            for (int hh = 0; hh < 2; ++hh) {
+                                const int id = (int)lane * 2 + hh, i = id >> 2, j = id & 3;
+                                const long long tok = tok0 + 8 * j;
+                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols &&
+                                    tok < args.ld_save) {
+                                    const uint4 v = *reinterpret_cast<const uint4*>(scr + i * 32 + 8 * j);
+                                    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.save) +
+                                                              (long long)(col + i - args.save_col0) * args.ld_save + tok) = v;
+                                }
+                            }
+                            __syncwarp();
                         }
                     }
                 }
+                }  // bf16 conversion
                 tmem_st_wait();
                 if (args.dbg & 32) prof[6] += (unsigned long long)(clock64() - tc0);
                 tc_fence_before();
@@ -633,6 +662,7 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
         if (issuer) bulk_wait<0>();
+        if ((args.dbg & 64) && issuer && wg == 0) g_b2b_ts[blockIdx.x][2] = gtimer();
         if ((args.dbg & 32) && issuer && wg == 0) {
             prof[5] = (unsigned long long)(clock64() - te0);
             for (int i = 0; i < 8; ++i) g_b2b_eprof[blockIdx.x][i] = prof[i];
@@ -645,6 +675,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<kCG>(tmem_base, 512);
     }
+    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][3] = gtimer();
 }
 
 }  // namespace dev

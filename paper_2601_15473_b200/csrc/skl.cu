@@ -1103,6 +1103,12 @@ extern "C" int skl_debug_b2b_prof(unsigned long long* out, int n) {
         return -1;
     return n;
 }
+extern "C" int skl_debug_b2b_ts(unsigned long long* out, int n) {
+    if (n > 296 * 4) n = 296 * 4;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_ts, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
 extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
     const int total = 296 * 8;
     if (n > total) n = total;
