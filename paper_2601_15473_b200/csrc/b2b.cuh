@@ -32,6 +32,9 @@
 
 #include "sm100.cuh"
 
+#ifndef SKL_FWD_BIAS_TAB
+#define SKL_FWD_BIAS_TAB 1  // 0 measured: 96 -> 106 us at c2 (per-tile bias loads cost more than the 6th stage)
+#endif
 #ifndef SKL_FWD_SINGLE_PASS
 #define SKL_FWD_SINGLE_PASS 0  // measured: 99 -> 116 us at c2 (3 stages starve GEMM2)
 #endif
@@ -140,9 +143,10 @@ struct B2BCfg {
     static constexpr int kStageBytes = (kCG == 1 || kSinglePassG1) ? 48 * 1024 : 32 * 1024;
     // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
-    static constexpr int kBiasTabBytes = kMode == 1 ? 32 * 1024 : 0;
+    static constexpr bool kBiasTab = kMode == 1 && SKL_FWD_BIAS_TAB;
+    static constexpr int kBiasTabBytes = kBiasTab ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kMode == 1 ? 1 : 0) - kKind;
+    static constexpr int kStages = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind;
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
     static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
@@ -421,7 +425,7 @@ __global__ void __launch_bounds__(384, 1)
                                   : __ldg(args.bias + col);
         };
         float bias_pref = 0.f;
-        if constexpr (kMode == 1) {
+        if constexpr (C::kBiasTab) {
             // whole bias resident in smem for the kernel's lifetime
             const int tid = (int)((warp - 4) * 32 + lane);
             for (int i = tid; i < args.N2; i += 256) bias_tab[i] = load_bias_col(i);
@@ -550,7 +554,7 @@ __global__ void __launch_bounds__(384, 1)
                 // Bias through smem (L1 is tiny with ~226 KB of smem in use);
                 // software-pipelined: this tile's value was loaded one tile ago.
                 float bval = 0.f;
-                if constexpr (kMode != 1) {
+                if constexpr (!C::kBiasTab) {
                     bval = bias_pref;
                     bias_pref = load_bias_col((j + 1 == n2_tiles ? 0 : j + 1) * 128 + (int)(wg * 64 + (srow & 63)));
                 }
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(384, 1)
                 SKL_TIMED(0, mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0));
                 if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
                 tc_fence_after();
-                if (kMode != 1 && srow < 64) bias_g[s * 64 + srow] = bval;  // published by the barrier below
+                if (!C::kBiasTab && srow < 64) bias_g[s * 64 + srow] = bval;  // published by the barrier below
                 if (args.dbg & 1) {  // perf bisection: release the slot without reading it
                     tc_fence_before();
                     __syncwarp();
@@ -624,7 +628,7 @@ __global__ void __launch_bounds__(384, 1)
                 }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
-                    const float4* bp = kMode == 1 ? reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)
+                    const float4* bp = C::kBiasTab ? reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)
                                                   : reinterpret_cast<const float4*>(bias_g + s * 64 + 8 * c);
                     const float4 b0 = bp[0], b1 = bp[1];
                     const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};

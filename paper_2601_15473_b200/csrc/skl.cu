@@ -346,7 +346,7 @@ void read_b2b_env() {
 bool direct_ok(const SklDims& d, skl_dtype t) {
     read_b2b_env();
     return g_b2b_direct && t == SKL_BF16 && d.k % 64 == 0 && d.R_pad == d.R &&
-           d.d_out <= dev::B2BCfg<2, 1, 0>::kMaxBiasTab;
+           (!dev::B2BCfg<2, 1, 0>::kBiasTab || d.d_out <= dev::B2BCfg<2, 1, 0>::kMaxBiasTab);
 }
 
 int pick_splits(int M, int N, int K, int bn, int cg, int sms, int bk) {
