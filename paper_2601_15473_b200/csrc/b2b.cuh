@@ -35,6 +35,9 @@
 #ifndef SKL_FWD_BIAS_TAB
 #define SKL_FWD_BIAS_TAB 1  // 0 measured: 96 -> 106 us at c2 (per-tile bias loads cost more than the 6th stage)
 #endif
+#ifndef SKL_SPLIT_RING
+#define SKL_SPLIT_RING 0  // measured at c2: fwd 96 -> 100-115 us, bwd 106 -> 105-133 us (off)
+#endif
 #ifndef SKL_FWD_SINGLE_PASS
 #define SKL_FWD_SINGLE_PASS 0  // measured: 99 -> 116 us at c2 (3 stages starve GEMM2)
 #endif
@@ -146,13 +149,34 @@ struct B2BCfg {
     static constexpr bool kBiasTab = kMode == 1 && SKL_FWD_BIAS_TAB;
     static constexpr int kBiasTabBytes = kBiasTab ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind;
+    static constexpr int kStages0 = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind;
+    // Split rings (kSplit, experiment, off): the activation tiles of GEMM1 (x /
+    // G, from HBM) get their own ring fed by a second producer warp, the
+    // L2-resident weight tiles (B1 chunks, B2) the main ring.  Tested because
+    // the MMA waits on full GEMM1 stages while the producer waits on empty
+    // ones; no split of the same smem beat the combined ring, and dropping a
+    // third of GEMM1's bytes (SKL_B2B_DEBUG & 128) gained only 3 %, so GEMM1
+    // is neither ingest- nor simply ring-depth-bound.
+    static constexpr bool kSplit = SKL_SPLIT_RING && kKind == 0 && kCG == 2;
+    static constexpr int kAOff = kSplit ? 0 : 16384;  // B1 offset inside a main-ring stage
+    static constexpr int kStageA = 16384;
+#ifndef SKL_SPLIT_A2
+#define SKL_SPLIT_A2 6
+#endif
+#ifndef SKL_SPLIT_A1
+#define SKL_SPLIT_A1 4
+#endif
+    static constexpr int kStagesA = !kSplit ? 0 : (kMode == 2 ? SKL_SPLIT_A2 : (kMode == 1 ? SKL_SPLIT_A1 : 5));
+    static constexpr int kStages = !kSplit ? kStages0 : (kMode == 2 ? (12 - SKL_SPLIT_A2) / 2 : (kMode == 1 ? 10 - SKL_SPLIT_A1 : 7));
+    static constexpr int kStageBytesW = !kSplit ? 0 : (kSinglePassG1 ? 32 * 1024 : 16 * 1024);
+    static constexpr int kStageMain = kSplit ? kStageBytesW : kStageBytes;
+    static constexpr int kRingBytes = kStages * kStageMain + kStagesA * kStageA;
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
-    static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
+    static constexpr int kKbPerStage2 = kStageMain / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
     static constexpr int kSmem =
-        kStages * kStageBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 256;
+        kRingBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 512;
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -174,7 +198,8 @@ __global__ void __launch_bounds__(384, 1)
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
-    uint8_t* stage_out = smem + C::kStages * C::kStageBytes;  // 2 x kOutBytes output staging
+    uint8_t* ringA = smem + C::kStages * C::kStageMain;       // kSplit: activation ring
+    uint8_t* stage_out = smem + C::kRingBytes;                  // 2 x kOutBytes output staging
     float* bias_s = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes);  // 2 slots x 128 bias values
     float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes + 1024);  // kMode 1: bias[N2]
     uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * C::kOutBytes + 1024 + C::kBiasTabBytes);
@@ -184,7 +209,9 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* hready = tfull1 + 2;                    // [2] chunk converted to bf16 H
     uint64_t* tfull2 = hready + 2;                    // [2] GEMM2 slot accumulated
     uint64_t* tempty2 = tfull2 + 2;                   // [2] GEMM2 slot drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty2 + 2);
+    uint64_t* fullA = tempty2 + 2;                    // [kStagesA] (kSplit)
+    uint64_t* emptyA = fullA + C::kStagesA;           // [kStagesA]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(emptyA + C::kStagesA);
 
     const uint32_t warp = warp_id();
     const uint32_t rank = kCG == 2 ? cluster_ctarank() : 0;
@@ -208,6 +235,10 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&hready[i], 8 * kCG);   // 8 epilogue warps per CTA
             mbar_init(&tfull2[i], 1);
             mbar_init(&tempty2[i], 8 * kCG);
+        }
+        for (int s = 0; s < C::kStagesA; ++s) {
+            mbar_init(&fullA[s], kCG);
+            mbar_init(&emptyA[s], 1);
         }
         fence_barrier_init();
     }
@@ -246,19 +277,21 @@ __global__ void __launch_bounds__(384, 1)
                 const int npass = C::kSinglePassG1 ? 1 : nch;
                 for (int pass = 0; pass < npass; ++pass) {
                     const int c_lo = C::kSinglePassG1 ? 0 : pass, c_hi = C::kSinglePassG1 ? nch : pass + 1;
-                    uint32_t bytes = 16384;
-                    for (int c = c_lo; c < c_hi; ++c) bytes += (min(256, args.R_pad - 256 * c) / kCG) * 128;
+                    uint32_t bytes = C::kSplit ? 0 : 16384;
+                    // perf experiment (SKL_B2B_DEBUG & 128): skip chunk 1's B1 bytes (wrong results)
+                    const int c_ld = (args.dbg & 128) ? min(c_hi, c_lo + 1) : c_hi;
+                    for (int c = c_lo; c < c_ld; ++c) bytes += (min(256, args.R_pad - 256 * c) / kCG) * 128;
                     for (int kb = 0; kb < nkb1; ++kb) {
                         SKL_TIMED(5, mbar_wait(&empty[stage], phase ^ 1));
-                        uint8_t* st = smem + stage * C::kStageBytes;
+                        uint8_t* st = smem + stage * C::kStageMain;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
-                        tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am);
-                        for (int c = c_lo; c < c_hi; ++c) {
+                        if constexpr (!C::kSplit) tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am);
+                        for (int c = c_lo; c < c_ld; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
                             const int brows = wc / kCG;
                             const int b0 = 256 * c + (int)rank * brows;
-                            uint8_t* bst = st + 16384 + (c - c_lo) * (256 / kCG) * 128;
+                            uint8_t* bst = st + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
                             if constexpr (kMode == 0) {
                                 for (int r = 0; r < brows; r += args.b1rows)
                                     tma_load_2d<kCG>(&tmB1, &full[stage], bst + r * 128, kb * C::kBK, b0 + r);
@@ -286,7 +319,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int kb0 = s * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
                         SKL_TIMED(6, mbar_wait(&empty[stage], phase ^ 1));
-                        uint8_t* st = smem + stage * C::kStageBytes;
+                        uint8_t* st = smem + stage * C::kStageMain;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
                         else mbar_arrive_cluster(&full[stage], 0);
                         if (kMode == 1 && args.b2tall) {
@@ -322,11 +355,32 @@ __global__ void __launch_bounds__(384, 1)
                 for (int i = 5; i < 8; ++i) g_b2b_prof[blockIdx.x][i] = prof[i];
             }
         }
+    } else if (warp == 3) {
+        // ---------------------------------------------------------------- producer A (kSplit)
+        if (C::kSplit && elect_one()) {
+            int sa = 0;
+            uint32_t pa = 0;
+            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+                const int am = t * tile_rows + (int)rank * 128;
+                const int npass = C::kSinglePassG1 ? 1 : nch;
+                for (int pass = 0; pass < npass; ++pass) {
+                    for (int kb = 0; kb < nkb1; ++kb) {
+                        mbar_wait(&emptyA[sa], pa ^ 1);
+                        if (leader) mbar_arrive_expect_tx(&fullA[sa], (uint32_t)C::kStageA * kCG);
+                        else mbar_arrive_cluster(&fullA[sa], 0);
+                        tma_load_2d<kCG>(&tmA1, &fullA[sa], ringA + sa * C::kStageA, kb * C::kBK, am);
+                        if (++sa == C::kStagesA) { sa = 0; pa ^= 1; }
+                    }
+                }
+            }
+        }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer
         if (leader && elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            int sa = 0;
+            uint32_t pa = 0;
             unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const long long tm0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
@@ -344,14 +398,16 @@ __global__ void __launch_bounds__(384, 1)
                         tc_fence_after();
                     }
                     for (int kb = 0; kb < nkb1; ++kb) {
+                        if constexpr (C::kSplit) SKL_TIMED(0, mbar_wait(&fullA[sa], pa));
                         SKL_TIMED(0, mbar_wait(&full[stage], phase));
                         tc_fence_after();
-                        const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
+                        const uint32_t w_addr = smem_u32(smem + stage * C::kStageMain);
+                        const uint32_t a_addr = C::kSplit ? smem_u32(ringA + sa * C::kStageA) : w_addr;
                         for (int c = c_lo; c < c_hi; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
                             const uint32_t idesc1 = make_idesc(kKind, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
                             const uint32_t d = tmem_base + 256 * c;
-                            const uint32_t b_addr = a_addr + 16384 + (c - c_lo) * (256 / kCG) * 128;
+                            const uint32_t b_addr = w_addr + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_ss<kCG, kKind>(d, make_sdesc(a_addr + k * 32, 0, 1024),
@@ -361,6 +417,10 @@ __global__ void __launch_bounds__(384, 1)
                         }
                         mma_commit<kCG>(&empty[stage]);
                         next();
+                        if constexpr (C::kSplit) {
+                            mma_commit<kCG>(&emptyA[sa]);
+                            if (++sa == C::kStagesA) { sa = 0; pa ^= 1; }
+                        }
                     }
                     for (int c = c_lo; c < c_hi; ++c) mma_commit<kCG>(&tfull1[c]);
                 }
@@ -378,7 +438,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
                         SKL_TIMED(1, mbar_wait(&full[stage], phase));
                         tc_fence_after();
-                        const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
+                        const uint32_t b_addr = smem_u32(smem + stage * C::kStageMain);
                         for (int q = 0; q < nk; ++q) {
                             if (args.dbg & 4) break;  // perf bisection: skip GEMM2 MMAs
 #pragma unroll
