@@ -777,8 +777,8 @@ skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned p
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::backward: T must be >= 0");
     if (phases == 0 || (phases & ~(unsigned)SKL_BWD_ALL)) return fail(SKL_ERR_PARAM, "bad phase mask %u", phases);
     const bool ph_u1 = (phases & SKL_BWD_DU1_DB) != 0, ph_data = (phases & SKL_BWD_DX_DU2) != 0;
-    if (!grad_y || !x || !S1s || !S2s || !U1s || !U2s || (ph_u1 && !grad_U1s) || (ph_data && !grad_U2s))
-        return fail(SKL_ERR_PARAM, "null tensor argument");
+    if ((ph_u1 && !grad_U1s) || (ph_data && !grad_U2s)) return fail(SKL_ERR_PARAM, "null gradient argument");
+    if (T > 0 && (!grad_y || !x || !S1s || !S2s || !U1s || !U2s)) return fail(SKL_ERR_PARAM, "null tensor argument");
     SKL_TRY(check_alignment(d, s->dtype));
     DevInfo di;
     SKL_TRY(check_device(di));

@@ -439,3 +439,98 @@ def test_skconv2d_matches_reference(skl, ref, dtype_name, stride, pad):
         check_close(f"conv dU1s ({tag})", _np(G.grad_u1), du1, dtype_name)
         check_close(f"conv dU2s ({tag})", _np(G.grad_u2), du2, dtype_name)
         check_close(f"conv db ({tag})", _np(G.grad_b), db, dtype_name)
+
+
+# --------------------------------------------------------------------------- edge cases and full-size properties
+@pytest.mark.parametrize("T", [0, 1, 7, 255, 257])
+def test_edge_token_counts(skl, port, T):
+    """Empty, single-token and ragged batches (the reference handles any T,
+    nn_layers.cpp:61-101): T = 0 is a no-op forward and zero gradients."""
+    import oracle
+    from tests._util import check_close
+    d_in, d_out, L, k = 256, 384, 2, 64
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, max(T, 1), skl.BF16)
+    X, G = X[:T], G[:T]
+    y = torch.full((T, d_out), 7.0, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(L * k, max(8, (T + 7) // 8 * 8), dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    gx = torch.empty(T, d_in, dtype=torch.bfloat16, device="cuda")
+    du1 = torch.full((L, k, d_out), 5.0, device="cuda")
+    du2 = torch.full((L, d_in, k), 5.0, device="cuda")
+    db = torch.full((d_out,), 5.0, device="cuda")
+    skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+    torch.cuda.synchronize()
+    if T == 0:
+        assert du1.abs().max().item() == 0 and du2.abs().max().item() == 0 and db.abs().max().item() == 0
+        return
+    x64, g64 = x64[:, :T].copy(), g64[:, :T].copy()
+    check_close(f"y T={T}", _np(y), port.forward(P, b64, x64).T, "bf16")
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    check_close(f"grad_x T={T}", _np(gx), rgx, "bf16")
+    check_close(f"dU1s T={T}", _np(du1), rgu1, "bf16")
+    check_close(f"dU2s T={T}", _np(du2), rgu2, "bf16")
+    check_close(f"db T={T}", _np(db), rgb, "bf16")
+
+
+def test_c3_shape_slice_matches_oracle(skl, port):
+    """BASELINE config 3 shape (4096 -> 4096, L=3, k=256: R = 1536, the unfused
+    chain) on a 512-token slice vs the f64 oracle (c3 parity on a
+    token slice; the f64 reference is too slow at 64k tokens)."""
+    import oracle
+    from tests._util import check_close
+    d_in, d_out, L, k, T = 4096, 4096, 3, 256, 512
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, skl.BF16)
+    y = torch.empty(T, d_out, dtype=torch.bfloat16, device="cuda")
+    saved = torch.empty(L * k, T, dtype=torch.bfloat16, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    gx = torch.empty(T, d_in, dtype=torch.bfloat16, device="cuda")
+    du1 = torch.empty(L, k, d_out, device="cuda")
+    du2 = torch.empty(L, d_in, k, device="cuda")
+    db = torch.empty(d_out, device="cuda")
+    skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+    torch.cuda.synchronize()
+    check_close("c3 y", _np(y), port.forward(P, b64, x64).T, "bf16")
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    check_close("c3 grad_x", _np(gx), rgx, "bf16")
+    check_close("c3 dU1s", _np(du1), rgu1, "bf16")
+    check_close("c3 dU2s", _np(du2), rgu2, "bf16")
+    check_close("c3 db", _np(db), rgb, "bf16")
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_full_size_c2_properties(skl, dtype_name):
+    """BASELINE config 2 at its full 32768 tokens, checked through
+    size-independent properties (the f64 oracle would take minutes):
+      * row independence: the forward of a token slice equals the same rows
+        of the full forward, bitwise;
+      * gradient additivity: dU1s/dU2s/db of the batch == the sums over two
+        ragged halves (reduction over tokens, nn_layers.cpp:90-99);
+      * determinism: a second backward is bitwise identical."""
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    d_in, d_out, L, k, T = 768, 3072, 2, 128, 32768
+    lyr = skl.SkLinear(d_in, d_out, L, k, seed=42, dtype=dtype)
+    gen = torch.Generator(device="cuda").manual_seed(1)
+    lyr.bias.copy_(torch.randn(d_out, device="cuda", generator=gen).to(td))
+    X = torch.randn(T, d_in, device="cuda", generator=gen).to(td)
+    G = torch.randn(T, d_out, device="cuda", generator=gen).to(td)
+    y = lyr.forward(X)
+    y_part = lyr.forward(X[1000:3000].contiguous())
+    torch.cuda.synchronize()
+    assert torch.equal(y[1000:3000], y_part)
+    h = 12345
+    full = lyr.backward(X, G)
+    a = lyr.backward(X[:h].contiguous(), G[:h].contiguous())
+    b = lyr.backward(X[h:].contiguous(), G[h:].contiguous())
+    again = lyr.backward(X, G)
+    torch.cuda.synchronize()
+    for name, f, p, q in (("dU1s", full.grad_u1, a.grad_u1, b.grad_u1), ("dU2s", full.grad_u2, a.grad_u2, b.grad_u2),
+                          ("db", full.grad_b, a.grad_b, b.grad_b)):
+        rel = ((f - (p + q)).norm() / f.norm()).item()
+        assert rel < 1e-4, (name, rel)  # fp32 sums of 32768 tokens in a different split order
+    assert torch.equal(full.grad_x[:h], a.grad_x) and torch.equal(full.grad_x[h:], b.grad_x)
+    for u, v in zip((full.grad_x, full.grad_u1, full.grad_u2, full.grad_b),
+                    (again.grad_x, again.grad_u1, again.grad_u2, again.grad_b)):
+        assert torch.equal(u, v)
