@@ -250,6 +250,8 @@ __global__ void __launch_bounds__(384, 1)
     if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_launch_dependents();
+    pdl_wait();  // inputs of this launch may come from the previous kernel in the stream
     if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][1] = gtimer();
 
     const int tile_rows = 128 * kCG;

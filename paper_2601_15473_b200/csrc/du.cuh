@@ -127,6 +127,8 @@ __global__ void __launch_bounds__(256, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_launch_dependents();  // lets the next kernel (the next layer / step) stage its prologue
+    pdl_wait();
 
     const int units = args.num_units;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;

@@ -122,6 +122,18 @@ skl_status make_tmap(CUtensorMap* m, const void* ptr, int elem_bytes, int64_t in
     return SKL_OK;
 }
 
+// Programmatic dependent launch on the fused / GEMM kernels (SKL_PDL=0 disables).
+bool pdl_enabled() {
+    static const bool on = !(getenv("SKL_PDL") && atoi(getenv("SKL_PDL")) == 0);
+    return on;
+}
+void add_pdl(cudaLaunchAttribute* attrs, unsigned& n) {
+    if (!pdl_enabled()) return;
+    attrs[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attrs[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+}
+
 // ---------------------------------------------------------------- GEMM launch
 // Operand view: element (row-major storage) pointer, storage rows x cols, ld.
 struct View {
@@ -163,13 +175,15 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     cfg.blockDim = dim3(256);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    unsigned nattr = 1;
+    add_pdl(attr, nattr);
+    cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
     SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, to, args));
     return SKL_OK;
@@ -238,13 +252,15 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     cfg.blockDim = dim3(384);  // 4 control warps + 2 epilogue warpgroups
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    unsigned nattr = 1;
+    add_pdl(attr, nattr);
+    cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
     SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, a));
     return SKL_OK;
@@ -272,13 +288,15 @@ skl_status run_b2b_tf32_wide(const char* name, const B2BSrc& src, B2BArgs a, int
     cfg.blockDim = dim3(384);
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    unsigned nattr = 1;
+    add_pdl(attr, nattr);
+    cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
     SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, ty, a));
     return SKL_OK;
