@@ -51,6 +51,8 @@ struct DuArgs {
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
     int dbg;         // SKL_DU_DEBUG=1: per-CTA cycle accounting into g_du_prof (perf analysis)
+    int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); the split
+                     // partials are summed from the peers' shared memory (DSMEM) instead of global memory
 };
 
 namespace dev {
@@ -62,7 +64,8 @@ constexpr int kDuBM = 128, kDuBN = 256, kDuStages = 6;
 constexpr int kDuABytes = kDuBM * 128;        // K-major [128 rows x 128 B of tokens]
 constexpr int kDuBBytes = (kDuBN / 2) * 128;  // MN-major blocks [tokens x 128 B of columns]
 constexpr int kDuStageBytes = kDuABytes + kDuBBytes;
-constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 8 * 128 * 4;
+constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 8 * 128 * 4 + 128 * 4;
+constexpr int kDuCrLd = kDuBN + 4;  // padded row stride (floats) of the cluster-reduce partial in smem
 template <int kKind>
 struct DuKind {
     static constexpr int kElem = kKind == 0 ? 2 : 4;
@@ -97,10 +100,15 @@ __global__ void __launch_bounds__(256, 1)
     int* ticket_s = reinterpret_cast<int*>(tmem_slot + 1);
     uint64_t* rbar = tempty + 3;  // (8-B slot after tmem_slot/ticket_s) reduction bulk-load barrier
     float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [8][128]
+    float* cr_cs = csum_s + 8 * 128;                        // [128] this CTA's column sums (cluster reduce)
+    float* cr_part = reinterpret_cast<float*>(smem);        // [128][kDuCrLd] accumulator (cluster reduce)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
-    const uint32_t rank = cluster_ctarank();
+    const uint32_t crank = cluster_ctarank();
+    const uint32_t rank = crank & 1u;           // rank inside the MMA pair
+    const uint32_t lead_cta = crank & ~1u;      // cluster rank of the pair's leader
+    const uint16_t pair_mask = (uint16_t)(3u << lead_cta);
     const bool leader = rank == 0;
 
     if (warp == 0 && elect_one()) {
@@ -142,8 +150,10 @@ __global__ void __launch_bounds__(256, 1)
         const DuProblem& P = args.p[x.p];
         const int ptiles = P.m_tiles * P.n_tiles;
         const int lu = u - P.unit0;
-        x.split = lu / ptiles;  // split-major within the problem: concurrent units share a token window
-        const int lt = lu % ptiles;
+        // split-major within the problem (concurrent units share a token window);
+        // cluster-reduce mode: tile-major, the S splits of a tile are one cluster
+        x.split = args.cr ? lu % P.splits : lu / ptiles;
+        const int lt = args.cr ? lu / P.splits : lu % ptiles;
         x.tile = P.tile0 + lt;
         x.slot = P.slot0 + lt * P.splits;
         x.nsplit = P.splits;
@@ -181,7 +191,7 @@ __global__ void __launch_bounds__(256, 1)
                     if (!args.relay) {
                         // no colsum anywhere: pair-signalled TMA straight onto the leader's barrier
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kDuStageBytes);
-                        else mbar_arrive_cluster(&full[stage], 0);
+                        else mbar_arrive_cluster(&full[stage], lead_cta);
                         tma_load_2d<2>(ma, &full[stage], a_dst, k0, m0);
 #pragma unroll
                         for (int j = 0; j < 128 / KT::kW; ++j)
@@ -234,12 +244,12 @@ __global__ void __launch_bounds__(256, 1)
                                          kKind == 0 ? make_sdesc(b_addr + k * KT::kUK * 128, KT::kBK * 128, 1024)
                                                     : make_sdesc(b_addr + k * KT::kUK * 128, KT::kBK * 128, 512, 1),
                                          idesc, (kb > x.kb0 || k > 0) ? 1u : 0u);
-                    mma_commit<2>(&empty[stage]);
+                    mma_commit_pair(&empty[stage], pair_mask);
                     if (!x.colsum)  // stand in for the 4 colsum warps (multicast to both CTAs)
-                        for (int i = 0; i < 4; ++i) mma_commit<2>(&empty[stage]);
+                        for (int i = 0; i < 4; ++i) mma_commit_pair(&empty[stage], pair_mask);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
-                mma_commit<2>(&tfull[acc]);
+                mma_commit_pair(&tfull[acc], pair_mask);
             }
             if (args.dbg) {
                 g_du_prof[blockIdx.x][2] = w_full;
@@ -255,7 +265,7 @@ __global__ void __launch_bounds__(256, 1)
                 const Unit x = decode(u);
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);        // our half has landed
-                    mbar_arrive_cluster(&full[stage], 0);  // tell the leader's MMA issuer
+                    mbar_arrive_cluster(&full[stage], lead_cta);  // tell the leader's MMA issuer
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -328,7 +338,8 @@ __global__ void __launch_bounds__(256, 1)
                     float s = 0.f;
 #pragma unroll
                     for (int g = 0; g < kGroups; ++g) s += csum_s[g * 128 + t];
-                    __stcg(args.cpart + ((long long)x.nt * x.nsplit + x.split) * kDuBN + rank * 128 + t, s);
+                    if (args.cr) cr_cs[t] = s;
+                    else __stcg(args.cpart + ((long long)x.nt * x.nsplit + x.split) * kDuBN + rank * 128 + t, s);
                 }
                 named_bar_sync(2, 128);
             } else {
@@ -342,6 +353,30 @@ __global__ void __launch_bounds__(256, 1)
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
             lap(e_acc);
+            if (args.cr) {
+                // accumulator -> this CTA's smem (the operand ring is idle now); the
+                // cluster sums it with its peers' after the kernel-wide cluster barrier
+                const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
+                float* srow = cr_part + t * kDuCrLd;
+#pragma unroll 1
+                for (int c = 0; c < kDuBN; c += 32) {
+                    uint32_t v[32];
+                    tmem_ld32(t_row + c, v);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int i = 0; i < 32; i += 4)
+                        *reinterpret_cast<float4*>(srow + c + i) =
+                            make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
+                                        __uint_as_float(v[i + 3]));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    if (leader) mbar_arrive(&tempty[acc]);
+                    else mbar_arrive_cluster(&tempty[acc], lead_cta);
+                }
+                continue;
+            }
             {
                 float* prow = args.part + (((long long)x.slot + x.split) * 256 + rank * 128 + t) * kDuBN;
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
@@ -361,7 +396,7 @@ __global__ void __launch_bounds__(256, 1)
             __syncwarp();
             if (lane == 0) {
                 if (leader) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(&tempty[acc], 0);
+                else mbar_arrive_cluster(&tempty[acc], lead_cta);
             }
 
             lap(e_part);
@@ -508,6 +543,48 @@ __global__ void __launch_bounds__(256, 1)
     }
     tc_fence_before();
     cluster_sync();
+    if (args.cr && pair < units) {
+        // ---- cluster reduction: this CTA (split p, pair rank r) sums rows
+        // [p*128/S, (p+1)*128/S) of its rank's 128 rows over the S splits' smem
+        // partials (DSMEM, split order 0..S-1: deterministic), and the same slice
+        // of the rank's 128 db columns.
+        const Unit x = decode(pair);
+        const DuProblem& P = args.p[x.p];
+        const int S = x.nsplit, sp = x.split;
+        const int r0 = sp * 128 / S, r1 = (sp + 1) * 128 / S;
+        const int m_base = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256;
+        const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
+                         (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
+        const int nf = (r1 - r0) * (kDuBN / 4);
+        for (int f = (int)threadIdx.x; f < nf; f += (int)blockDim.x) {
+            const int row = r0 + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
+            const float* src = cr_part + row * kDuCrLd + c;
+            float4 sum = ld_dsmem_f4(src, (uint32_t)rank);  // split 0 lives in cluster rank 0 / 1
+            for (int q2 = 1; q2 < S; ++q2) {
+                const float4 v = ld_dsmem_f4(src, (uint32_t)(2 * q2) + rank);
+                sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+            }
+            const int m = m_base + row, n = n0 + c;
+            if (m >= P.M || n >= P.N) continue;
+            const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
+            const long long mo = P.mb >= P.M ? (long long)m * P.ms : (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
+            if (vec && n + 4 <= P.N) {
+                *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
+            } else {
+                for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
+            }
+        }
+        if (x.colsum) {
+            for (int c = r0 + (int)threadIdx.x; c < r1; c += (int)blockDim.x) {
+                const int n = n0 + (int)rank * 128 + c;
+                if (n >= P.N) continue;
+                float sum = 0.f;
+                for (int q2 = 0; q2 < S; ++q2) sum += ld_dsmem_f32(cr_cs + c, (uint32_t)(2 * q2) + rank);
+                P.db[n] = sum;
+            }
+        }
+        cluster_sync();  // the peers are done reading this CTA's smem
+    }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<2>(tmem_base, 512);

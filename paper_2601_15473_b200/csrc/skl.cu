@@ -442,6 +442,7 @@ int64_t t8(int64_t T) { return (T + 7) / 8 * 8; }
 // serial reductions).
 struct DuShape {
     int m0, n0t, m1, n1t, t0, t1, s0, s1, kb, units;  // t*/s*: tiles / T splits of dU1 (0) and dU2 (1)
+    bool cr;                                          // cluster (DSMEM) reduction of the split partials
     int tiles() const { return t0 + t1; }
 };
 DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) {
@@ -477,6 +478,12 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
         if (n >= 1 && a > 0) s.s0 = std::min(a, s.kb), s.s1 = std::min(n == 2 && b > 0 ? b : a, s.kb);
     }
     s.units = s.t0 * s.s0 + s.t1 * s.s1;
+    // Cluster reduction (du.cuh, DuArgs::cr): one cluster of 2S CTAs per tile, the
+    // split partials summed over DSMEM -- needs one S for both problems and a
+    // cluster of at most 8 CTAs.  Otherwise partials go through global memory.
+    static const bool cr_on = !(getenv("SKL_DU_CR") && atoi(getenv("SKL_DU_CR")) == 0);
+    const int sc = s.t0 ? s.s0 : s.s1;
+    s.cr = cr_on && sc <= 4 && (!s.t0 || !s.t1 || s.s0 == s.s1);
     return s;
 }
 
@@ -566,7 +573,7 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     tb0 = (which & 1) ? tu1b : tu2b;
     ta1 = tu2a;
     tb1 = tu2b;
-    SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles() * 4, st));
+    if (!u.cr) SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles() * 4, st));
     auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
     static bool attr_set[2] = {false, false};
     if (!attr_set[kind]) {
@@ -575,6 +582,30 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     }
     const int units = u.units;  // CTA-pair work units
     a.relay = colsum ? 1 : 0;
+    if (u.cr) {
+        // one cluster of 2S CTAs per tile: no cross-cluster synchronisation, so
+        // neither a cooperative launch nor co-residency of all units is needed
+        a.cr = 1;
+        a.coop = 0;
+        const int S = u.t0 ? u.s0 : u.s1;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(2 * units);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = dev::kDuSmem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2 * S;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        unsigned nattr = 1;
+        add_pdl(attr, nattr);
+        cfg.attrs = attr;
+        cfg.numAttrs = nattr;
+        ProfScope ps_("du_fused", st);
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a));
+        return SKL_OK;
+    }
     static const int du_dbg = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;  // perf analysis
     a.dbg = du_dbg;
     static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers

@@ -210,6 +210,38 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
             : "memory");
 }
 
+// cta_group::2 commit multicast to an explicit CTA mask (a pair inside a larger cluster).
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+// 16-byte load from CTA `cta`'s shared memory at the offset of `p` (DSMEM).
+__device__ __forceinline__ float4 ld_dsmem_f4(const void* p, uint32_t cta) {
+    float4 v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %4, %5;\n\t"
+        "ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [ra];\n\t}"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "r"(smem_u32(p)), "r"(cta)
+        : "memory");
+    return v;
+}
+__device__ __forceinline__ float ld_dsmem_f32(const void* p, uint32_t cta) {
+    float v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
+        "ld.shared::cluster.f32 %0, [ra];\n\t}"
+        : "=f"(v)
+        : "r"(smem_u32(p)), "r"(cta)
+        : "memory");
+    return v;
+}
+
 // 32 lanes x 32 bit, 16 consecutive columns per thread.
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
