@@ -114,11 +114,6 @@ __device__ unsigned long long g_b2b_eprof[296][8];
 // SKL_B2B_DEBUG & 64: %globaltimer (ns) per CTA at [0] entry, [1] after the
 // prologue, [2] epilogue done (stores drained), [3] exit.
 __device__ unsigned long long g_b2b_ts[296][4];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
 #define SKL_TIMED(slot, call)                                                  \
     do {                                                                       \
         if (args.dbg & 32) {                                                   \
@@ -250,8 +245,8 @@ __global__ void __launch_bounds__(384, 1)
     if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_launch_dependents();
     pdl_wait();  // inputs of this launch may come from the previous kernel in the stream
+    pdl_launch_dependents();  // after the wait: a dependent starts only once our predecessor completed
     if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][1] = gtimer();
 
     const int tile_rows = 128 * kCG;

@@ -112,8 +112,8 @@ __global__ void __launch_bounds__(384, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_launch_dependents();
     pdl_wait();
+    pdl_launch_dependents();  // after the wait: a dependent starts only once our predecessor completed
 
     const int tile_rows = 256;
     const int num_tiles = (args.T + tile_rows - 1) / tile_rows;

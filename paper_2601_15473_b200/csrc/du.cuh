@@ -21,8 +21,12 @@
 // their own stages).
 //
 // Reduction is deterministic and in-kernel: every (tile, split, rank) writes
-// its fp32 partial; with a cooperative launch all units are co-resident and
-// the 2·S CTAs of a tile each reduce a 1/(2S) slice in split order 0..S-1.
+// its fp32 partial and the 2·S CTAs of a tile each reduce a 1/(2S) slice in
+// split order 0..S-1.  Default (DuArgs::cr): the S split pairs of a tile are
+// one thread-block cluster; partials move with single bulk copies (smem ->
+// global -> the reducing CTA's smem) around one cluster barrier.  Fallbacks
+// (S > 4): a cooperative launch with a grid-wide ticket barrier, or the last
+// CTA of a tile reducing it alone (SKL_DU_NOCOOP).
 #pragma once
 
 #include "sm100.cuh"
@@ -51,8 +55,9 @@ struct DuArgs {
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
     int dbg;         // SKL_DU_DEBUG=1: per-CTA cycle accounting into g_du_prof (perf analysis)
-    int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); the split
-                     // partials are summed from the peers' shared memory (DSMEM) instead of global memory
+    int early;       // 1: dU1 units skip the PDL wait (see du_kernel); needs cr and a dU2 problem in p[1]
+    int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); each CTA
+                     // bulk-stores its partial, the cluster barrier publishes it, each CTA bulk-loads its slice
 };
 
 namespace dev {
@@ -65,7 +70,6 @@ constexpr int kDuABytes = kDuBM * 128;        // K-major [128 rows x 128 B of to
 constexpr int kDuBBytes = (kDuBN / 2) * 128;  // MN-major blocks [tokens x 128 B of columns]
 constexpr int kDuStageBytes = kDuABytes + kDuBBytes;
 constexpr int kDuSmem = kDuStages * kDuStageBytes + 1024 + 256 + 8 * 128 * 4 + 128 * 4;
-constexpr int kDuCrLd = kDuBN + 4;  // padded row stride (floats) of the cluster-reduce partial in smem
 template <int kKind>
 struct DuKind {
     static constexpr int kElem = kKind == 0 ? 2 : 4;
@@ -79,13 +83,30 @@ struct DuKind {
 // colsum phase, [5] epilogue waits on the accumulator, [6] partial write,
 // [7] reduction (ticket wait + sum).
 __device__ unsigned long long g_du_prof[296][8];
+__device__ unsigned long long g_du_ts[296][10];
+__device__ unsigned long long g_du_wend[296][16];  // SKL_DU_DEBUG&2: per-warp reduce-loop end / kernel end  // SKL_DU_DEBUG&2: globaltimer at entry / exit / prologue done / reduce start
 __device__ unsigned long long g_du_wait[296][4];  // [cta]: fence+ticket wait, +fence, +sum, +colsum/release
+
+// Cluster-reduce tail parameters, precomputed at kernel start into shared memory:
+// the tail runs once per CTA with a cold instruction cache (ncu: stall_no_inst),
+// so it is kept short and free of the unit decode.
+struct DuTail {
+    float* out;        // P.out
+    float* db;         // P.db (colsum units)
+    const float* g0;   // split-0 partial of this pair rank: [128][256]; splits 2*128*256 apart
+    const float* c0;   // split-0 column sums of this rank; splits 256 apart
+    long long mbs, ms, ns;
+    int mb, M, N, m0, n0, r0, rows, S, colsum, vec;
+    float alpha;
+};
+static_assert(132 * kDuBN * 4 + 4 * 512 <= kDuStages * kDuStageBytes, "cluster-reduce staging exceeds the ring");
 
 template <int kKind>
 __global__ void __launch_bounds__(256, 1)
     du_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1, DuArgs args) {
     using KT = DuKind<kKind>;
+    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][0] = gtimer();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -100,8 +121,7 @@ __global__ void __launch_bounds__(256, 1)
     int* ticket_s = reinterpret_cast<int*>(tmem_slot + 1);
     uint64_t* rbar = tempty + 3;  // (8-B slot after tmem_slot/ticket_s) reduction bulk-load barrier
     float* csum_s = reinterpret_cast<float*>(smem + kDuStages * kDuStageBytes + 256);  // [8][128]
-    float* cr_cs = csum_s + 8 * 128;                        // [128] this CTA's column sums (cluster reduce)
-    float* cr_part = reinterpret_cast<float*>(smem);        // [128][kDuCrLd] accumulator (cluster reduce)
+    float* cr_part = reinterpret_cast<float*>(smem);        // [128][256] chunk-swizzled accumulator (cluster reduce)
 
     const uint32_t warp = warp_id();
     const uint32_t lane = lane_id();
@@ -135,8 +155,19 @@ __global__ void __launch_bounds__(256, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_launch_dependents();  // lets the next kernel (the next layer / step) stage its prologue
-    pdl_wait();
+    // early (cluster-reduce launches right after this backward's dX kernel): dU1
+    // units read only Savedᵀ and G, produced before that kernel, so they start on
+    // the SMs its last wave leaves idle.  They do not trigger dependents; the
+    // dU2 units wait, then trigger, which keeps the chain invariant above.
+    const bool early_cta = args.early && args.cr && (int)(blockIdx.x >> 1) < args.p[1].unit0;
+    if (!early_cta) {
+        pdl_wait();
+        pdl_launch_dependents();
+    }
+    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) {
+        g_du_ts[blockIdx.x][2] = gtimer();
+        g_du_ts[blockIdx.x][4] = (unsigned long long)clock64();
+    }
 
     const int units = args.num_units;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -164,6 +195,32 @@ __global__ void __launch_bounds__(256, 1)
         x.colsum = args.p[x.p].colsum && x.mt == 0;
         return x;
     };
+
+    DuTail* tail = reinterpret_cast<DuTail*>(csum_s + 8 * 128);  // 512 B slot after the colsum scratch
+    if (args.cr && threadIdx.x == 0 && pair < units) {
+        const Unit x = decode(pair);
+        const DuProblem& P = args.p[x.p];
+        DuTail d;
+        d.out = P.out;
+        d.db = P.db;
+        d.g0 = args.part + ((long long)(pair - x.split) * 2 + rank) * 128 * kDuBN;
+        d.c0 = args.cpart + (long long)x.nt * x.nsplit * kDuBN + rank * 128;
+        d.mbs = P.mbs;
+        d.ms = P.ms;
+        d.ns = P.ns;
+        d.mb = P.mb >= P.M ? P.M : (int)P.mb;
+        d.M = P.M;
+        d.N = P.N;
+        d.r0 = x.split * 128 / x.nsplit;
+        d.rows = (x.split + 1) * 128 / x.nsplit - d.r0;
+        d.m0 = x.mt * 256 + (int)rank * 128 + d.r0;
+        d.n0 = x.nt * 256;
+        d.S = x.nsplit;
+        d.colsum = x.colsum ? 1 : 0;
+        d.vec = P.ns == 1 && ((P.ms | P.mbs) & 3) == 0 && (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
+        d.alpha = P.alpha;
+        *tail = d;
+    }
 
     if (warp == 0) {
         // ------------------------------------------------------------ producer (both CTAs, own half)
@@ -338,8 +395,7 @@ __global__ void __launch_bounds__(256, 1)
                     float s = 0.f;
 #pragma unroll
                     for (int g = 0; g < kGroups; ++g) s += csum_s[g * 128 + t];
-                    if (args.cr) cr_cs[t] = s;
-                    else __stcg(args.cpart + ((long long)x.nt * x.nsplit + x.split) * kDuBN + rank * 128 + t, s);
+                    __stcg(args.cpart + ((long long)x.nt * x.nsplit + x.split) * kDuBN + rank * 128 + t, s);
                 }
                 named_bar_sync(2, 128);
             } else {
@@ -357,7 +413,9 @@ __global__ void __launch_bounds__(256, 1)
                 // accumulator -> this CTA's smem (the operand ring is idle now); the
                 // cluster sums it with its peers' after the kernel-wide cluster barrier
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc * kDuBN;
-                float* srow = cr_part + t * kDuCrLd;
+                // row t, 16-B chunk j at chunk (j ^ (t & 7)): conflict-free, and rows stay
+                // contiguous so the partial moves with one bulk copy
+                float* srow = cr_part + t * kDuBN;
 #pragma unroll 1
                 for (int c = 0; c < kDuBN; c += 32) {
                     uint32_t v[32];
@@ -365,7 +423,7 @@ __global__ void __launch_bounds__(256, 1)
                     tmem_ld_wait();
 #pragma unroll
                     for (int i = 0; i < 32; i += 4)
-                        *reinterpret_cast<float4*>(srow + c + i) =
+                        *reinterpret_cast<float4*>(srow + ((((c + i) >> 2) ^ (t & 7)) << 2)) =
                             make_float4(__uint_as_float(v[i]), __uint_as_float(v[i + 1]), __uint_as_float(v[i + 2]),
                                         __uint_as_float(v[i + 3]));
                 }
@@ -541,54 +599,115 @@ __global__ void __launch_bounds__(256, 1)
             g_du_prof[blockIdx.x][7] = e_red;
         }
     }
-    tc_fence_before();
-    cluster_sync();
     if (args.cr && pair < units) {
-        // ---- cluster reduction: this CTA (split p, pair rank r) sums rows
-        // [p*128/S, (p+1)*128/S) of its rank's 128 rows over the S splits' smem
-        // partials (DSMEM, split order 0..S-1: deterministic), and the same slice
-        // of the rank's 128 db columns.
-        const Unit x = decode(pair);
-        const DuProblem& P = args.p[x.p];
-        const int S = x.nsplit, sp = x.split;
-        const int r0 = sp * 128 / S, r1 = (sp + 1) * 128 / S;
-        const int m_base = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256;
-        const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
-                         (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
-        const int nf = (r1 - r0) * (kDuBN / 4);
-        for (int f = (int)threadIdx.x; f < nf; f += (int)blockDim.x) {
-            const int row = r0 + f / (kDuBN / 4), c = (f % (kDuBN / 4)) * 4;
-            const float* src = cr_part + row * kDuCrLd + c;
-            float4 sum = ld_dsmem_f4(src, (uint32_t)rank);  // split 0 lives in cluster rank 0 / 1
-            for (int q2 = 1; q2 < S; ++q2) {
-                const float4 v = ld_dsmem_f4(src, (uint32_t)(2 * q2) + rank);
-                sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
-            }
-            const int m = m_base + row, n = n0 + c;
-            if (m >= P.M || n >= P.N) continue;
-            const float o[4] = {sum.x * P.alpha, sum.y * P.alpha, sum.z * P.alpha, sum.w * P.alpha};
-            const long long mo = P.mb >= P.M ? (long long)m * P.ms : (m / P.mb) * P.mbs + (m % P.mb) * P.ms;
-            if (vec && n + 4 <= P.N) {
-                *reinterpret_cast<float4*>(P.out + mo + n) = make_float4(o[0], o[1], o[2], o[3]);
-            } else {
-                for (int i = 0; i < 4 && n + i < P.N; ++i) P.out[mo + (long long)(n + i) * P.ns] = o[i];
+        // ---- cluster reduction.  Every CTA bulk-stores its (chunk-swizzled) smem
+        // partial to its global slot [unit][rank][128][256]; the cluster barrier
+        // publishes them; this CTA (split sp, pair rank r) then bulk-loads rows
+        // [sp*128/S, (sp+1)*128/S) of its rank's 128 rows from every split (one
+        // copy per split) plus the splits' column sums, and sums in split order
+        // 0..S-1.  Few, large copies: per-copy TMA overhead and the cold tail code
+        // (ncu: stall_no_inst) are what this phase costs.
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            fence_proxy_async_smem();  // the dump was written by generic stores
+            bulk_store_1d(args.part + ((long long)pair * 2 + rank) * 128 * kDuBN, cr_part, 128 * kDuBN * 4);
+            bulk_commit();
+            bulk_wait<0>();
+            __threadfence();
+        }
+        tc_fence_before();
+        cluster_sync();
+        const bool ts = (args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296;
+        if (ts) {
+            g_du_ts[blockIdx.x][3] = gtimer();
+            g_du_ts[blockIdx.x][5] = (unsigned long long)clock64();
+        }
+        const DuTail d = *tail;  // registers: the output stores must not force reloads
+        const int S = d.S, rows = d.rows;
+        float* cs = cr_part + 132 * kDuBN;  // past S * ceil(128 / S) <= 131 slice rows
+        if (threadIdx.x == 0) {
+            fence_proxy_async_global();  // order the acquired view before the bulk reads
+            mbar_arrive_expect_tx(rbar, (uint32_t)(S * rows * kDuBN * 4 + (d.colsum ? S * 512 : 0)));
+            for (int q2 = 0; q2 < S; ++q2) {
+                bulk_load_1d(cr_part + q2 * rows * kDuBN, d.g0 + ((long long)q2 * 256 + d.r0) * kDuBN,
+                             (uint32_t)rows * kDuBN * 4, rbar);
+                if (d.colsum) bulk_load_1d(cs + q2 * 128, d.c0 + q2 * kDuBN, 512, rbar);
             }
         }
-        if (x.colsum) {
-            for (int c = r0 + (int)threadIdx.x; c < r1; c += (int)blockDim.x) {
-                const int n = n0 + (int)rank * 128 + c;
-                if (n >= P.N) continue;
-                float sum = 0.f;
-                for (int q2 = 0; q2 < S; ++q2) sum += ld_dsmem_f32(cr_cs + c, (uint32_t)(2 * q2) + rank);
-                P.db[n] = sum;
+        if (ts) g_du_ts[blockIdx.x][6] = gtimer();
+        mbar_wait(rbar, 0);
+        if (ts) g_du_ts[blockIdx.x][7] = gtimer();
+        // element (slice row r, column c) of split q2: row q2 * rows + r, chunk (c/4) ^ ((r0 + r) & 7)
+        if (d.ns == 1) {
+            // row-contiguous output (dU1): lanes over 4-column chunks, float4 stores
+#pragma unroll 1
+            for (int f = (int)threadIdx.x; f < rows * (kDuBN / 4); f += 256) {
+                const int r = f >> 6, j = f & 63;
+                const int m = d.m0 + r, n = d.n0 + j * 4;
+                if (m >= d.M || n >= d.N) continue;
+                const float* src = cr_part + r * kDuBN + ((j ^ ((d.r0 + r) & 7)) << 2);
+                float4 a = *reinterpret_cast<const float4*>(src);
+#pragma unroll 1
+                for (int q2 = 1; q2 < S; ++q2) {
+                    const float4 v = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
+                    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                }
+                float* o = d.out + (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms + n;
+                if (d.vec && n + 4 <= d.N) {
+                    *reinterpret_cast<float4*>(o) = make_float4(a.x * d.alpha, a.y * d.alpha, a.z * d.alpha, a.w * d.alpha);
+                } else {
+                    const float av[4] = {a.x, a.y, a.z, a.w};
+                    for (int i = 0; i < 4 && n + i < d.N; ++i) o[i] = av[i] * d.alpha;
+                }
+            }
+        } else {
+            // strided columns (dU2ᵀ: consecutive rows contiguous): lanes over rows,
+            // one 4-column chunk per step, so each scalar store covers 32 rows
+#pragma unroll 1
+            for (int j = (int)warp; j < kDuBN / 4; j += 8) {
+                const int n = d.n0 + j * 4;
+                if (n >= d.N) break;
+#pragma unroll 1
+                for (int r = (int)lane; r < rows; r += 32) {
+                    const int m = d.m0 + r;
+                    if (m >= d.M) break;
+                    const float* src = cr_part + r * kDuBN + ((j ^ ((d.r0 + r) & 7)) << 2);
+                    float4 a = *reinterpret_cast<const float4*>(src);
+#pragma unroll 1
+                    for (int q2 = 1; q2 < S; ++q2) {
+                        const float4 v = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
+                        a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                    }
+                    float* o = d.out + (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms + n * d.ns;
+                    const float av[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)
+                        if (n + i < d.N) o[i * d.ns] = av[i] * d.alpha;
+                }
             }
         }
-        cluster_sync();  // the peers are done reading this CTA's smem
+        if (d.colsum) {
+            for (int c = d.r0 + (int)threadIdx.x; c < d.r0 + rows; c += 256) {
+                const int n = d.n0 + (int)rank * 128 + c;
+                if (n >= d.N) continue;
+                float sum = cs[c];
+                for (int q2 = 1; q2 < S; ++q2) sum += cs[q2 * 128 + c];
+                d.db[n] = sum;
+            }
+        }
+        if (ts) g_du_ts[blockIdx.x][8] = gtimer();
+        if ((args.dbg & 2) && lane == 0 && blockIdx.x < 296) g_du_wend[blockIdx.x][warp] = gtimer();
+        if (ts) g_du_ts[blockIdx.x][4] = (unsigned long long)clock64() - g_du_ts[blockIdx.x][5];
+    } else {
+        tc_fence_before();
+        cluster_sync();  // the pair's MMAs into this CTA's TMEM are done before it is freed
     }
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<2>(tmem_base, 512);
     }
+    if ((args.dbg & 2) && lane == 0 && blockIdx.x < 296) g_du_wend[blockIdx.x][8 + warp] = gtimer();
+    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][1] = gtimer();
 }
 
 }  // namespace dev

@@ -121,8 +121,8 @@ __global__ void __launch_bounds__(256, 1)
     if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    pdl_launch_dependents();
     pdl_wait();
+    pdl_launch_dependents();  // after the wait: a dependent starts only once our predecessor completed
 
     const int num_tiles = args.num_m_tiles * args.num_n_tiles;
     const int cluster_id = blockIdx.x / kCG;

@@ -587,6 +587,11 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         // neither a cooperative launch nor co-residency of all units is needed
         a.cr = 1;
         a.coop = 0;
+        // which == 3 runs right after this backward's dX / P kernel: dU1 may start early
+        static const bool early_on = !(getenv("SKL_DU_EARLY") && atoi(getenv("SKL_DU_EARLY")) == 0);
+        a.early = (early_on && which == 3 && pdl_enabled()) ? 1 : 0;
+        static const int du_dbg_cr = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;
+        a.dbg = du_dbg_cr;  // perf analysis: cycle accounting (bit 0), entry/exit timestamps (bit 1)
         const int S = u.t0 ? u.s0 : u.s1;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * units);
@@ -1165,6 +1170,20 @@ extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
         return -1;
     return n;
 }
+extern "C" int skl_debug_du_ts(unsigned long long* out, int n) {
+    if (n > 296 * 10) n = 296 * 10;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_ts, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
+
+extern "C" int skl_debug_du_wend(unsigned long long* out, int n) {
+    if (n > 296 * 16) n = 296 * 16;
+    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_wend, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
+        return -1;
+    return n;
+}
+
 extern "C" int skl_debug_du_wait(unsigned long long* out, int n) {
     if (n > 296 * 4) n = 296 * 4;
     if (cudaMemcpyFromSymbol(out, skl::dev::g_du_wait, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)

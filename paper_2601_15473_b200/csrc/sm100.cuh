@@ -45,11 +45,19 @@ __device__ __forceinline__ void cluster_sync() {
 // the stream is launched while this one runs; its CTAs take SMs as ours exit,
 // run their prologue (barriers, TMEM, tensor-map prefetch), then pdl_wait()
 // until this grid has completed and its memory is visible.  Without the
-// attribute both are no-ops.
+// attribute both are no-ops.  Every kernel here triggers only AFTER its own
+// wait, so when kernel N+1 starts, every kernel before N has completed: a
+// dependent may read their outputs without waiting (du's early dU1 units).
 __device__ __forceinline__ void pdl_launch_dependents() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned long long gtimer() {  // ns wall clock (debug traces)
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
 
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
@@ -284,6 +292,12 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, const void*
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(map)),
                  "r"(smem_u32(smem)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+// 1-D bulk copy this CTA's smem -> global (bulk group; complete with bulk_wait).
+__device__ __forceinline__ void bulk_store_1d(void* gmem, const void* smem, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(reinterpret_cast<uint64_t>(gmem)),
+                 "r"(smem_u32(smem)), "r"(bytes)
                  : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
