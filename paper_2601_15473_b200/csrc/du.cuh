@@ -408,6 +408,7 @@ __global__ void __launch_bounds__(256, 1)
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
+            if ((args.dbg & 2) && t == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][9] = gtimer();
             lap(e_acc);
             if (args.cr) {
                 // accumulator -> this CTA's smem (the operand ring is idle now); the
@@ -614,6 +615,7 @@ __global__ void __launch_bounds__(256, 1)
             bulk_commit();
             bulk_wait<0>();
             __threadfence();
+            if ((args.dbg & 2) && blockIdx.x < 296) g_du_wend[blockIdx.x][15] = gtimer();
         }
         tc_fence_before();
         cluster_sync();

@@ -588,7 +588,9 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         a.cr = 1;
         a.coop = 0;
         // which == 3 runs right after this backward's dX / P kernel: dU1 may start early
-        static const bool early_on = !(getenv("SKL_DU_EARLY") && atoi(getenv("SKL_DU_EARLY")) == 0);
+        // on the SMs that kernel's last wave leaves idle.  Opt-in (SKL_DU_EARLY=1): only
+        // the clusters that fit there start early and the step time did not move.
+        static const bool early_on = getenv("SKL_DU_EARLY") && atoi(getenv("SKL_DU_EARLY")) != 0;
         a.early = (early_on && which == 3 && pdl_enabled()) ? 1 : 0;
         static const int du_dbg_cr = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;
         a.dbg = du_dbg_cr;  // perf analysis: cycle accounting (bit 0), entry/exit timestamps (bit 1)
