@@ -125,7 +125,7 @@ __device__ unsigned long long g_b2b_ts[296][4];
         }                                                                      \
     } while (0)
 
-template <int kCG, int kMode, int kKind = 0>
+template <int kCG, int kMode, int kKind = 0, bool kMask = false>
 struct B2BCfg {
     // kKind 1 (TF32, fp32 I/O): a k-block is 32 fp32 (still 128 B per row, so
     // every smem tile / descriptor has the bf16 byte geometry); the output
@@ -144,7 +144,13 @@ struct B2BCfg {
     static constexpr bool kBiasTab = kMode == 1 && SKL_FWD_BIAS_TAB;
     static constexpr int kBiasTabBytes = kBiasTab ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
-    static constexpr int kStages0 = kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind;
+    // kMask (backward with a fused ReLU mask): the mask tile of the next output
+    // tile is TMA-loaded into smem one tile ahead (one kOutBytes buffer per
+    // epilogue group); the ring gives up the stages that space takes.
+    static constexpr bool kMaskStage = kMask;
+    static constexpr int kMaskBytes = kMask ? 2 * kOutBytes : 0;
+    static constexpr int kStages0 = (kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind) -
+                                    (kMaskBytes + kStageBytes - 1) / kStageBytes;
     // Split rings (kSplit, experiment, off): the activation tiles of GEMM1 (x /
     // G, from HBM) get their own ring fed by a second producer warp, the
     // L2-resident weight tiles (B1 chunks, B2) the main ring.  Tested because
@@ -171,7 +177,7 @@ struct B2BCfg {
     static constexpr int kKbPerStage2 = kStageMain / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
     static constexpr int kSmem =
-        kRingBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + 1024 /*align*/ + 512;
+        kRingBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + kMaskBytes + 1024 /*align*/ + 512;
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -187,8 +193,9 @@ template <int kCG, int kMode, int kKind, bool kPost>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
-               const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode, kKind>;
+               const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
+               const __grid_constant__ CUtensorMap tmM, B2BArgs args) {
+    using C = B2BCfg<kCG, kMode, kKind, kPost && kMode != 1>;
     if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][0] = gtimer();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -197,7 +204,8 @@ __global__ void __launch_bounds__(384, 1)
     uint8_t* stage_out = smem + C::kRingBytes;                  // 2 x kOutBytes output staging
     float* bias_s = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes);  // 2 slots x 128 bias values
     float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes + 1024);  // kMode 1: bias[N2]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(stage_out + 2 * C::kOutBytes + 1024 + C::kBiasTabBytes);
+    uint8_t* mask_s = stage_out + 2 * C::kOutBytes + 1024 + C::kBiasTabBytes;  // kMask: [2 groups][kOutBytes]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(mask_s + C::kMaskBytes);
     uint64_t* full = bars;                            // [kStages]
     uint64_t* empty = bars + C::kStages;              // [kStages]
     uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
@@ -206,7 +214,8 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* tempty2 = tfull2 + 2;                   // [2] GEMM2 slot drained
     uint64_t* fullA = tempty2 + 2;                    // [kStagesA] (kSplit)
     uint64_t* emptyA = fullA + C::kStagesA;           // [kStagesA]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(emptyA + C::kStagesA);
+    uint64_t* mfull = emptyA + C::kStagesA;           // [2] kMask: this group's mask tile landed
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mfull + 2);
 
     const uint32_t warp = warp_id();
     const uint32_t rank = kCG == 2 ? cluster_ctarank() : 0;
@@ -235,6 +244,9 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&fullA[s], kCG);
             mbar_init(&emptyA[s], 1);
         }
+        mbar_init(&mfull[0], 1);
+        mbar_init(&mfull[1], 1);
+        if constexpr (C::kMaskStage) prefetch_tmap(&tmM);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -473,6 +485,16 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t tf_par0 = 0, tf_par1 = 0;
         const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
         uint8_t* buf = stage_out + wg * C::kOutBytes;  // this group's output staging buffer
+        uint8_t* mbuf = mask_s + wg * C::kOutBytes;    // kMask: this group's mask tile (same layout as buf)
+        uint32_t mph = 0;
+        const bool use_mask = C::kMaskStage && args.mask != nullptr;
+        // mask tile of output tile (t, j) for this group's 64 columns -> mbuf (issuer only)
+        auto issue_mask = [&](int t_, int j_) {
+            const int mn0 = j_ * 128 + 64 * (int)wg, mr0 = t_ * tile_rows + (int)rank * 128;
+            mbar_arrive_expect_tx(&mfull[wg], C::kOutBytes);
+            tma_load_2d<1>(&tmM, &mfull[wg], mbuf, mn0, mr0);
+            if constexpr (kKind == 1) tma_load_2d<1>(&tmM, &mfull[wg], mbuf + 16384, mn0 + 32, mr0);
+        };
         float* bias_g = bias_s + wg * 128;            // [2 slots][64]
         unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SKL_B2B_DEBUG & 32
         const long long te0 = clock64();
@@ -499,6 +521,7 @@ __global__ void __launch_bounds__(384, 1)
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             const int row = t * tile_rows + (int)rank * 128 + (int)srow;
             const bool row_ok = row < args.T;
+            if (use_mask && issuer) issue_mask(t, 0);  // lands during the GEMM1 conversion
             // ---- convert GEMM1 chunks: fp32 -> bf16 H in TMEM (+ saved columns)
             for (int c = 0; c < nch; ++c) {
                 const int wc = min(256, args.R_pad - 256 * c);
@@ -642,12 +665,20 @@ __global__ void __launch_bounds__(384, 1)
                 if (issuer) SKL_TIMED(2, bulk_wait_read<0>());  // our previous store has read `buf`
                 SKL_TIMED(3, named_bar_sync(1 + wg, 128));
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
+                const uint32_t mrow_addr = smem_u32(mbuf) + srow * 128;
                 const long long tm0 = clock64();
-                // 16-B chunk of the ReLU mask (the layer input) for columns [col, col + 16 B)
-                auto mask_chunk = [&](int col) -> uint4 {
-                    if (args.mask == nullptr || !row_ok || col >= args.N2) return make_uint4(0u, 0u, 0u, 0u);
-                    return __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint8_t*>(args.mask) +
-                                                                ((long long)row * args.ld_mask + col) * C::kElem));
+                if (use_mask) {
+                    mbar_wait(&mfull[wg], mph);
+                    mph ^= 1u;
+                }
+                // 16-B chunk of the ReLU mask (the layer input) at staging offset `off`
+                // (the TMA-loaded mask tile has the output tile's layout; OOB is zero)
+                auto mask_chunk = [&](uint32_t off) -> uint4 {
+                    uint4 v;
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                                 : "r"(mrow_addr + off));
+                    return v;
                 };
                 if constexpr (kKind == 1) {
                     // fp32 output: the group's 64 columns are two [128 x 32] fp32 boxes
@@ -664,8 +695,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                             for (int i = 0; i < 4; ++i) v[i] = fmaxf(v[i], 0.f);
                         }
-                        if (kPost && args.mask) {
-                            const uint4 mk = mask_chunk(n0 + 4 * c);
+                        if (use_mask) {
+                            const uint4 mk = mask_chunk((c >> 3) * 16384 + ((uint32_t)((c & 7) ^ (srow & 7)) << 4));
                             const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
 #pragma unroll
                             for (int i = 0; i < 4; ++i) v[i] = __uint_as_float(m[i]) > 0.f ? v[i] : 0.f;
@@ -680,6 +711,7 @@ __global__ void __launch_bounds__(384, 1)
                         tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
                         tma_store_2d(&tmY, buf + 16384, n0 + 32, t * tile_rows + (int)rank * 128);
                         bulk_commit();
+                        if (use_mask && j + 1 < n2_tiles) issue_mask(t, j + 1);  // mbuf was read by all
                     }
                     continue;
                 }
@@ -698,8 +730,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                         for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
                     }
-                    if (kPost && args.mask) {
-                        const uint4 mk = mask_chunk(n0 + 8 * c);
+                    if (use_mask) {
+                        const uint4 mk = mask_chunk((uint32_t)(c ^ (srow & 7)) << 4);
                         const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
 #pragma unroll
                         for (int i = 0; i < 4; ++i) {
@@ -720,6 +752,7 @@ __global__ void __launch_bounds__(384, 1)
                     tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
                     bulk_commit();
                 }
+                if (use_mask && issuer && j + 1 < n2_tiles) issue_mask(t, j + 1);  // mbuf was read by all
             }
         }
         if (issuer) bulk_wait<0>();

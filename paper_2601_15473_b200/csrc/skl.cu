@@ -207,9 +207,9 @@ struct B2BSrc {
 
 template <int kCG, int kMode, int kKind, bool kPost = false>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode, kKind>;
+    using C = dev::B2BCfg<kCG, kMode, kKind, kPost && kMode != 1>;
     constexpr int eb = C::kElem, bk = C::kBK;
-    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty;
+    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
     if constexpr (kMode == 0) {
         SKL_TRY(make_tmap(&tb1, src.b1, eb, a.K1, a.R_pad, a.K1, bk, a.b1rows));
@@ -234,6 +234,8 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.k, srows, a.k, 64, C::kB2Rows));
     }
     SKL_TRY(make_tmap(&ty, a.out, eb, a.N2, a.T, a.ldo, bk, 128));
+    tm = ty;
+    if (C::kMaskStage && a.mask) SKL_TRY(make_tmap(&tm, a.mask, eb, a.N2, a.T, a.ld_mask, bk, 128));  // output-tile boxes
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     static const int grid_cap = [] {  // SKL_B2B_GRID: cap on CTAs (experiments)
         const char* e = getenv("SKL_B2B_GRID");
@@ -262,7 +264,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     add_pdl(attr, nattr);
     cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, a));
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, tm, a));
     return SKL_OK;
 }
 
@@ -464,8 +466,11 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     static const double kW1 = getenv("SKL_DU_W1") ? atof(getenv("SKL_DU_W1")) : 1.0;
     double best = 1e30;
     s.s0 = s.s1 = 1;
-    for (int a = (s.t0 ? 1 : 0); a <= (s.t0 ? smax : 0); ++a)
-        for (int b = (s.t1 ? 1 : 0); b <= (s.t1 ? smax : 0); ++b) {
+    // one wave: a <= pairs / t0 and b <= pairs / t1 (the search is on every call's host path)
+    const int amax = s.t0 ? std::max(1, std::min(smax, pairs / s.t0)) : 0;
+    const int bmax = s.t1 ? std::max(1, std::min(smax, pairs / s.t1)) : 0;
+    for (int a = (s.t0 ? 1 : 0); a <= amax; ++a)
+        for (int b = (s.t1 ? 1 : 0); b <= bmax; ++b) {
             if (s.t0 * a + s.t1 * b > pairs && (a > 1 || b > 1)) continue;
             const double len = std::max(a ? std::ceil((double)s.kb / a) : 0.0,
                                         b ? std::ceil((double)s.kb / b) * kW1 : 0.0);
