@@ -347,6 +347,40 @@ def test_chain_with_fused_relu_matches_oracle(skl, port, dtype_name):
         check_close(f"chain db[{i}]", _np(b.db), db, dtype_name)
 
 
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("unfused", [False, True])
+def test_fused_relu_mask_is_exact_at_scale(skl, dtype_name, unfused):
+    """The backward's fused ReLU mask (FUSE_RELU_IN, Relu::backward nn_layers.cpp:347-354)
+    equals the plain backward's grad_x times (x > 0), bitwise, at a size where
+    every CTA runs several output tiles and more than one row tile (the mask
+    tiles are prefetched one tile ahead), with ragged T and N2 % 128 != 0."""
+    if unfused and os.environ.get("SKL_FORCE_UNFUSED") is None:
+        pytest.skip("unfused path is exercised in a separate process (SKL_FORCE_UNFUSED=1)")
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    d_in, d_out, L, k, T = 1088, 512, 2, 64, 20003
+    lyr = skl.SkLinear(d_in, d_out, L, k, seed=77, dtype=dtype)
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(T, d_in, device="cuda", generator=gen).to(td)
+    g = torch.randn(T, d_out, device="cuda", generator=gen).to(td)
+    s = lyr.shape
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    out = []
+    for fuse in (0, skl.FUSE_RELU_IN):
+        gx = torch.empty(T, d_in, dtype=td, device="cuda")
+        du1 = torch.empty(L, k, d_out, device="cuda")
+        du2 = torch.empty(L, d_in, k, device="cuda")
+        db = torch.empty(d_out, device="cuda")
+        skl.backward_phase(s, skl.BWD_ALL, g, x, None, lyr.S1s, lyr.S2s, lyr.U1s, lyr.U2s, gx, du1, du2, db, ws,
+                           fuse=fuse)
+        out.append((gx, du1, du2, db))
+    torch.cuda.synchronize()
+    plain, fused = out
+    assert torch.equal(fused[0], plain[0] * (x > 0).to(td))
+    for a, b in zip(fused[1:], plain[1:]):
+        assert torch.equal(a, b)
+
+
 def test_bert_stack_overlapped_dp_step_runs(skl):
     """Config 5 at reduced depth: the BERT FFN/proj stack with the phased,
     per-layer all-reduce schedule on a world-1 NCCL group gives the same
@@ -534,3 +568,19 @@ def test_full_size_c2_properties(skl, dtype_name):
     for u, v in zip((full.grad_x, full.grad_u1, full.grad_u2, full.grad_b),
                     (again.grad_x, again.grad_u1, again.grad_u2, again.grad_b)):
         assert torch.equal(u, v)
+
+
+def test_unfused_path_parity_in_subprocess():
+    """Every parity test above once more with SKL_FORCE_UNFUSED=1 (the env switch is
+    read once per process): the unfused GEMM chain -- the path for R > 512 --
+    against the same oracle gates."""
+    import subprocess
+    import sys
+    if os.environ.get("SKL_FORCE_UNFUSED") is not None:
+        pytest.skip("already the unfused process")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKL_FORCE_UNFUSED="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu.py", "-k",
+                        "parity or mask_is_exact or chain or edge or deterministic"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
