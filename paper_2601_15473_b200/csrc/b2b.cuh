@@ -270,6 +270,11 @@ __global__ void __launch_bounds__(384, 1)
     const int nkb2 = args.R_pad / C::kBK;
     const int nst2 = (nkb2 + C::kKbPerStage2 - 1) / C::kKbPerStage2;
     const int n2_tiles = (args.N2 + 127) / 128;
+    // Ping-pong H (R_pad <= 128): tile t's H lives in TMEM region (t & 1) * 128, so
+    // GEMM1 of the next tile is issued BEFORE GEMM2 of this one and its HBM reads
+    // overlap this tile's output drain (the epilogue's stores) instead of
+    // alternating with it.  Producer, MMA issuer and epilogue all follow this order.
+    const bool pp = !C::kSplit && nch == 1 && args.R_pad <= 128 && !(args.dbg & 256);
 
     if (warp == 0) {
         // ---------------------------------------------------------------- producer
@@ -279,7 +284,7 @@ __global__ void __launch_bounds__(384, 1)
             unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const long long tp0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
-            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+            auto load_g1 = [&](int t) {
                 const int am = t * tile_rows + (int)rank * 128;
                 // GEMM1 passes: one per chunk, or (single-pass mode) one pass that
                 // feeds every chunk from the same A1 stage -> A1 is read once.
@@ -322,6 +327,8 @@ __global__ void __launch_bounds__(384, 1)
                         next();
                     }
                 }
+            };
+            auto load_g2 = [&]() {
                 for (int j = 0; j < n2_tiles; ++j) {
                     const int brow = j * 128 + (int)rank * C::kB2Rows;
                     for (int s = 0; s < nst2; ++s) {
@@ -358,6 +365,12 @@ __global__ void __launch_bounds__(384, 1)
                         next();
                     }
                 }
+            };
+            if (pp && cluster_id < num_tiles) load_g1(cluster_id);
+            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+                if (!pp) load_g1(t);
+                else if (t + num_clusters < num_tiles) load_g1(t + num_clusters);
+                load_g2();
             }
             if (args.dbg & 32) {
                 prof[7] = (unsigned long long)(clock64() - tp0);
@@ -396,7 +409,7 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t slot_seq = 0;
             const uint32_t idesc2 = make_idesc(kKind, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
             int it = 0;
-            for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+            auto issue_g1 = [&](uint32_t hoff, int r) {  // hoff: TMEM column of this tile's H (ping-pong)
                 // ---- GEMM1: H chunks (one pass per chunk, or one pass for all)
                 const int npass = C::kSinglePassG1 ? 1 : nch;
                 for (int pass = 0; pass < npass; ++pass) {
@@ -415,7 +428,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int c = c_lo; c < c_hi; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
                             const uint32_t idesc1 = make_idesc(kKind, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
-                            const uint32_t d = tmem_base + 256 * c;
+                            const uint32_t d = tmem_base + 256 * c + hoff;
                             const uint32_t b_addr = w_addr + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
@@ -431,11 +444,10 @@ __global__ void __launch_bounds__(384, 1)
                             if (++sa == C::kStagesA) { sa = 0; pa ^= 1; }
                         }
                     }
-                    for (int c = c_lo; c < c_hi; ++c) mma_commit<kCG>(&tfull1[c]);
+                    for (int c = c_lo; c < c_hi; ++c) mma_commit<kCG>(&tfull1[pp ? r : c]);
                 }
-                // ---- wait for the bf16 H of this tile (both CTAs)
-                for (int c = 0; c < nch; ++c) SKL_TIMED(3, mbar_wait(&hready[c], it & 1));
-                tc_fence_after();
+            };
+            auto issue_g2 = [&](uint32_t hoff) {
                 // ---- GEMM2: 128-wide output tiles, A = H from TMEM
                 for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                     const uint32_t s = slot_seq & 1;
@@ -452,7 +464,7 @@ __global__ void __launch_bounds__(384, 1)
                             if (args.dbg & 4) break;  // perf bisection: skip GEMM2 MMAs
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
-                                const uint32_t a_t = tmem_base + (uint32_t)((kb0 + q) * 32 + k * 8);
+                                const uint32_t a_t = tmem_base + hoff + (uint32_t)((kb0 + q) * 32 + k * 8);
                                 const uint64_t bdesc = kMode == 1
                                     ? make_sdesc(b_addr + q * C::kB2KbBytes + k * 2048, 8192, 1024)
                                     : make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024);
@@ -464,6 +476,16 @@ __global__ void __launch_bounds__(384, 1)
                     }
                     mma_commit<kCG>(&tfull2[s]);
                 }
+            };
+            if (pp && cluster_id < num_tiles) issue_g1(0, 0);
+            for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+                if (!pp) issue_g1(0, 0);
+                else if (t + num_clusters < num_tiles) issue_g1(128u * ((it + 1) & 1), (it + 1) & 1);
+                // ---- wait for the bf16 H of this tile (both CTAs)
+                if (pp) SKL_TIMED(3, mbar_wait(&hready[it & 1], (it >> 1) & 1));
+                else for (int c = 0; c < nch; ++c) SKL_TIMED(3, mbar_wait(&hready[c], it & 1));
+                tc_fence_after();
+                issue_g2(pp ? 128u * (it & 1) : 0u);
             }
             if (args.dbg & 32) {
                 prof[4] = (unsigned long long)(clock64() - tm0);
@@ -531,7 +553,9 @@ __global__ void __launch_bounds__(384, 1)
                 // 0/1, so round 0 reads Q0,Q1 before anyone writes (barrier), and
                 // round 1's writes only hit Q1, which round 0 already consumed.
                 const int W = wc / 4;
-                SKL_TIMED(4, mbar_wait(&tfull1[c], it & 1));
+                const int hb = pp ? (int)(it & 1) : c;            // tfull1 / hready index
+                const uint32_t hoff = pp ? 128u * (it & 1) : 0u;  // TMEM column of this tile's H
+                SKL_TIMED(4, mbar_wait(&tfull1[hb], pp ? ((it >> 1) & 1) : (it & 1)));
                 tc_fence_after();
                 const long long tc0 = clock64();
                 if constexpr (kKind == 1) {
@@ -540,15 +564,15 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
                     for (int cl = (int)wg * (wc / 2); cl < ((int)wg + 1) * (wc / 2); cl += 16) {
                         uint32_t r[16];
-                        tmem_ld16(tmem_base + lane_base + 256 * c + cl, r);
+                        tmem_ld16(tmem_base + lane_base + hoff + 256 * c + cl, r);
                         tmem_ld_wait();
 #pragma unroll
                         for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(tf32_rna(__uint_as_float(r[i])));
                         uint32_t lo[8], hi[8];
 #pragma unroll
                         for (int i = 0; i < 8; ++i) { lo[i] = r[i]; hi[i] = r[8 + i]; }
-                        tmem_st8(tmem_base + lane_base + 256 * c + cl, lo);
-                        tmem_st8(tmem_base + lane_base + 256 * c + cl + 8, hi);
+                        tmem_st8(tmem_base + lane_base + hoff + 256 * c + cl, lo);
+                        tmem_st8(tmem_base + lane_base + hoff + 256 * c + cl + 8, hi);
                         const int col = 256 * c + cl;
                         if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
                             float* dst = reinterpret_cast<float*>(args.save) + row;
@@ -569,7 +593,7 @@ __global__ void __launch_bounds__(384, 1)
                     uint32_t rr[4][16];
 #pragma unroll
                     for (int g = 0; g < 4; ++g)
-                        if (16 * g < W) tmem_ld16(tmem_base + lane_base + 256 * c + qi * W + 16 * g, rr[g]);
+                        if (16 * g < W) tmem_ld16(tmem_base + lane_base + hoff + 256 * c + qi * W + 16 * g, rr[g]);
                     tmem_ld_wait();
                     if (rd == 0) {
                         tc_fence_before();
@@ -585,7 +609,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int i = 0; i < 8; ++i)
                             p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
                         const int cl = qi * W + 16 * g;  // chunk-local fp32 column
-                        tmem_st8(tmem_base + lane_base + 128 * c + cl / 2, p);
+                        tmem_st8(tmem_base + lane_base + hoff + 128 * c + cl / 2, p);
                         const int col = 256 * c + cl;  // H column (R order)
                         // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
                         // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
@@ -620,7 +644,7 @@ __global__ void __launch_bounds__(384, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
-                    arrive_leader(&hready[c]);
+                    arrive_leader(&hready[hb]);
                     if (c == 1) {  // release the two slots chunk 1 overlaid
                         arrive_leader(&tempty2[slot_seq & 1]);
                         arrive_leader(&tempty2[(slot_seq + 1) & 1]);

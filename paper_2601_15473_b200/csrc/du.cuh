@@ -97,9 +97,10 @@ struct DuTail {
     const float* c0;   // split-0 column sums of this rank; splits 256 apart
     long long mbs, ms, ns;
     int mb, M, N, m0, n0, r0, rows, S, colsum, vec;
+    int valid;         // rows of this CTA's 128-row half inside M (only those move)
     float alpha;
 };
-static_assert(132 * kDuBN * 4 + 4 * 512 <= kDuStages * kDuStageBytes, "cluster-reduce staging exceeds the ring");
+static_assert(136 * kDuBN * 4 + 8 * 512 <= kDuStages * kDuStageBytes, "cluster-reduce staging exceeds the ring");
 
 template <int kKind>
 __global__ void __launch_bounds__(256, 1)
@@ -213,6 +214,7 @@ __global__ void __launch_bounds__(256, 1)
         d.N = P.N;
         d.r0 = x.split * 128 / x.nsplit;
         d.rows = (x.split + 1) * 128 / x.nsplit - d.r0;
+        d.valid = min(128, max(0, P.M - (x.mt * 256 + (int)rank * 128)));
         d.m0 = x.mt * 256 + (int)rank * 128 + d.r0;
         d.n0 = x.nt * 256;
         d.S = x.nsplit;
@@ -611,7 +613,9 @@ __global__ void __launch_bounds__(256, 1)
         __syncthreads();
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();  // the dump was written by generic stores
-            bulk_store_1d(args.part + ((long long)pair * 2 + rank) * 128 * kDuBN, cr_part, 128 * kDuBN * 4);
+            if (tail->valid > 0)
+                bulk_store_1d(args.part + ((long long)pair * 2 + rank) * 128 * kDuBN, cr_part,
+                              (uint32_t)tail->valid * kDuBN * 4);
             bulk_commit();
             bulk_wait<0>();
             __threadfence();
@@ -625,14 +629,15 @@ __global__ void __launch_bounds__(256, 1)
             g_du_ts[blockIdx.x][5] = (unsigned long long)clock64();
         }
         const DuTail d = *tail;  // registers: the output stores must not force reloads
-        const int S = d.S, rows = d.rows;
-        float* cs = cr_part + 132 * kDuBN;  // past S * ceil(128 / S) <= 131 slice rows
+        const int S = d.S, rows = max(0, min(d.rows, d.valid - d.r0));  // slice rows inside M
+        float* cs = cr_part + 136 * kDuBN;  // past S * ceil(128 / S) <= 135 slice rows (S <= 8)
         if (threadIdx.x == 0) {
             fence_proxy_async_global();  // order the acquired view before the bulk reads
             mbar_arrive_expect_tx(rbar, (uint32_t)(S * rows * kDuBN * 4 + (d.colsum ? S * 512 : 0)));
             for (int q2 = 0; q2 < S; ++q2) {
-                bulk_load_1d(cr_part + q2 * rows * kDuBN, d.g0 + ((long long)q2 * 256 + d.r0) * kDuBN,
-                             (uint32_t)rows * kDuBN * 4, rbar);
+                if (rows > 0)
+                    bulk_load_1d(cr_part + q2 * rows * kDuBN, d.g0 + ((long long)q2 * 256 + d.r0) * kDuBN,
+                                 (uint32_t)rows * kDuBN * 4, rbar);
                 if (d.colsum) bulk_load_1d(cs + q2 * 128, d.c0 + q2 * kDuBN, 512, rbar);
             }
         }
@@ -689,7 +694,7 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         if (d.colsum) {
-            for (int c = d.r0 + (int)threadIdx.x; c < d.r0 + rows; c += 256) {
+            for (int c = d.r0 + (int)threadIdx.x; c < d.r0 + d.rows; c += 256) {  // columns: not clamped by M
                 const int n = d.n0 + (int)rank * 128 + c;
                 if (n >= d.N) continue;
                 float sum = cs[c];

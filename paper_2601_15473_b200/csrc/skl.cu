@@ -488,7 +488,8 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     // cluster of at most 8 CTAs.  Otherwise partials go through global memory.
     static const bool cr_on = !(getenv("SKL_DU_CR") && atoi(getenv("SKL_DU_CR")) == 0);
     const int sc = s.t0 ? s.s0 : s.s1;
-    s.cr = cr_on && sc <= 4 && (!s.t0 || !s.t1 || s.s0 == s.s1);
+    static const int cr_max = getenv("SKL_DU_CR_MAX") ? atoi(getenv("SKL_DU_CR_MAX")) : 4;  // 8: clusters of 16
+    s.cr = cr_on && sc <= std::min(cr_max, 8) && (!s.t0 || !s.t1 || s.s0 == s.s1);
     return s;
 }
 
@@ -583,6 +584,7 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     static bool attr_set[2] = {false, false};
     if (!attr_set[kind]) {
         SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
+        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));  // 2S up to 16
         attr_set[kind] = true;
     }
     const int units = u.units;  // CTA-pair work units
