@@ -38,9 +38,11 @@ ABI_SYMBOLS = (
     "skl_profile_enable", "skl_profile_collect", "sketched_linear_backward_phase", "skl_set_reserved_sms",
     "sketched_linear_forward_ex", "sketched_linear_backward_ex", "skl_from_dense", "skl_from_dense_workspace_size",
     "skl_conv_workspace_size", "sketched_conv2d_forward", "sketched_conv2d_backward",
+    "sketched_linear_forward_bits", "sketched_linear_backward_bits", "skl_relu_bits_row_words",
+    "skl_relu_bits_supported",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
-FUSE_RELU_OUT, FUSE_RELU_IN = 1, 2
+FUSE_RELU_OUT, FUSE_RELU_IN, FUSE_RELU_BITS = 1, 2, 4
 
 
 class SklError(RuntimeError):
@@ -123,6 +125,10 @@ def lib() -> ctypes.CDLL:
     L.skl_from_dense.argtypes = [sp, ctypes.c_int, u64] + [vp] * 8 + [sz, vp]
     L.sketched_linear_forward_ex.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 9 + [sz, vp]
     L.sketched_linear_backward_ex.argtypes = [sp, i64, ctypes.c_uint, ctypes.c_uint] + [vp] * 12 + [sz, vp]
+    L.sketched_linear_forward_bits.argtypes = [sp, i64, ctypes.c_uint] + [vp] * 10 + [sz, vp]
+    L.sketched_linear_backward_bits.argtypes = [sp, i64, ctypes.c_uint, ctypes.c_uint] + [vp] * 13 + [sz, vp]
+    L.skl_relu_bits_row_words.argtypes = [i64]
+    L.skl_relu_bits_supported.argtypes = [sp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
     L.skl_launch_count.restype = u64
     L.skl_profile_enable.argtypes = [ctypes.c_int]
@@ -131,8 +137,9 @@ def lib() -> ctypes.CDLL:
     L.skl_profile_collect.restype = ctypes.c_int
     for name in ABI_SYMBOLS:
         if name not in ("skl_version", "skl_last_error", "skl_rng_algorithm", "skl_derive_seed",
-                        "skl_exceeds_dense", "skl_launch_count"):
+                        "skl_exceeds_dense", "skl_launch_count", "skl_relu_bits_row_words"):
             getattr(L, name).restype = ctypes.c_int
+    L.skl_relu_bits_row_words.restype = i64
     _lib = L
     return L
 
@@ -204,12 +211,29 @@ def init_params(s: _Shape, seed, U1s, U2s, stream=None):
     _check(lib().skl_init_params(ctypes.byref(s), seed, _ptr(U1s), _ptr(U2s), _stream(stream)))
 
 
-def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None, fuse=0):
-    """sketched_linear_forward(_ex): fuse = FUSE_RELU_OUT applies the following ReLU."""
+def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None, fuse=0, relu_bits=None):
+    """sketched_linear_forward(_ex/_bits): fuse = FUSE_RELU_OUT applies the following ReLU;
+    with relu_bits (int32 [T, relu_bits_row_words(d_out)]) it also writes the 1-bit ReLU mask."""
     T = x.shape[0]
+    if relu_bits is not None:
+        _check(lib().sketched_linear_forward_bits(ctypes.byref(s), T, fuse | FUSE_RELU_BITS, _ptr(x), _ptr(S1s),
+                                                  _ptr(S2s), _ptr(U1s), _ptr(U2s), _ptr(bias), _ptr(y), _ptr(saved),
+                                                  _ptr(relu_bits), _ptr(workspace),
+                                                  workspace.numel() if workspace is not None else 0, _stream(stream)))
+        return
     _check(lib().sketched_linear_forward_ex(ctypes.byref(s), T, fuse, _ptr(x), _ptr(S1s), _ptr(S2s), _ptr(U1s),
                                             _ptr(U2s), _ptr(bias), _ptr(y), _ptr(saved), _ptr(workspace),
                                             workspace.numel() if workspace is not None else 0, _stream(stream)))
+
+
+def relu_bits_row_words(width: int) -> int:
+    """skl_relu_bits_row_words: int32 words per token of a 1-bit ReLU mask of `width` columns."""
+    return int(lib().skl_relu_bits_row_words(int(width)))
+
+
+def relu_bits_supported(s: _Shape) -> bool:
+    """skl_relu_bits_supported: whether this shape's kernels take 1-bit ReLU masks."""
+    return bool(lib().skl_relu_bits_supported(ctypes.byref(s)))
 
 
 def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace, stream=None):
@@ -221,10 +245,18 @@ def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db,
 
 
 def backward_phase(s: _Shape, phases, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace,
-                   stream=None, fuse=0):
-    """sketched_linear_backward_ex: phases BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s) / BWD_ALL;
-    fuse = FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward)."""
+                   stream=None, fuse=0, relu_bits=None):
+    """sketched_linear_backward_ex/_bits: phases BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s) / BWD_ALL;
+    fuse = FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward), read from
+    relu_bits (the previous layer's 1-bit mask) when given."""
     T = x.shape[0]
+    if relu_bits is not None:
+        _check(lib().sketched_linear_backward_bits(ctypes.byref(s), T, phases, fuse | FUSE_RELU_BITS, _ptr(g), _ptr(x),
+                                                   _ptr(saved), _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s),
+                                                   _ptr(grad_x), _ptr(dU1s), _ptr(dU2s), _ptr(db), _ptr(relu_bits),
+                                                   _ptr(workspace), workspace.numel() if workspace is not None else 0,
+                                                   _stream(stream)))
+        return
     _check(lib().sketched_linear_backward_ex(ctypes.byref(s), T, phases, fuse, _ptr(g), _ptr(x), _ptr(saved),
                                              _ptr(S1s), _ptr(S2s), _ptr(U1s), _ptr(U2s), _ptr(grad_x),
                                              _ptr(dU1s), _ptr(dU2s), _ptr(db), _ptr(workspace),

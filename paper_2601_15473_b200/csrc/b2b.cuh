@@ -64,6 +64,10 @@ struct B2BArgs {
     const void* mask;   // backward: out *= (mask > 0), mask = the layer input [T, N2] that a ReLU
                         // produced (Relu::backward, nn_layers.cpp:347-354); nullable
     long long ld_mask;
+    // 1-bit ReLU masks (kPost == 2): bit (c % 32) of word [t * bits_ld + c / 32] is (out[t][c] > 0).
+    uint32_t* relu_bits;         // forward with relu: written alongside out
+    const uint32_t* mask_bits;   // backward: out *= bit, instead of reading `mask`
+    long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
 };
 
 namespace dev {
@@ -187,15 +191,16 @@ struct B2BCfg {
 //          [L*k][d_out] (MN-major tiles).  No packing pass.
 // kMode 2: backward straight from the stacks: B1 = U1s|S2s [L*k][d_out]
 //          (K-major), B2 = S1s|U2s [L*d_in][k] (K-major, per-term row offset).
-// kPost: the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
-// mask); a separate instantiation so the plain layer keeps its register budget.
-template <int kCG, int kMode, int kKind, bool kPost>
+// kPost: 1 = the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
+// mask), 2 = the same with 1-bit masks (relu_bits / mask_bits); separate
+// instantiations so the plain layer keeps its register budget.
+template <int kCG, int kMode, int kKind, int kPost>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
                const __grid_constant__ CUtensorMap tmM, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode, kKind, kPost && kMode != 1>;
+    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1>;
     if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][0] = gtimer();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -510,6 +515,9 @@ __global__ void __launch_bounds__(384, 1)
         uint8_t* mbuf = mask_s + wg * C::kOutBytes;    // kMask: this group's mask tile (same layout as buf)
         uint32_t mph = 0;
         const bool use_mask = C::kMaskStage && args.mask != nullptr;
+        const bool use_bits_in = kPost == 2 && args.mask_bits != nullptr;
+        const bool use_bits_out = kPost == 2 && args.relu_bits != nullptr;
+        uint2 mbits = make_uint2(0u, 0u), mbits_next = make_uint2(0u, 0u);
         // mask tile of output tile (t, j) for this group's 64 columns -> mbuf (issuer only)
         auto issue_mask = [&](int t_, int j_) {
             const int mn0 = j_ * 128 + 64 * (int)wg, mr0 = t_ * tile_rows + (int)rank * 128;
@@ -544,6 +552,13 @@ __global__ void __launch_bounds__(384, 1)
             const int row = t * tile_rows + (int)rank * 128 + (int)srow;
             const bool row_ok = row < args.T;
             if (use_mask && issuer) issue_mask(t, 0);  // lands during the GEMM1 conversion
+            // this row's mask bits of output tile jj, this group's 64 columns (one 8-B load)
+            auto load_bits = [&](int jj) -> uint2 {
+                const int col = jj * 128 + 64 * (int)wg;
+                if (!row_ok || col >= args.N2) return make_uint2(0u, 0u);
+                return __ldg(reinterpret_cast<const uint2*>(args.mask_bits + (long long)row * args.bits_ld + col / 32));
+            };
+            if (use_bits_in) mbits_next = load_bits(0);
             // ---- convert GEMM1 chunks: fp32 -> bf16 H in TMEM (+ saved columns)
             for (int c = 0; c < nch; ++c) {
                 const int wc = min(256, args.R_pad - 256 * c);
@@ -686,6 +701,11 @@ __global__ void __launch_bounds__(384, 1)
                 if (lane == 0) arrive_leader(&tempty2[s]);
                 if (args.dbg & 16) continue;  // perf bisection: TMEM reads only
                 const int n0 = j * 128 + 64 * (int)wg;
+                if (use_bits_in) {  // this tile's bits were loaded one tile ago; fetch the next tile's
+                    mbits = mbits_next;
+                    if (j + 1 < n2_tiles) mbits_next = load_bits(j + 1);
+                }
+                uint32_t bo0 = 0u, bo1 = 0u;  // use_bits_out: this row's bits of the group's 64 columns
                 if (issuer) SKL_TIMED(2, bulk_wait_read<0>());  // our previous store has read `buf`
                 SKL_TIMED(3, named_bar_sync(1 + wg, 128));
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
@@ -719,6 +739,20 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                             for (int i = 0; i < 4; ++i) v[i] = fmaxf(v[i], 0.f);
                         }
+                        if (kPost == 2) {
+                            const int sh = 4 * (c & 7);
+                            if (use_bits_in) {
+                                const uint32_t b4 = ((c < 8 ? mbits.x : mbits.y) >> sh) & 0xFu;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) v[i] = ((b4 >> i) & 1u) ? v[i] : 0.f;
+                            }
+                            if (use_bits_out) {
+                                uint32_t b4 = 0u;
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) b4 |= (v[i] > 0.f ? 1u : 0u) << i;
+                                if (c < 8) bo0 |= b4 << sh; else bo1 |= b4 << sh;
+                            }
+                        }
                         if (use_mask) {
                             const uint4 mk = mask_chunk((c >> 3) * 16384 + ((uint32_t)((c & 7) ^ (srow & 7)) << 4));
                             const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
@@ -729,6 +763,9 @@ __global__ void __launch_bounds__(384, 1)
                                      __float_as_uint(v[0]), __float_as_uint(v[1]), __float_as_uint(v[2]),
                                      __float_as_uint(v[3]));
                     }
+                    if (use_bits_out && row_ok && n0 < args.N2)
+                        *reinterpret_cast<uint2*>(args.relu_bits + (long long)row * args.bits_ld + n0 / 32) =
+                            make_uint2(bo0, bo1);
                     fence_proxy_async_smem();
                     named_bar_sync(1 + wg, 128);
                     if (issuer) {
@@ -754,6 +791,20 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll
                         for (int i = 0; i < 8; ++i) v[i] = fmaxf(v[i], 0.f);
                     }
+                    if (kPost == 2) {
+                        const int sh = 8 * (c & 3);
+                        if (use_bits_in) {
+                            const uint32_t b8 = ((c < 4 ? mbits.x : mbits.y) >> sh) & 0xFFu;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) v[i] = ((b8 >> i) & 1u) ? v[i] : 0.f;
+                        }
+                        if (use_bits_out) {
+                            uint32_t b8 = 0u;
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) b8 |= (v[i] > 0.f ? 1u : 0u) << i;
+                            if (c < 4) bo0 |= b8 << sh; else bo1 |= b8 << sh;
+                        }
+                    }
                     if (use_mask) {
                         const uint4 mk = mask_chunk((uint32_t)(c ^ (srow & 7)) << 4);
                         const uint32_t m[4] = {mk.x, mk.y, mk.z, mk.w};
@@ -769,6 +820,9 @@ __global__ void __launch_bounds__(384, 1)
                     for (int i = 0; i < 4; ++i) w[i] = pack_bf16x2(v[2 * i], v[2 * i + 1]);
                     st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
                 }
+                if (use_bits_out && row_ok && n0 < args.N2)
+                    *reinterpret_cast<uint2*>(args.relu_bits + (long long)row * args.bits_ld + n0 / 32) =
+                        make_uint2(bo0, bo1);
                 fence_proxy_async_smem();
                 if (args.dbg & 32) prof[1] += (unsigned long long)(clock64() - tm0);
                 named_bar_sync(1 + wg, 128);

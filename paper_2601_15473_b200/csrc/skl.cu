@@ -205,9 +205,9 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode, int kKind, bool kPost = false>
+template <int kCG, int kMode, int kKind, int kPost = 0>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode, kKind, kPost && kMode != 1>;
+    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1>;
     constexpr int eb = C::kElem, bk = C::kBK;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
@@ -331,12 +331,19 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         if (a.K1 >= 2048) return run_b2b_tf32_wide<true>(name, src, a, sms, st);
         return run_b2b_tf32_wide<false>(name, src, a, sms, st);
     }
+    if (a.relu_bits || a.mask_bits) {  // fused ReLU with 1-bit masks
+        if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "fused ReLU needs the CTA-pair kernel (SKL_B2B_CG=2)");
+        if (kind == 1) return run_b2b_cg<2, 0, 1, 2>(name, src, a, sms, st);
+        if (mode == 1) return run_b2b_cg<2, 1, 0, 2>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2, 0, 2>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0, 0, 2>(name, src, a, sms, st);
+    }
     if (a.relu || a.mask) {  // fused ReLU / ReLU-mask epilogue (CTA pairs only)
         if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "fused ReLU needs the CTA-pair kernel (SKL_B2B_CG=2)");
-        if (kind == 1) return run_b2b_cg<2, 0, 1, true>(name, src, a, sms, st);
-        if (mode == 1) return run_b2b_cg<2, 1, 0, true>(name, src, a, sms, st);
-        if (mode == 2) return run_b2b_cg<2, 2, 0, true>(name, src, a, sms, st);
-        return run_b2b_cg<2, 0, 0, true>(name, src, a, sms, st);
+        if (kind == 1) return run_b2b_cg<2, 0, 1, 1>(name, src, a, sms, st);
+        if (mode == 1) return run_b2b_cg<2, 1, 0, 1>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2, 0, 1>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0, 0, 1>(name, src, a, sms, st);
     }
     if (kind == 1) {
         if (g_b2b_cg == 2) return run_b2b_cg<2, 0, 1>(name, src, a, sms, st);
@@ -422,6 +429,14 @@ bool use_fused(const SklDims& d, skl_dtype t) {
     if (force_unfused) return false;
     if (t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad)) return g_b2b_cg == 2;
     return b2b_supported(d.R_pad, t == SKL_BF16 ? 0 : 1);
+}
+
+// 1-bit ReLU masks are implemented in the CTA-pair b2b kernel only (not in the
+// wide-rank TF32 kernel or the unfused GEMM chain).
+bool relu_bits_ok(const SklDims& d, skl_dtype t) {
+    static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
+    if (!use_fused(d, t) || g_b2b_cg != 2) return false;
+    return !(t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad));
 }
 
 struct Plan {
@@ -739,8 +754,31 @@ skl_status sketched_linear_forward_ex(const skl_shape* s, int64_t T, unsigned fu
                                       const void* S2s, const void* U1s, const void* U2s, const void* bias, void* y,
                                       void* saved_proj, void* workspace, size_t ws_bytes, void* stream) {
     if (fuse & ~(unsigned)SKL_FUSE_RELU_OUT) return fail(SKL_ERR_PARAM, "forward: unsupported fuse flags %u", fuse);
+    return sketched_linear_forward_bits(s, T, fuse, x, S1s, S2s, U1s, U2s, bias, y, saved_proj, nullptr, workspace,
+                                        ws_bytes, stream);
+}
+
+int64_t skl_relu_bits_row_words(int64_t width) { return width < 1 ? 0 : (width + 63) / 64 * 2; }
+
+int skl_relu_bits_supported(const skl_shape* s) {
+    SklDims d;
+    if (get_dims(s, d) != SKL_OK) return 0;
+    return relu_bits_ok(d, s->dtype) ? 1 : 0;
+}
+
+skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned fuse, const void* x, const void* S1s,
+                                        const void* S2s, const void* U1s, const void* U2s, const void* bias, void* y,
+                                        void* saved_proj, uint32_t* relu_bits, void* workspace, size_t ws_bytes,
+                                        void* stream) {
+    if (fuse & ~(unsigned)(SKL_FUSE_RELU_OUT | SKL_FUSE_RELU_BITS))
+        return fail(SKL_ERR_PARAM, "forward: unsupported fuse flags %u", fuse);
+    const bool bits = (fuse & SKL_FUSE_RELU_BITS) != 0;
+    if (bits && (!(fuse & SKL_FUSE_RELU_OUT) || !relu_bits))
+        return fail(SKL_ERR_PARAM, "forward: SKL_FUSE_RELU_BITS needs SKL_FUSE_RELU_OUT and a relu_bits buffer");
     SklDims d;
     SKL_TRY(get_dims(s, d));
+    if (bits && !relu_bits_ok(d, s->dtype))
+        return fail(SKL_ERR_UNSUPPORTED, "forward: 1-bit ReLU masks need the fused CTA-pair kernel for this shape");
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::forward: T must be >= 0");
     if (T == 0) return SKL_OK;
     if (!x || !S1s || !S2s || !U1s || !U2s || !y) return fail(SKL_ERR_PARAM, "null tensor argument");
@@ -770,6 +808,8 @@ skl_status sketched_linear_forward_ex(const skl_shape* s, int64_t T, unsigned fu
         a.N2 = (int)d.d_out;
         a.alpha = inv;
         a.relu = (fuse & SKL_FUSE_RELU_OUT) ? 1 : 0;
+        a.relu_bits = bits ? relu_bits : nullptr;
+        a.bits_ld = skl_relu_bits_row_words(d.d_out);
         a.bias = direct ? reinterpret_cast<const float*>(bias) : bias32;
         a.bias_bf16 = direct ? 1 : 0;
         a.out = y;
@@ -835,8 +875,24 @@ skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned p
                                        float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
                                        size_t ws_bytes, void* stream) {
     if (fuse & ~(unsigned)SKL_FUSE_RELU_IN) return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
+    return sketched_linear_backward_bits(s, T, phases, fuse, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x,
+                                         grad_U1s, grad_U2s, grad_bias, nullptr, workspace, ws_bytes, stream);
+}
+
+skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned phases, unsigned fuse,
+                                         const void* grad_y, const void* x, const void* saved_proj, const void* S1s,
+                                         const void* S2s, const void* U1s, const void* U2s, void* grad_x,
+                                         float* grad_U1s, float* grad_U2s, float* grad_bias, const uint32_t* relu_bits,
+                                         void* workspace, size_t ws_bytes, void* stream) {
+    if (fuse & ~(unsigned)(SKL_FUSE_RELU_IN | SKL_FUSE_RELU_BITS))
+        return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
+    const bool bits = (fuse & SKL_FUSE_RELU_BITS) != 0;
+    if (bits && (!(fuse & SKL_FUSE_RELU_IN) || (T > 0 && !relu_bits)))
+        return fail(SKL_ERR_PARAM, "backward: SKL_FUSE_RELU_BITS needs SKL_FUSE_RELU_IN and a relu_bits buffer");
     SklDims d;
     SKL_TRY(get_dims(s, d));
+    if (bits && !relu_bits_ok(d, s->dtype))
+        return fail(SKL_ERR_UNSUPPORTED, "backward: 1-bit ReLU masks need the fused CTA-pair kernel for this shape");
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::backward: T must be >= 0");
     if (phases == 0 || (phases & ~(unsigned)SKL_BWD_ALL)) return fail(SKL_ERR_PARAM, "bad phase mask %u", phases);
     const bool ph_u1 = (phases & SKL_BWD_DU1_DB) != 0, ph_data = (phases & SKL_BWD_DX_DU2) != 0;
@@ -904,7 +960,9 @@ skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned p
         a.N2 = (int)d.d_in;
         a.alpha = inv;
         a.bias = nullptr;
-        a.mask = (fuse & SKL_FUSE_RELU_IN) ? x : nullptr;  // grad_x *= (x > 0): the preceding ReLU's backward
+        a.mask = (fuse & SKL_FUSE_RELU_IN) && !bits ? x : nullptr;  // grad_x *= (x > 0): the preceding ReLU's backward
+        a.mask_bits = bits ? relu_bits : nullptr;                       // ... or its 1-bit form from the forward
+        a.bits_ld = skl_relu_bits_row_words(d.d_in);
         a.ld_mask = d.d_in;
         a.out = grad_x;
         a.ldo = d.d_in;

@@ -23,7 +23,8 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 from . import (BF16, BWD_ALL, BWD_DU1_DB, BWD_DX_DU2, FUSE_RELU_IN, FUSE_RELU_OUT, ShapeError, SkLinear,
-               SklError, backward_phase, forward, torch_dtype, workspace_size)
+               SklError, backward_phase, forward, relu_bits_row_words, relu_bits_supported, torch_dtype,
+               workspace_size)
 
 
 class Relu:
@@ -40,6 +41,7 @@ class _Step:
     relu_in: bool = False   # the input came out of a ReLU (its mask is fused into this layer's dX)
     x: object = None        # saved input (needed by the backward: dU2s, the ReLU mask)
     saved: object = None    # saved projection x·S1 [L*k][round8(T)]
+    bits: object = None     # relu_in: the 1-bit ReLU mask of x written by the previous layer's forward
 
 
 @dataclass
@@ -53,8 +55,12 @@ class ChainGrads:
 class SkChain:
     """model_forward over a list of SkLinear / Relu layers, with a training backward."""
 
-    def __init__(self, layers):
+    def __init__(self, layers, relu_bits=True):
+        """relu_bits: carry each fused ReLU's mask from the forward to the next
+        layer's backward as 1 bit per element (skl.h SKL_FUSE_RELU_BITS) where both
+        layers' kernels support it, instead of re-reading the ReLU output."""
         layers = list(layers)
+        self.relu_bits = relu_bits
         if not layers or not isinstance(layers[0], SkLinear):
             raise ShapeError(1, "SkChain: a chain starts with an SKLinear layer (a leading ReLU has no "
                                 "producing layer to fuse into)")
@@ -113,15 +119,21 @@ class SkChain:
         ws = self._workspace(T, x.device)
         td = torch_dtype(self.dtype)
         cur = x
-        for st in self.steps:
+        for i, st in enumerate(self.steps):
             L = st.layer
             y = torch.empty(T, L.d_out, dtype=td, device=x.device)
             saved = torch.empty(L.num_terms * L.low_rank, (T + 7) // 8 * 8, dtype=td, device=x.device) \
                 if train else None
+            bits = None
+            if train and st.relu_out and self.relu_bits and i + 1 < len(self.steps) and \
+                    relu_bits_supported(L.shape) and relu_bits_supported(self.steps[i + 1].layer.shape):
+                bits = torch.empty(T, relu_bits_row_words(L.d_out), dtype=torch.int32, device=x.device)
             forward(L.shape, cur, L.S1s, L.S2s, L.U1s, L.U2s, L.bias, y, saved, ws,
-                    fuse=FUSE_RELU_OUT if st.relu_out else 0)
+                    fuse=FUSE_RELU_OUT if st.relu_out else 0, relu_bits=bits)
             if train:
                 st.x, st.saved = cur, saved
+                if i + 1 < len(self.steps):
+                    self.steps[i + 1].bits = bits
             cur = y
         return cur
 
@@ -162,13 +174,13 @@ class SkChain:
                 if w is not None:
                     works.append(w)
                 backward_phase(L.shape, BWD_DX_DU2, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
-                               None, b.dU2s, None, ws, fuse=fuse)
+                               None, b.dU2s, None, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
                 w = b.allreduce_tail(group, async_op=True)
                 if w is not None:
                     works.append(w)
             else:
                 backward_phase(L.shape, BWD_ALL, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
-                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse)
+                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
             cur = gx
         return ChainGrads(cur, buckets), works
 

@@ -381,6 +381,50 @@ def test_fused_relu_mask_is_exact_at_scale(skl, dtype_name, unfused):
         assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_chain_relu_bits_match_x_mask_bitwise(skl, dtype_name):
+    """The 1-bit ReLU mask carried from FFN1's forward to FFN2's backward
+    (SKL_FUSE_RELU_BITS) gives bitwise the same activations and gradients as
+    re-reading the ReLU output, at a c5 FFN shape with ragged T."""
+    from paper_2601_15473_b200.model import Relu, SkChain
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    k = 128 if dtype_name == "bf16" else 64  # TF32: R = 256 stays on the CTA-pair kernel
+    l1 = skl.SkLinear(768, 3072, 2, k, seed=11, dtype=dtype)
+    l2 = skl.SkLinear(3072, 768, 2, k, seed=12, dtype=dtype)
+    if not (skl.relu_bits_supported(l1.shape) and skl.relu_bits_supported(l2.shape)):
+        assert os.environ.get("SKL_FORCE_UNFUSED") is not None  # only the unfused chain lacks them
+        pytest.skip("1-bit masks are a fused-kernel feature")
+    T = 5000
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    x = torch.randn(T, 768, device="cuda", generator=gen).to(td)
+    g = torch.randn(T, 768, device="cuda", generator=gen).to(td)
+    res = []
+    for bits in (False, True):
+        chain = SkChain([l1, Relu(), l2], relu_bits=bits)
+        y = chain.forward(x)
+        assert (chain.steps[1].bits is not None) == bits
+        grads, _ = chain.backward(g, overlap=False)
+        torch.cuda.synchronize()
+        res.append((y.clone(), grads.grad_x.clone(), [(b.dU1s.clone(), b.dU2s.clone(), b.db.clone())
+                                                       for b in grads.layers]))
+    (y0, gx0, l0), (y1, gx1, lb) = res
+    assert torch.equal(y0, y1) and torch.equal(gx0, gx1)
+    for a, b in zip(l0, lb):
+        for u, v in zip(a, b):
+            assert torch.equal(u, v)
+    # the bits are the ReLU output's sign, bit (c % 32) of word c / 32
+    chain = SkChain([l1, Relu(), l2], relu_bits=True)
+    h = chain.forward(x)
+    bits = chain.steps[1].bits
+    a1 = chain.steps[1].x
+    w = skl.relu_bits_row_words(3072)
+    assert bits.shape == (T, w)
+    cols = torch.arange(3072, device="cuda")
+    got = (bits[:, cols // 32] >> (cols % 32)) & 1
+    assert torch.equal(got.bool(), a1 > 0)
+
+
 def test_bert_stack_overlapped_dp_step_runs(skl):
     """Config 5 at reduced depth: the BERT FFN/proj stack with the phased,
     per-layer all-reduce schedule on a world-1 NCCL group gives the same
