@@ -167,7 +167,19 @@ def roofline_time(d_in, d_out, l, k, T, ebytes, peak_tf, peak_bw):
     return max(t_tensor, t_hbm), ("tensor" if t_tensor >= t_hbm else "hbm"), flops, bytes_
 
 
-def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=10, warmup=3, phased=False):
+def _time_steps(torch, fn, steps):
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st = torch.cuda.current_stream()
+    e0.record(st)
+    for _ in range(steps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=10, warmup=3, phased=False,
+                     graph=False):
     kind = skl.BF16 if dtype == "bf16" else skl.F32_TF32
     td = torch.bfloat16 if dtype == "bf16" else torch.float32
     s = skl.shape(d_in, d_out, l, k, kind)
@@ -201,14 +213,11 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
     for _ in range(warmup):
         step()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st = torch.cuda.current_stream()
-    e0.record(st)
-    for _ in range(steps):
-        step()
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    ms = ms_eager = _time_steps(torch, step, steps)
+    if graph:  # launch-bound shapes: the same step replayed from a CUDA graph
+        from paper_2601_15473_b200.graphs import capture
+        g = capture(step)
+        ms = _time_steps(torch, g.replay, steps)
     peak_bf16, peak_bw, _ = peaks()
     peak_tf = peak_bf16 if dtype == "bf16" else peak_bf16 / 2  # TF32 dense = bf16 / 2 (not separately measured)
     t_roof, bound, flops, bytes_ = roofline_time(d_in, d_out, l, k, T, 2 if dtype == "bf16" else 4, peak_tf, peak_bw)
@@ -216,7 +225,8 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
             "bound": bound, "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
             "tflops": flops / (ms / 1e3) / 1e12, "hbm_gbs_alg": bytes_ / (ms / 1e3) / 1e9,
             "fused": bool((2 * l * k + 63) // 64 * 64 <= (512 if dtype == "bf16" else 256)),
-            "peak_tflops_used": peak_tf, "phased_backward": phased}
+            "peak_tflops_used": peak_tf, "phased_backward": phased, "cuda_graph": graph,
+            "ms_per_step_eager": ms_eager}
 
 
 def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers=12):
@@ -243,14 +253,12 @@ def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    st = torch.cuda.current_stream()
-    e0.record(st)
-    for _ in range(steps):
-        step()
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1) / steps
+    ms = ms_eager = _time_steps(torch, step, steps)
+    graph = world == 1  # one process: replay the 72-layer step from a CUDA graph (no per-call host work)
+    if graph:
+        from paper_2601_15473_b200.graphs import capture
+        gr = capture(step)
+        ms = _time_steps(torch, gr.replay, steps)
     if world > 1:
         t = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -270,7 +278,7 @@ def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers
                                                                         if world > 1 else ""),
             "dtype": "bf16", "tokens": T * world, "ms_per_step": ms, "tokens_per_s": world * T / (ms / 1e3),
             "bound": "tensor", "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
-            "tflops": flops / (ms / 1e3) / 1e12, "n_gpus": world}
+            "tflops": flops / (ms / 1e3) / 1e12, "n_gpus": world, "cuda_graph": graph, "ms_per_step_eager": ms_eager}
 
 
 def run_reference(args, rank):
@@ -476,7 +484,8 @@ def main():
         workloads = []
         for (name, di, do, l, k, tt, dt) in SWEEP:
             try:
-                workloads.append(measure_workload(skl, torch, dev, name, di, do, l, k, tt, dt))
+                # launch-bound (T=64): replayed from a CUDA graph; ms_per_step_eager keeps the per-call figure
+                workloads.append(measure_workload(skl, torch, dev, name, di, do, l, k, tt, dt, graph=tt < 4096))
             except Exception as e:  # report, never fake
                 workloads.append({"workload": name, "error": str(e)[:200]})
             torch.cuda.empty_cache()

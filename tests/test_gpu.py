@@ -628,3 +628,34 @@ def test_unfused_path_parity_in_subprocess():
                         "parity or mask_is_exact or chain or edge or deterministic"],
                        env=env, cwd=root, capture_output=True, text=True, timeout=1200)
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_graph_replay_is_bitwise_equal(skl):
+    """A fixed-shape chain step (forward + backward through SkChain, 2 encoder
+    layers of the c5 stack) recorded with graphs.capture replays to bitwise the
+    eager results -- what bench.py relies on for the launch-bound lines."""
+    from paper_2601_15473_b200.graphs import capture
+    from paper_2601_15473_b200.model import bert_ffn_stack
+    chain = bert_ffn_stack(num_layers=1)
+    T = 1000
+    gen = torch.Generator(device="cuda").manual_seed(21)
+    x = torch.randn(T, 768, device="cuda", generator=gen).to(torch.bfloat16)
+    g = torch.randn(T, 768, device="cuda", generator=gen).to(torch.bfloat16)
+    buckets = chain.allocate_grads("cuda")
+
+    def step():
+        chain.forward(x)
+        chain.backward(g, buckets=buckets, need_grad_x=False, overlap=False)
+
+    step()
+    torch.cuda.synchronize()
+    ref = [b.flat.clone() for b in buckets]
+    for b in buckets:
+        b.flat.zero_()
+    gr = capture(step)
+    for b in buckets:
+        b.flat.zero_()
+    gr.replay()
+    torch.cuda.synchronize()
+    for a, b in zip(ref, buckets):
+        assert torch.equal(a, b.flat)
