@@ -547,8 +547,40 @@ __global__ void __launch_bounds__(384, 1)
             if (leader) mbar_arrive(bar);
             else mbar_arrive_cluster(bar, 0);
         };
+        // The backward's single-pass GEMM1 finishes both H chunks at once, so the
+        // MMA idles while they convert: there the saved columns (P_S2) are written
+        // AFTER hready, from the bf16 H in TMEM, under the first GEMM2 MMAs.  The
+        // next tile's GEMM1 cannot overwrite H before that: its pass first waits
+        // for both GEMM2 slots, which this group releases only after its drain.
+        const bool defer_save = C::kSinglePassG1 && kKind == 0 && nch == 2;
+        int cur_t = 0;
+        // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
+        // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
+        // The warp's [32 tokens x 16 cols] block is transposed through a 1 KB smem
+        // scratch so every lane writes two 16-B chunks (8 tokens of one column)
+        // instead of 16 scattered 2-B stores (8 % of the kernel).
+        auto save_cols16 = [&](const uint32_t (&p)[8], int col) {
+            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
+            __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(buf + q * 1024);  // [16 cols][32 tokens]
+#pragma unroll
+            for (int i = 0; i < 16; ++i) scr[i * 32 + lane] = pb[i];
+            __syncwarp();
+            const long long tok0 = (long long)cur_t * tile_rows + (int)rank * 128 + q * 32;
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+                const int id = (int)lane * 2 + hh, i = id >> 2, j = id & 3;
+                const long long tok = tok0 + 8 * j;
+                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols && tok < args.ld_save) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(scr + i * 32 + 8 * j);
+                    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.save) +
+                                              (long long)(col + i - args.save_col0) * args.ld_save + tok) = v;
+                }
+            }
+            __syncwarp();
+        };
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+            cur_t = t;
             const int row = t * tile_rows + (int)rank * 128 + (int)srow;
             const bool row_ok = row < args.T;
             if (use_mask && issuer) issue_mask(t, 0);  // lands during the GEMM1 conversion
@@ -598,7 +630,7 @@ __global__ void __launch_bounds__(384, 1)
                         }
                     }
                 } else {
-                if (args.save) {  // buf doubles as the transpose scratch: the last store must have left it
+                if (args.save && !defer_save) {  // buf doubles as the transpose scratch: the last store must have left it
                     if (issuer) bulk_wait_read<0>();
                     named_bar_sync(1 + wg, 128);
                 }
@@ -626,31 +658,9 @@ __global__ void __launch_bounds__(384, 1)
                         const int cl = qi * W + 16 * g;  // chunk-local fp32 column
                         tmem_st8(tmem_base + lane_base + hoff + 128 * c + cl / 2, p);
                         const int col = 256 * c + cl;  // H column (R order)
-                        // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
-                        // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
-                        // The warp's [32 tokens x 16 cols] block is transposed through a 1 KB
-                        // smem scratch so every lane writes two 16-B chunks (8 tokens of one
-                        // column) instead of 16 scattered 2-B stores (8 % of the kernel).
-                        if (args.save && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
-                            const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
-                            __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(buf + q * 1024);  // [16 cols][32 tokens]
-#pragma unroll
-                            for (int i = 0; i < 16; ++i) scr[i * 32 + lane] = pb[i];
-                            __syncwarp();
-                            const long long tok0 = (long long)t * tile_rows + (int)rank * 128 + q * 32;
-#pragma unroll
-                            for (int hh = 0; hh < 2; ++hh) {
-                                const int id = (int)lane * 2 + hh, i = id >> 2, j = id & 3;
-                                const long long tok = tok0 + 8 * j;
-                                if (col + i >= args.save_col0 && col + i < args.save_col0 + args.save_cols &&
-                                    tok < args.ld_save) {
-                                    const uint4 v = *reinterpret_cast<const uint4*>(scr + i * 32 + 8 * j);
-                                    *reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(args.save) +
-                                                              (long long)(col + i - args.save_col0) * args.ld_save + tok) = v;
-                                }
-                            }
-                            __syncwarp();
-                        }
+                        if (args.save && !defer_save && col + 16 > args.save_col0 &&
+                            col < args.save_col0 + args.save_cols)
+                            save_cols16(p, col);
                     }
                 }
                 }  // bf16 conversion
@@ -666,6 +676,26 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
                 if (c == 1) slot_seq += 2;
+            }
+            if (defer_save && args.save) {  // saved columns from the bf16 H, under the first GEMM2 MMAs
+                if (issuer) bulk_wait_read<0>();  // buf is the transpose scratch
+                named_bar_sync(1 + wg, 128);
+                for (int c = 0; c < nch; ++c) {
+                    const int W = min(256, args.R_pad - 256 * c) / 4;
+#pragma unroll 1
+                    for (int rd = 0; rd < 2; ++rd) {
+                        const int qi = 2 * rd + (int)wg;
+#pragma unroll 1
+                        for (int g = 0; g < 4 && 16 * g < W; ++g) {
+                            const int cl = qi * W + 16 * g, col = 256 * c + cl;
+                            if (!(col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols)) continue;
+                            uint32_t p[8];
+                            tmem_ld8(tmem_base + lane_base + 128 * c + cl / 2, p);
+                            tmem_ld_wait();
+                            save_cols16(p, col);
+                        }
+                    }
+                }
             }
             // ---- GEMM2 output tiles: this group's 64 columns of every 128-wide tile
             for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
