@@ -68,6 +68,7 @@ struct B2BArgs {
     uint32_t* relu_bits;         // forward with relu: written alongside out
     const uint32_t* mask_bits;   // backward: out *= bit, instead of reading `mask`
     long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
+    int l2hint;                  // L2 cache-hint policy bits for the producer's TMA loads
 };
 
 namespace dev {
@@ -288,6 +289,13 @@ __global__ void __launch_bounds__(384, 1)
             uint32_t phase = 0;
             unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             const long long tp0 = clock64();
+            // activations (x / G) stream through L2 once; the weight panels are re-read by every tile
+            // (SKL_B2B_L2HINT bit 0: activations evict_first when GEMM1 reads them once, bit 1: weights
+            // evict_last; a two-pass GEMM1 re-reads its activation tile from L2, so it keeps the default)
+            const int hint = args.l2hint;
+            const uint64_t pol_norm = l2_evict_normal();
+            const uint64_t pol_act = ((hint & 1) && (C::kSinglePassG1 || nch == 1)) ? l2_evict_first() : pol_norm;
+            const uint64_t pol_w = (hint & 2) ? l2_evict_last() : pol_norm;
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             auto load_g1 = [&](int t) {
                 const int am = t * tile_rows + (int)rank * 128;
@@ -305,7 +313,7 @@ __global__ void __launch_bounds__(384, 1)
                         uint8_t* st = smem + stage * C::kStageMain;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], 0);
-                        if constexpr (!C::kSplit) tma_load_2d<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am);
+                        if constexpr (!C::kSplit) tma_load_2d_hint<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am, pol_act);
                         for (int c = c_lo; c < c_ld; ++c) {
                             const int wc = min(256, args.R_pad - 256 * c);
                             const int brows = wc / kCG;
@@ -313,19 +321,19 @@ __global__ void __launch_bounds__(384, 1)
                             uint8_t* bst = st + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
                             if constexpr (kMode == 0) {
                                 for (int r = 0; r < brows; r += args.b1rows)
-                                    tma_load_2d<kCG>(&tmB1, &full[stage], bst + r * 128, kb * C::kBK, b0 + r);
+                                    tma_load_2d_hint<kCG>(&tmB1, &full[stage], bst + r * 128, kb * C::kBK, b0 + r, pol_w);
                             } else if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
                                 for (int r = 0; r < brows; r += args.b1rows) {
                                     const int rg = b0 + r;
-                                    tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + r * 128, kb * 64,
-                                                     rg < args.Lk ? rg : rg - args.Lk);
+                                    tma_load_2d_hint<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + r * 128, kb * 64,
+                                                     rg < args.Lk ? rg : rg - args.Lk, pol_w);
                                 }
                             } else {  // MN-major [64 d_in rows x 64 rank cols] blocks of S1s | U2s
                                 for (int jb = 0; jb < brows / 64; ++jb) {
                                     const int rg = b0 + 64 * jb;
                                     const int rr = rg < args.Lk ? rg : rg - args.Lk;
-                                    tma_load_2d<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + jb * 8192,
-                                                     rr % args.k, (rr / args.k) * args.dS + kb * 64);
+                                    tma_load_2d_hint<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + jb * 8192,
+                                                     rr % args.k, (rr / args.k) * args.dS + kb * 64, pol_w);
                                 }
                             }
                         }
@@ -347,24 +355,24 @@ __global__ void __launch_bounds__(384, 1)
                             // whole stage (kKbPerStage2 k-blocks, one source half) in one
                             // {64 x 64*kKbPerStage2} box; layouts coincide for 64-wide N.
                             const int r0 = kb0 * 64;
-                            tma_load_2d<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st, brow,
-                                             r0 < args.Lk ? r0 : r0 - args.Lk);
+                            tma_load_2d_hint<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st, brow,
+                                             r0 < args.Lk ? r0 : r0 - args.Lk, pol_w);
                             next();
                             continue;
                         }
                         for (int q = 0; q < nk; ++q) {
                             const int r0 = (kb0 + q) * C::kBK;  // rank index of this k-block
                             if constexpr (kMode == 0) {
-                                tma_load_2d<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, r0, brow);
+                                tma_load_2d_hint<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, r0, brow, pol_w);
                             } else if constexpr (kMode == 1) {  // MN-major rows of [U1s ; S2s]
                                 const CUtensorMap* m = r0 < args.Lk ? &tmB2 : &tmB2b;
                                 const int rr = r0 < args.Lk ? r0 : r0 - args.Lk;
                                 for (int jb = 0; jb < C::kB2Rows / 64; ++jb)
-                                    tma_load_2d<kCG>(m, &full[stage], st + q * C::kB2KbBytes + jb * 8192, brow + 64 * jb, rr);
+                                    tma_load_2d_hint<kCG>(m, &full[stage], st + q * C::kB2KbBytes + jb * 8192, brow + 64 * jb, rr, pol_w);
                             } else {  // K-major [d_in rows x 64 rank cols] of S1s | U2s, term row offset
                                 const int rr = r0 < args.Lk ? r0 : r0 - args.Lk;
-                                tma_load_2d<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st + q * C::kB2KbBytes,
-                                                 rr % args.k, (rr / args.k) * args.dS + brow);
+                                tma_load_2d_hint<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st + q * C::kB2KbBytes,
+                                                 rr % args.k, (rr / args.k) * args.dS + brow, pol_w);
                             }
                         }
                         next();

@@ -55,6 +55,7 @@ struct DuArgs {
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
     int dbg;         // SKL_DU_DEBUG=1: per-CTA cycle accounting into g_du_prof (perf analysis)
+    int l2hint;      // L2 cache-hint policy bits for the operand loads (see the producer)
     int early;       // 1: dU1 units skip the PDL wait (see du_kernel); needs cr and a dU2 problem in p[1]
     int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); each CTA
                      // bulk-stores its partial, the cluster barrier publishes it, each CTA bulk-loads its slice
@@ -231,6 +232,11 @@ __global__ void __launch_bounds__(256, 1)
             uint32_t phase = 0;
             unsigned long long w_empty = 0;
             const long long t_beg = clock64();
+            // A (Savedᵀ / P_S2ᵀ) is re-read by every N tile of the same split; B (G / X) once
+            // (DuArgs::l2hint bit 0: A evict_last, bit 1: B evict_first; 0 = the default policy)
+            const uint64_t pol_norm = l2_evict_normal();
+            const uint64_t pol_a = (args.l2hint & 1) ? l2_evict_last() : pol_norm;
+            const uint64_t pol_b = (args.l2hint & 2) ? l2_evict_first() : pol_norm;
             for (int u = pair; u < units; u += npairs) {
                 const Unit x = decode(u);
                 const CUtensorMap* ma = x.p ? &tmA1 : &tmA0;
@@ -251,18 +257,18 @@ __global__ void __launch_bounds__(256, 1)
                         // no colsum anywhere: pair-signalled TMA straight onto the leader's barrier
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kDuStageBytes);
                         else mbar_arrive_cluster(&full[stage], lead_cta);
-                        tma_load_2d<2>(ma, &full[stage], a_dst, k0, m0);
+                        tma_load_2d_hint<2>(ma, &full[stage], a_dst, k0, m0, pol_a);
 #pragma unroll
                         for (int j = 0; j < 128 / KT::kW; ++j)
-                            tma_load_2d<2>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0);
+                            tma_load_2d_hint<2>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0, pol_b);
                         if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                         continue;
                     }
                     mbar_arrive_expect_tx(&full[stage], kDuStageBytes);
-                    tma_load_2d<1>(ma, &full[stage], a_dst, k0, m0);
+                    tma_load_2d_hint<1>(ma, &full[stage], a_dst, k0, m0, pol_a);
 #pragma unroll
                     for (int j = 0; j < 128 / KT::kW; ++j)
-                        tma_load_2d<1>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0);
+                        tma_load_2d_hint<1>(mb, &full[stage], b_dst + j * KT::kBK * 128, n0 + j * KT::kW, k0, pol_b);
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }

@@ -314,6 +314,12 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         return e ? atoi(e) : 0;
     }();
     a.dbg = dbg;
+    // L2 hints: weight panels evict_last (every tile re-reads them); the streamed
+    // activation evict_first only when it is far larger than L2 (126 MB) -- a
+    // smaller one (c2's G, 201 MB) is partly still in L2 when du re-reads it.
+    static const int l2hint = getenv("SKL_B2B_L2HINT") ? atoi(getenv("SKL_B2B_L2HINT")) : -1;
+    const double act_bytes = (double)a.T * a.K1 * (kind == 0 ? 2 : 4);
+    a.l2hint = l2hint >= 0 ? l2hint : (2 | (act_bytes > 256e6 ? 1 : 0));
     {  // B1 box rows: largest power of two <= 128 dividing every chunk's per-CTA rows (and Lk in mode 2)
         const int cg = g_b2b_cg;
         int r = 128;
@@ -563,6 +569,8 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     DuArgs a = {};
     a.k_blocks = u.kb;
     a.num_units = u.units;
+    static const int du_l2hint = getenv("SKL_DU_L2HINT") ? atoi(getenv("SKL_DU_L2HINT")) : 0;
+    a.l2hint = du_l2hint;
     a.num_tiles = u.tiles();
     const int u1_units = (which & 1) ? u.t0 * u.s0 : 0;
     const DuProblem pu1{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, u.s0, 0, 0, grad_bias ? 1 : 0, inv, grad_U1s,
