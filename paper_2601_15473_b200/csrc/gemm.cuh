@@ -27,6 +27,7 @@ namespace skl {
 
 struct GemmArgs {
     int M, N, K;
+    int l2hint;  // bit 1: B loads evict_last
     int num_m_tiles, num_n_tiles, k_blocks;
     float alpha;
     const float* bias;  // [N] fp32, nullable
@@ -142,6 +143,10 @@ __global__ void __launch_bounds__(256, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
+            // B (the weight panel) is re-read by every m tile: evict_last.  A keeps the
+            // default: n-fastest order re-reads each activation panel from L2.
+            const uint64_t pol_a = l2_evict_normal();
+            const uint64_t pol_b = (args.l2hint & 2) ? l2_evict_last() : pol_a;
             for (int t = cluster_id; t < num_tiles; t += num_clusters) {
                 int m0, n0;
                 decode(t, m0, n0);
@@ -154,8 +159,8 @@ __global__ void __launch_bounds__(256, 1)
                         mbar_arrive_expect_tx(&full[stage], C::kStageBytes * kCG);
                     else
                         mbar_arrive_cluster(&full[stage], 0);
-                    tma_load_2d<kCG>(&tmA, &full[stage], sA + stage * C::kABytes, k0, am);
-                    tma_load_2d<kCG>(&tmB, &full[stage], sB + stage * C::kBBytes, k0, bn);
+                    tma_load_2d_hint<kCG>(&tmA, &full[stage], sA + stage * C::kABytes, k0, am, pol_a);
+                    tma_load_2d_hint<kCG>(&tmB, &full[stage], sB + stage * C::kBBytes, k0, bn, pol_b);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }

@@ -156,6 +156,8 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     } else {
         to = ta;  // unused
     }
+    static const int gemm_l2hint = getenv("SKL_GEMM_L2HINT") ? atoi(getenv("SKL_GEMM_L2HINT")) : 0;  // 2: measured neutral at c3
+    args.l2hint = gemm_l2hint;
     args.M = M;
     args.N = N;
     args.K = K;
@@ -498,6 +500,19 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
             const double cost = len + 1e-3 * (s.t0 * a + s.t1 * b);  // tie-break: fewer partials
             if (cost < best) { best = cost; s.s0 = std::max(a, 1); s.s1 = std::max(b, 1); }
         }
+    if (s.t0 + s.t1 > pairs) {
+        // More tiles than CTA pairs: several waves whatever S is, so pick the
+        // uniform S with the shortest wave-quantised time, waves(S) * ceil(kb / S).
+        // Clusters of 2S CTAs must fit a GPC's free SMs as earlier waves retire:
+        // measured at c3 (96 tiles), S = 1/2/3/4 -> du 983/808/956/966 us, so
+        // only S <= 2 is considered.
+        double bestw = 1e30;
+        for (int S = 1; S <= std::min(2, smax); ++S) {
+            const int64_t waves = ((int64_t)(s.t0 + s.t1) * S + pairs - 1) / pairs;
+            const double cost = (double)waves * std::ceil((double)s.kb / S) * (1.0 + 1e-3 * S);
+            if (cost < bestw) { bestw = cost; s.s0 = s.s1 = S; }
+        }
+    }
     if (const char* e = getenv("SKL_DU_SPLITS")) {  // experiments: "S" or "S0,S1"
         int a = 0, b = 0;
         const int n = sscanf(e, "%d,%d", &a, &b);
