@@ -584,7 +584,8 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     DuArgs a = {};
     a.k_blocks = u.kb;
     a.num_units = u.units;
-    static const int du_l2hint = getenv("SKL_DU_L2HINT") ? atoi(getenv("SKL_DU_L2HINT")) : 0;
+    // B (G / X, each tile read once) evict_first: c2 du 72.7 -> 69.7 us, c5 projection du -10 %
+    static const int du_l2hint = getenv("SKL_DU_L2HINT") ? atoi(getenv("SKL_DU_L2HINT")) : 2;
     a.l2hint = du_l2hint;
     a.num_tiles = u.tiles();
     const int u1_units = (which & 1) ? u.t0 * u.s0 : 0;
