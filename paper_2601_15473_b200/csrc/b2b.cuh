@@ -560,7 +560,12 @@ __global__ void __launch_bounds__(384, 1)
         // AFTER hready, from the bf16 H in TMEM, under the first GEMM2 MMAs.  The
         // next tile's GEMM1 cannot overwrite H before that: its pass first waits
         // for both GEMM2 slots, which this group releases only after its drain.
-        const bool defer_save = C::kSinglePassG1 && kKind == 0 && nch == 2;
+        // Same for a single chunk (R <= 256): its conversion has no other chunk's
+        // GEMM1 to hide under.  Needs >= 3 GEMM2 tiles, so that the MMA issuer
+        // has waited on a slot this group released after its saves before it
+        // issues the next tile's GEMM1 (which overwrites, or -- ping-pong -- is
+        // followed by a GEMM1 that overwrites, this H).
+        const bool defer_save = kKind == 0 && ((C::kSinglePassG1 && nch == 2) || (nch == 1 && n2_tiles >= 3));
         int cur_t = 0;
         // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
         // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
@@ -698,7 +703,7 @@ __global__ void __launch_bounds__(384, 1)
                             const int cl = qi * W + 16 * g, col = 256 * c + cl;
                             if (!(col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols)) continue;
                             uint32_t p[8];
-                            tmem_ld8(tmem_base + lane_base + 128 * c + cl / 2, p);
+                            tmem_ld8(tmem_base + lane_base + (pp ? 128u * (it & 1) : 0u) + 128 * c + cl / 2, p);
                             tmem_ld_wait();
                             save_cols16(p, col);
                         }
