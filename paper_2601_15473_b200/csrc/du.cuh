@@ -84,7 +84,7 @@ struct DuKind {
 // colsum phase, [5] epilogue waits on the accumulator, [6] partial write,
 // [7] reduction (ticket wait + sum).
 __device__ unsigned long long g_du_prof[296][8];
-__device__ unsigned long long g_du_ts[296][10];
+__device__ unsigned long long g_du_ts[296][12];
 __device__ unsigned long long g_du_wend[296][16];  // SKL_DU_DEBUG&2: per-warp reduce-loop end / kernel end  // SKL_DU_DEBUG&2: globaltimer at entry / exit / prologue done / reduce start
 __device__ unsigned long long g_du_wait[296][4];  // [cta]: fence+ticket wait, +fence, +sum, +colsum/release
 
@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(256, 1)
         // 0..S-1.  Few, large copies: per-copy TMA overhead and the cold tail code
         // (ncu: stall_no_inst) are what this phase costs.
         __syncthreads();
+        if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][10] = gtimer();
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();  // the dump was written by generic stores
             if (tail->valid > 0)
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(256, 1)
             bulk_commit();
             bulk_wait<0>();
             __threadfence();
-            if ((args.dbg & 2) && blockIdx.x < 296) g_du_wend[blockIdx.x][15] = gtimer();
+            if ((args.dbg & 2) && blockIdx.x < 296) g_du_ts[blockIdx.x][11] = gtimer();
         }
         tc_fence_before();
         cluster_sync();
@@ -659,13 +660,22 @@ __global__ void __launch_bounds__(256, 1)
                 const int m = d.m0 + r, n = d.n0 + j * 4;
                 if (m >= d.M || n >= d.N) continue;
                 const float* src = cr_part + r * kDuBN + ((j ^ ((d.r0 + r) & 7)) << 2);
-                float4 a = *reinterpret_cast<const float4*>(src);
+                float4 v[4];  // up to 4 partial loads in flight, then the ordered sum (split 0, 1, ...)
+#pragma unroll
+                for (int q2 = 0; q2 < 4; ++q2)
+                    if (q2 < S) v[q2] = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
+                float4 a = v[0];
+#pragma unroll
+                for (int q2 = 1; q2 < 4; ++q2)
+                    if (q2 < S) { a.x += v[q2].x; a.y += v[q2].y; a.z += v[q2].z; a.w += v[q2].w; }
 #pragma unroll 1
-                for (int q2 = 1; q2 < S; ++q2) {
-                    const float4 v = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
-                    a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
+                for (int q2 = 4; q2 < S; ++q2) {  // SKL_DU_CR_MAX > 4
+                    const float4 w = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
+                    a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
                 }
-                float* o = d.out + (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms + n;
+                const long long mo = d.mb >= d.M ? (long long)m * d.ms
+                                                 : (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms;
+                float* o = d.out + mo + n;
                 if (d.vec && n + 4 <= d.N) {
                     *reinterpret_cast<float4*>(o) = make_float4(a.x * d.alpha, a.y * d.alpha, a.z * d.alpha, a.w * d.alpha);
                 } else {

@@ -1262,7 +1262,7 @@ extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
     return n;
 }
 extern "C" int skl_debug_du_ts(unsigned long long* out, int n) {
-    if (n > 296 * 10) n = 296 * 10;
+    if (n > 296 * 12) n = 296 * 12;
     if (cudaMemcpyFromSymbol(out, skl::dev::g_du_ts, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
         return -1;
     return n;
