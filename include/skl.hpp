@@ -176,13 +176,23 @@ class SkLinear {
     // SkLinear::forward (nn_layers.cpp:61-76), device pointers:
     // x [T, d_in] -> y [T, d_out]; saved (nullable) [L*k][round8(T)] keeps x·S1_i.
     // fuse = SKL_FUSE_RELU_OUT applies a following ReLU in the epilogue.
+    // relu_bits (with SKL_FUSE_RELU_OUT): also write the 1-bit ReLU mask,
+    // [T][skl_relu_bits_row_words(d_out)] uint32, for the next layer's backward.
     void forward(const void* x, int64_t T, void* y, void* saved = nullptr, cudaStream_t st = nullptr,
-                 unsigned fuse = 0) const {
+                 unsigned fuse = 0, uint32_t* relu_bits = nullptr) const {
         if (T < 0) throw shape_error("SkLinear::forward: negative token count");
         void* ws = workspace(T, st);
+        if (relu_bits) {
+            check(sketched_linear_forward_bits(&shape_, T, fuse | SKL_FUSE_RELU_BITS, x, S1s_.get(), S2s_.get(),
+                                               U1s_.get(), U2s_.get(), bias_.get(), y, saved, relu_bits, ws,
+                                               ws_.bytes(), st));
+            return;
+        }
         check(sketched_linear_forward_ex(&shape_, T, fuse, x, S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(),
                                          bias_.get(), y, saved, ws, ws_.bytes(), st));
     }
+    // Whether this layer's kernels take 1-bit ReLU masks (skl_relu_bits_supported).
+    bool relu_bits_supported() const { return skl_relu_bits_supported(&shape_) != 0; }
 
     // SkLinear::backward (nn_layers.cpp:78-101): gradients allocated here.
     Grads backward(const void* x, const void* grad_out, int64_t T, const void* saved = nullptr,
@@ -200,11 +210,18 @@ class SkLinear {
     // dU1s | dU2s | db bucket for the NCCL all-reduce).  grad_x / grad_b nullable.
     // phases: SKL_BWD_ALL, or SKL_BWD_DU1_DB then SKL_BWD_DX_DU2 (data-parallel overlap);
     // fuse = SKL_FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward).
+    // relu_bits (with SKL_FUSE_RELU_IN): the previous layer's 1-bit ReLU mask instead of x.
     void backward_into(const void* x, const void* grad_out, int64_t T, const void* saved, void* grad_x, float* dU1s,
                        float* dU2s, float* db, cudaStream_t st = nullptr, unsigned phases = SKL_BWD_ALL,
-                       unsigned fuse = 0) const {
+                       unsigned fuse = 0, const uint32_t* relu_bits = nullptr) const {
         if (T < 0) throw shape_error("SkLinear::backward: negative token count");
         void* ws = workspace(T, st);
+        if (relu_bits) {
+            check(sketched_linear_backward_bits(&shape_, T, phases, fuse | SKL_FUSE_RELU_BITS, grad_out, x, saved,
+                                                S1s_.get(), S2s_.get(), U1s_.get(), U2s_.get(), grad_x, dU1s, dU2s,
+                                                db, relu_bits, ws, ws_.bytes(), st));
+            return;
+        }
         check(sketched_linear_backward_ex(&shape_, T, phases, fuse, grad_out, x, saved, S1s_.get(), S2s_.get(),
                                           U1s_.get(), U2s_.get(), grad_x, dU1s, dU2s, db, ws, ws_.bytes(), st));
     }

@@ -453,6 +453,41 @@ void test_fused_relu_forward() {
     bool ok = true;
     for (size_t i = 0; i < y.size(); ++i) ok &= r[i] == (y[i] > 0 ? y[i] : 0.0);
     report("fused ReLU forward == max(0, forward) bitwise", ok);
+    // 1-bit masks: bits == (relu(y) > 0), and the next layer's backward with the
+    // bits equals its backward with the x-mask, bitwise (skl.h SKL_FUSE_RELU_BITS)
+    if (!L.relu_bits_supported()) {
+        std::printf("SKIP relu bits (shape not on the CTA-pair kernel)\n");
+        return;
+    }
+    const int64_t W = skl_relu_bits_row_words(d_out);
+    skl::DeviceBuffer Bits((size_t)(T * W) * 4), R2(T * d_out * 2);
+    L.forward(X.get(), T, R2.get(), nullptr, nullptr, SKL_FUSE_RELU_OUT, Bits.as<uint32_t>());
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+    std::vector<uint32_t> bits((size_t)(T * W));
+    Bits.download(bits.data(), bits.size() * 4);
+    const vec r2 = download(R2.get(), T * d_out, SKL_BF16);
+    bool okb = r2 == r;
+    for (int64_t t = 0; t < T; ++t)
+        for (int64_t c = 0; c < d_out; ++c)
+            okb &= (((bits[t * W + c / 32] >> (c % 32)) & 1u) != 0) == (r[t * d_out + c] > 0);
+    report("relu bits from the forward == (relu(y) > 0)", okb);
+    skl::SkLinear L2 = skl::SkLinear::fresh(d_out, 96, 1, 64, 8, SKL_DIST_GAUSSIAN, SKL_BF16);
+    if (!L2.relu_bits_supported()) return;
+    vec gv(T * 96);
+    orc_gaussian_matrix(T, 96, 9, gv.data());
+    const auto gh = to_dev(gv, SKL_BF16);
+    skl::DeviceBuffer G(gh.size());
+    G.upload(gh.data(), gh.size());
+    std::vector<vec> out[2];
+    for (int mode = 0; mode < 2; ++mode) {
+        skl::DeviceBuffer GX(T * d_out * 2), D1(64 * 96 * 4), D2(d_out * 64 * 4), DB(96 * 4);
+        L2.backward_into(R.get(), G.get(), T, nullptr, GX.get(), D1.as<float>(), D2.as<float>(), DB.as<float>(),
+                         nullptr, SKL_BWD_ALL, SKL_FUSE_RELU_IN, mode ? Bits.as<uint32_t>() : nullptr);
+        skl::check_cuda(cudaDeviceSynchronize(), "sync");
+        out[mode] = {download(GX.get(), T * d_out, SKL_BF16), download_f32(D1.get(), 64 * 96),
+                     download_f32(D2.get(), d_out * 64), download_f32(DB.get(), 96)};
+    }
+    report("next layer's backward: relu bits == x-mask, bitwise", out[0] == out[1]);
 }
 
 void test_nccl_allreduce_world1() {
