@@ -207,42 +207,55 @@ cudaError_t launch_realize(int dist, int64_t k, int64_t dd, uint64_t seed, int u
 // block 0 also converts the bias to fp32.
 template <typename T>
 __global__ void __launch_bounds__(256) pack_tiles_kernel(const void* S1s, const void* U2s, const void* U1s,
-                                                         const void* S2s, int64_t L, int64_t k, int64_t d_in,
-                                                         int64_t d_out, int64_t R_pad, void* Acat, void* Bcat,
+                                                         const void* S2s, int64_t L, int64_t k64, int64_t d_in64,
+                                                         int64_t d_out64, int64_t R_pad64, void* Acat, void* Bcat,
                                                          void* AcatT, void* BcatT, const void* bias, float* bias32) {
+    // 32-bit index math: every panel here is far below 2^31 elements, and 64-bit
+    // division / modulo (emulated, ~70 instructions each) made this kernel
+    // instruction-bound (13 us for 8 MB at c2-TF32).  The per-thread column of
+    // a tile is fixed across its 4 rows, so its term / rank split is hoisted.
     __shared__ float tile[32][33];
-    const int64_t Lk = L * k;
-    const int64_t ta_r = R_pad / 32, ta_c = (d_in + 31) / 32;
-    const int64_t tb_c = (d_out + 31) / 32;
-    const int64_t nA = ta_r * ta_c, nB = ta_r * tb_c;
+    const int k = (int)k64, d_in = (int)d_in64, d_out = (int)d_out64, R_pad = (int)R_pad64;
+    const int Lk = (int)L * k;
+    const int ta_r = R_pad / 32, ta_c = (d_in + 31) / 32;
+    const int tb_c = (d_out + 31) / 32;
+    const int nA = ta_r * ta_c, nB = ta_r * tb_c;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     if (bias32 && blockIdx.x == 0)
-        for (int64_t i = threadIdx.x; i < d_out; i += blockDim.x) bias32[i] = bias ? ld_f<T>(bias, i) : 0.f;
-    for (int64_t b = blockIdx.x; b < nA + nB; b += gridDim.x) {
+        for (int i = threadIdx.x; i < d_out; i += blockDim.x) bias32[i] = bias ? ld_f<T>(bias, i) : 0.f;
+    for (int b = blockIdx.x; b < nA + nB; b += gridDim.x) {
         const bool isA = b < nA;
-        int64_t row0, col0, rows, cols;  // natural layout: A = [d_in][R_pad], B = [R_pad][d_out]
+        int row0, col0, rows, cols;  // natural layout: A = [d_in][R_pad], B = [R_pad][d_out]
         if (isA) { row0 = (b / ta_r) * 32; col0 = (b % ta_r) * 32; rows = d_in; cols = R_pad; }
-        else { const int64_t bb = b - nA; row0 = (bb / tb_c) * 32; col0 = (bb % tb_c) * 32; rows = R_pad; cols = d_out; }
+        else { const int bb = b - nA; row0 = (bb / tb_c) * 32; col0 = (bb % tb_c) * 32; rows = R_pad; cols = d_out; }
+        // A: column c = rank index -> (source stack, term, rank-in-term), fixed for this thread
+        const int c = col0 + tx;
+        const void* asrc = nullptr;
+        int64_t abase = 0;
+        if (isA && c < 2 * Lk) {
+            const int cc = c < Lk ? c : c - Lk;
+            asrc = c < Lk ? S1s : U2s;
+            abase = (int64_t)(cc / k) * d_in * k + cc % k;  // + r * k
+        }
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int64_t r = row0 + ty + 8 * i, c = col0 + tx;
+            const int r = row0 + ty + 8 * i;
             float v = 0.f;
             if (r < rows && c < cols) {
                 if (isA) {  // (c_in = r, rank = c)
-                    if (c < Lk) v = ld_f<T>(S1s, ((c / k) * d_in + r) * k + c % k);
-                    else if (c < 2 * Lk) v = ld_f<T>(U2s, (((c - Lk) / k) * d_in + r) * k + (c - Lk) % k);
+                    if (asrc) v = ld_f<T>(asrc, abase + (int64_t)r * k);
                 } else {    // (rank = r, c_out = c)
-                    if (r < Lk) v = ld_f<T>(U1s, r * d_out + c);
-                    else if (r < 2 * Lk) v = ld_f<T>(S2s, (r - Lk) * d_out + c);
+                    if (r < Lk) v = ld_f<T>(U1s, (int64_t)r * d_out + c);
+                    else if (r < 2 * Lk) v = ld_f<T>(S2s, (int64_t)(r - Lk) * d_out + c);
                 }
             }
             if constexpr (sizeof(T) == 4) v = dev::tf32_rna(v);
             tile[ty + 8 * i][tx] = v;
             void* nat = isA ? Acat : Bcat;
             if (nat && r < rows && c < cols) {
-                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(nat)[r * cols + c] = __float2bfloat16_rn(v);
-                else reinterpret_cast<float*>(nat)[r * cols + c] = v;
+                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(nat)[(int64_t)r * cols + c] = __float2bfloat16_rn(v);
+                else reinterpret_cast<float*>(nat)[(int64_t)r * cols + c] = v;
             }
         }
         void* tr = isA ? AcatT : BcatT;
@@ -250,11 +263,11 @@ __global__ void __launch_bounds__(256) pack_tiles_kernel(const void* S1s, const 
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-            const int64_t c = col0 + ty + 8 * i, r = row0 + tx;  // transposed: [cols][rows]
-            if (r < rows && c < cols) {
+            const int cT = col0 + ty + 8 * i, rT = row0 + tx;  // transposed: [cols][rows]
+            if (rT < rows && cT < cols) {
                 const float v = tile[tx][ty + 8 * i];
-                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(tr)[c * rows + r] = __float2bfloat16_rn(v);
-                else reinterpret_cast<float*>(tr)[c * rows + r] = v;
+                if constexpr (sizeof(T) == 2) reinterpret_cast<__nv_bfloat16*>(tr)[(int64_t)cT * rows + rT] = __float2bfloat16_rn(v);
+                else reinterpret_cast<float*>(tr)[(int64_t)cT * rows + rT] = v;
             }
         }
     }
