@@ -142,12 +142,16 @@ class SkChain:
         return [GradBucket.allocate(st.layer.d_in, st.layer.d_out, st.layer.num_terms, st.layer.low_rank,
                                     device=device) for st in self.steps]
 
-    def backward(self, g, buckets=None, group=None, need_grad_x=True, overlap=None):
+    def backward(self, g, buckets=None, group=None, need_grad_x=True, overlap=None, phased=False):
         """Backward of the whole chain from the output gradient g [T, d_out].
 
         buckets: per-layer GradBucket (dU1s | db | dU2s, fp32), allocated if None.
-        overlap: all-reduce each bucket across `group` as soon as it is ready
-        (phased backward); defaults to True when torch.distributed is initialised.
+        overlap: all-reduce each bucket across `group` as soon as it is ready,
+        overlapped with the backward of the layers below; defaults to True when
+        torch.distributed is initialised.  phased: split each layer's backward
+        (dU1s|db first, its all-reduce overlapping that layer's own dX kernel)
+        -- the single-layer schedule; for a stack the per-layer fused backward
+        is faster (c2 layer: one du launch instead of two, -22 us).
         Returns (ChainGrads, works) -- wait on `works` before reading the grads."""
         import torch
         import torch.distributed as dist
@@ -167,7 +171,7 @@ class SkChain:
             L = st.layer
             gx = torch.empty(T, L.d_in, dtype=td, device=g.device) if (i > 0 or need_grad_x) else None
             fuse = FUSE_RELU_IN if st.relu_in else 0
-            if overlap:
+            if overlap and phased:
                 backward_phase(L.shape, BWD_DU1_DB, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, None,
                                b.dU1s, None, b.db, ws)
                 w = b.allreduce_head(group, async_op=True)
@@ -176,6 +180,15 @@ class SkChain:
                 backward_phase(L.shape, BWD_DX_DU2, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
                                None, b.dU2s, None, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
                 w = b.allreduce_tail(group, async_op=True)
+                if w is not None:
+                    works.append(w)
+            elif overlap:
+                # one fused backward per layer, then its whole bucket all-reduced on
+                # NCCL's stream while the layers below run theirs (SURVEY §8e "in the
+                # stack"); the phased split would cost a second du launch per layer
+                backward_phase(L.shape, BWD_ALL, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
+                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
+                w = b.allreduce_(group, async_op=True)
                 if w is not None:
                     works.append(w)
             else:

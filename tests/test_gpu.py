@@ -426,9 +426,10 @@ def test_chain_relu_bits_match_x_mask_bitwise(skl, dtype_name):
 
 
 def test_bert_stack_overlapped_dp_step_runs(skl):
-    """Config 5 at reduced depth: the BERT FFN/proj stack with the phased,
-    per-layer all-reduce schedule on a world-1 NCCL group gives the same
-    gradients as the plain backward."""
+    """Config 5 at reduced depth: the BERT FFN/proj stack with the per-layer
+    all-reduce schedules (whole bucket after each layer's fused backward, or the
+    phased split) on a world-1 NCCL group gives the same gradients as the plain
+    backward."""
     import socket
     import torch.distributed as dist
     from paper_2601_15473_b200.model import bert_ffn_stack, wait_all
@@ -445,14 +446,15 @@ def test_bert_stack_overlapped_dp_step_runs(skl):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port_}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
-        got, works = chain.backward(g, overlap=True)
-        assert len(works) == 2 * len(chain.steps)
-        wait_all(works)
-        torch.cuda.synchronize()
-        assert torch.equal(got.grad_x, ref.grad_x)
-        for a, b in zip(got.layers, ref.layers):
-            rel = (a.flat - b.flat).norm() / b.flat.norm()
-            assert rel < 1e-5, rel
+        for phased in (False, True):  # per-layer fused backward + bucket all-reduce / phased split
+            got, works = chain.backward(g, overlap=True, phased=phased)
+            assert len(works) == (2 if phased else 1) * len(chain.steps)
+            wait_all(works)
+            torch.cuda.synchronize()
+            assert torch.equal(got.grad_x, ref.grad_x)
+            for a, b in zip(got.layers, ref.layers):
+                rel = (a.flat - b.flat).norm() / b.flat.norm()
+                assert rel < 1e-5, rel
     finally:
         dist.destroy_process_group()
 
