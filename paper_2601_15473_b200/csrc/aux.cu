@@ -221,8 +221,12 @@ __global__ void __launch_bounds__(256) pack_tiles_kernel(const void* S1s, const 
     const int tb_c = (d_out + 31) / 32;
     const int nA = ta_r * ta_c, nB = ta_r * tb_c;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    if (bias32 && blockIdx.x == 0)
-        for (int i = threadIdx.x; i < d_out; i += blockDim.x) bias32[i] = bias ? ld_f<T>(bias, i) : 0.f;
+    // the bias -> fp32 copy is spread over the whole grid: block 0 looping over
+    // it alone was the kernel's critical path (c2-TF32: 13.8 us with the SMs
+    // active half of that; the loop's dependent load/store pairs serialise)
+    if (bias32)
+        for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < d_out; i += gridDim.x * blockDim.x)
+            bias32[i] = bias ? ld_f<T>(bias, i) : 0.f;
     for (int b = blockIdx.x; b < nA + nB; b += gridDim.x) {
         const bool isA = b < nA;
         int row0, col0, rows, cols;  // natural layout: A = [d_in][R_pad], B = [R_pad][d_out]
