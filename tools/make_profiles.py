@@ -1,0 +1,47 @@
+# Regenerate profiles/ summaries from gpurun_out/{launches.csv, r1_full.ncu-rep}.
+import csv, subprocess, json
+from collections import OrderedDict
+rows = list(csv.reader(open('gpurun_out/launches.csv')))
+hi = [i for i, r in enumerate(rows) if r and r[0] == 'ID'][0]
+h = rows[hi]; data = rows[hi + 1:]
+ci = {k: i for i, k in enumerate(h)}
+conv = {'nsecond': 1e-3, 'ns': 1e-3, 'usecond': 1.0, 'us': 1.0, 'msecond': 1e3, 'ms': 1e3}
+agg = OrderedDict()
+for r in data:
+    if len(r) < len(h) or r[ci['Metric Name']] != 'gpu__time_duration.sum': continue
+    agg.setdefault(r[ci['Kernel Name']], []).append(float(r[ci['Metric Value']].replace(',', '')) * conv[r[ci['Metric Unit']]])
+out = ["# r1 launch list: ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, serialised: compare SHARES)",
+       "# command: python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-sweep",
+       "# (du is a plain cluster launch -- no cooperative launch -- so ncu replays it as run)",
+       "# kernel, launches, mean_us, min_us, max_us"]
+step = []
+for k, v in agg.items():
+    tag = 'b2b_fwd ' if 'b2b_kernel<2, 1' in k else 'b2b_bwd ' if 'b2b_kernel<2, 2' in k else 'du_fused ' if 'du_kernel' in k else ''
+    out.append("%s%s, %d, %.1f, %.1f, %.1f" % (tag, k[:52], len(v), sum(v) / len(v), min(v), max(v)))
+    if tag: step.append(sum(v) / len(v))
+out.append("# c2 step (b2b_fwd + b2b_bwd + du) under ncu: %.1f us; shares %s" % (sum(step), ", ".join("%.1f%%" % (100 * x / sum(step)) for x in step)))
+open('profiles/r1_launches.txt', 'w').write("\n".join(out) + "\n")
+print("\n".join(out[-4:]))
+o = subprocess.run(["ncu", "-i", "gpurun_out/r1_full.ncu-rep", "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+rows = list(csv.reader(o.splitlines()))
+h = rows[0]; units = rows[1]; ci = {k: i for i, k in enumerate(h)}
+keys = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed', 'sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active',
+        'sm__pipe_tensor_cycles_active.max.pct_of_peak_sustained_elapsed', 'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed',
+        'lts__throughput.avg.pct_of_peak_sustained_elapsed', 'lts__t_sector_hit_rate.pct', 'gpc__cycles_elapsed.avg.per_second',
+        'launch__registers_per_thread', 'launch__grid_size', 'launch__block_size', 'launch__cluster_dim_x', 'launch__shared_mem_per_block_dynamic']
+lines = ["# r1 ncu --set full --clock-control none --import-source on (one launch each; c2 workload via scratch/one_step.py)",
+         "# gpc__cycles_elapsed.avg.per_second = the SM clock during the capture", ""]
+traffic = {}
+for r in rows[2:]:
+    name = r[ci['Kernel Name']]
+    tag = 'b2b_fwd' if 'b2b_kernel<2, 1' in name else 'b2b_bwd' if 'b2b_kernel<2, 2' in name else 'du_fused' if 'du_kernel' in name else name[:30]
+    lines.append("[%s] %s" % (tag, name[:100]))
+    for k in keys:
+        if k in ci: lines.append("  %s = %s %s" % (k, r[ci[k]], units[ci[k]]))
+    val = lambda k: float(r[ci[k]].replace(',', '')) * {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9}.get(units[ci[k]], 1)
+    traffic[tag] = val('dram__bytes_read.sum') + val('dram__bytes_write.sum')
+    lines.append("")
+open('profiles/r1_ncu_full_summary.txt', 'w').write("\n".join(lines))
+json.dump(traffic, open('profiles/traffic.json', 'w'), indent=1)
+print(traffic)
