@@ -114,6 +114,8 @@ CASES = [
     (256, 512, 3, 32, 129),        # R = 192 (single GEMM1 chunk), ragged
     (512, 256, 4, 64, 200),        # R = 512, d_out < d_in
     (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
+    (768, 768, 1, 128, 600),       # c5 projection: R = 256 (one chunk, saves deferred after hready), du M = 128
+    (1024, 512, 1, 64, 20000),     # R = 128 ping-pong H: > 74 pair tiles, so CTAs alternate TMEM regions
 ]
 
 
@@ -172,6 +174,7 @@ TF32_CASES = [
     (768, 3072, 2, 128, 200),      # c2 shape, R = 512 (TF32 H through HBM)
     (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
     (96, 160, 3, 8, 77),           # k % 64 != 0, odd tokens
+    (512, 512, 1, 64, 20000),      # R = 128 ping-pong H in TF32, several tiles per CTA
 ]
 
 
