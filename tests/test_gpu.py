@@ -388,7 +388,8 @@ def test_fused_relu_mask_is_exact_at_scale(skl, dtype_name, unfused):
 def test_chain_relu_bits_match_x_mask_bitwise(skl, dtype_name):
     """The 1-bit ReLU mask carried from FFN1's forward to FFN2's backward
     (SKL_FUSE_RELU_BITS) gives bitwise the same activations and gradients as
-    re-reading the ReLU output, at a c5 FFN shape with ragged T."""
+    re-reading the ReLU output, at a c5 FFN shape with ragged T and several
+    row tiles per CTA."""
     from paper_2601_15473_b200.model import Relu, SkChain
     dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
     td = skl.torch_dtype(dtype)
@@ -398,7 +399,7 @@ def test_chain_relu_bits_match_x_mask_bitwise(skl, dtype_name):
     if not (skl.relu_bits_supported(l1.shape) and skl.relu_bits_supported(l2.shape)):
         assert os.environ.get("SKL_FORCE_UNFUSED") is not None  # only the unfused chain lacks them
         pytest.skip("1-bit masks are a fused-kernel feature")
-    T = 5000
+    T = 20003  # > 74 pair tiles: the bits of the next row tile are prefetched across tiles
     gen = torch.Generator(device="cuda").manual_seed(3)
     x = torch.randn(T, 768, device="cuda", generator=gen).to(td)
     g = torch.randn(T, 768, device="cuda", generator=gen).to(td)
