@@ -704,3 +704,29 @@ def test_from_dense_is_unbiased_over_sketch_seeds(skl):
         return torch.stack(v).var(0, unbiased=True).mean().item()
     ratio = mean_var(4, 10) / mean_var(1, 20)
     assert 0.2 <= ratio <= 0.35, ratio
+
+
+def test_sketched_conv_from_dense_is_unbiased(skl):
+    """test_nn_montecarlo.cpp:80-114 on the device path: a SkConv2d whose inner
+    SKLinear comes from sk_linear_from_dense of a dense conv's lowered weight
+    (sk_conv2d_from_dense) averages, over 600 sketch seeds, to the dense conv within
+    3 standard errors per output.  Channels widened 2 -> 4 for the ABI's 16-byte rows."""
+    import torch.nn.functional as F
+    from paper_2601_15473_b200 import derive_seed
+    from paper_2601_15473_b200.conv import ConvShape, SkConv2d
+    c_in, c_out, kh = 4, 4, 3
+    shape = ConvShape(c_in, c_out, kh, kh, 1, 0)
+    gen = torch.Generator(device="cuda").manual_seed(31)
+    Wc = torch.randn(c_out, c_in, kh, kh, device="cuda", generator=gen)      # [c_out][c_in][kh][kw]
+    b = torch.tensor([0.2, -0.1, 0.05, 0.0], device="cuda")
+    x = torch.randn(1, c_in, 5, 5, device="cuda", generator=gen)
+    expect = F.conv2d(x.double(), Wc.double(), b.double())                   # [1, c_out, 3, 3]
+    W = Wc.reshape(c_out, c_in * kh * kh)   # lowered feature order (channel, kernel row, kernel col)
+    ys = []
+    for s in range(600):
+        inner = skl.SkLinear.from_dense(W, b, 1, 4, seed=derive_seed(888, s), dtype=skl.F32_TF32)
+        ys.append(SkConv2d(shape, 1, 4, dtype=skl.F32_TF32, inner=inner).forward(x).double())
+    ys = torch.stack(ys)
+    mean, se = ys.mean(0), ys.std(0, unbiased=True) / 600 ** 0.5
+    slack = 2e-3 * expect.abs() + 1e-4  # TF32 operand rounding
+    assert bool(((mean - expect).abs() <= 3 * se + slack).all()), ((mean - expect).abs() / se).max()
