@@ -730,3 +730,35 @@ def test_sketched_conv_from_dense_is_unbiased(skl):
     mean, se = ys.mean(0), ys.std(0, unbiased=True) / 600 ** 0.5
     slack = 2e-3 * expect.abs() + 1e-4  # TF32 operand rounding
     assert bool(((mean - expect).abs() <= 3 * se + slack).all()), ((mean - expect).abs() / se).max()
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_from_dense_zero_weights_leaves_bias(skl, dtype_name):
+    """test_nn_layers.cpp:99-111: sk_linear_from_dense of a zero W has zero U1s / U2s
+    and its forward is exactly the bias, on the device path."""
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    d_in, d_out = 16, 8
+    b = torch.tensor([1.5, -2.0, 0.25, 3.0, -1.0, 0.5, 0.0, 2.0], device="cuda").to(td)
+    lyr = skl.SkLinear.from_dense(torch.zeros(d_out, d_in, device="cuda", dtype=td), b, 2, 8, seed=17, dtype=dtype)
+    assert not bool(lyr.U1s.any()) and not bool(lyr.U2s.any())
+    x = torch.randn(40, d_in, device="cuda").to(td)
+    y = lyr.forward(x)
+    torch.cuda.synchronize()
+    assert torch.equal(y, b.expand(40, d_out))
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+def test_conv_zero_input_gives_bias_colored_maps(skl, dtype_name):
+    """test_nn_layers.cpp:263-281 on the device path (channels widened for the
+    ABI's 16-byte rows): a zero image maps to each output channel's bias."""
+    from paper_2601_15473_b200.conv import ConvShape, SkConv2d
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    td = skl.torch_dtype(dtype)
+    conv = SkConv2d(ConvShape(8, 8, 3, 3, 1, 0), 1, 8, seed=59, dtype=dtype)
+    bias = torch.linspace(-0.7, 0.7, 8, device="cuda").to(td)
+    conv.inner.bias.copy_(bias)
+    y = conv.forward(torch.zeros(2, 8, 5, 5, device="cuda", dtype=td))
+    torch.cuda.synchronize()
+    assert y.shape == (2, 8, 3, 3)
+    assert torch.equal(y, bias.view(1, 8, 1, 1).expand(2, 8, 3, 3))
