@@ -116,6 +116,8 @@ CASES = [
     (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
     (768, 768, 1, 128, 600),       # c5 projection: R = 256 (one chunk, saves deferred after hready), du M = 128
     (1024, 512, 1, 64, 20000),     # R = 128 ping-pong H: > 74 pair tiles, so CTAs alternate TMEM regions
+    (4096, 4096, 1, 16, 300),      # c4 L1 k16 shape: R = 32 on d = 4096 (packed panels, 32 GEMM2 tiles)
+    (4096, 4096, 4, 64, 257),      # c4 L4 k64 shape: R = 512, ragged T
 ]
 
 
@@ -175,6 +177,8 @@ TF32_CASES = [
     (128, 64, 1, 16, 50),          # small rank R = 32 (padded to 64)
     (96, 160, 3, 8, 77),           # k % 64 != 0, odd tokens
     (512, 512, 1, 64, 20000),      # R = 128 ping-pong H in TF32, several tiles per CTA
+    (768, 768, 1, 128, 600),       # c5 projection shape in TF32 (R = 256, the widest TMEM-only TF32 H)
+    (4096, 4096, 2, 64, 130),      # c4 TF32 L2 k64 shape (R = 256), ragged T
 ]
 
 
