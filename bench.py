@@ -517,8 +517,9 @@ def main():
             "data": "synthetic (seeded Gaussian activations; sketches/U from the reference seed chain)",
             "config": {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
                        "tokens_per_gpu": T, "global_tokens": world * T,
-                       "parallelism": f"dp{world} (token sharding; NCCL all-reduce of dU1s|db overlapped with "
-                                      f"the dX kernel, then dU2s)",
+                       "parallelism": (f"dp{world} (token sharding; NCCL all-reduce of dU1s|db overlapped with "
+                                       f"the dX kernel, then dU2s)") if world > 1
+                                      else "dp1 (one GPU: fused backward, no collective)",
                        "l2": "inputs larger than L2 (X 50 MB + G 201 MB read, Y 201 MB written per step)"},
             "roofline": roof,
             "step_tflops": step_roof, "step_roofline_frac": step_roof / peak_tf,
