@@ -5,7 +5,7 @@ import paper_2601_15473_b200 as skl
 dev = torch.device("cuda", 0)
 d_in, d_out, l, k = [int(v) for v in sys.argv[1:5]]
 which = sys.argv[5]
-T = 32768
+T = int(os.environ.get("T", "32768"))
 s = skl.shape(d_in, d_out, l, k, skl.BF16)
 td = torch.bfloat16
 S1s = torch.empty(l, d_in, k, dtype=td, device=dev); S2s = torch.empty(l, k, d_out, dtype=td, device=dev)
