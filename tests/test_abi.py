@@ -96,3 +96,31 @@ def test_unsupported_alignment_is_reported():
     s = skl.shape(6, 8, 2, 3)  # reference test shape: d_in*2 bytes not 16-B aligned
     rc = skl.lib().sketched_linear_forward(ctypes.byref(s), 4, *([ctypes.c_void_p(16)] * 9), 1 << 30, None)
     assert rc == 5 and b"multiples of" in skl.lib().skl_last_error()
+
+
+def test_relu_bits_contract():
+    """1-bit ReLU mask entry points (skl.h SKL_FUSE_RELU_BITS): row stride in
+    64-column groups, support query, and parameter errors raised before any
+    device work."""
+    import ctypes
+    assert skl.relu_bits_row_words(1) == 2
+    assert skl.relu_bits_row_words(64) == 2
+    assert skl.relu_bits_row_words(160) == 6
+    assert skl.relu_bits_row_words(3072) == 96
+    assert skl.relu_bits_supported(skl.shape(768, 3072, 2, 128, skl.BF16))       # CTA-pair b2b kernel
+    assert not skl.relu_bits_supported(skl.shape(4096, 4096, 3, 256, skl.BF16))  # R = 1536: unfused chain
+    lib = skl.lib()
+    s = skl.shape(768, 3072, 2, 128, skl.BF16)
+    vp = ctypes.c_void_p
+    dummy = vp(16)
+    # BITS without RELU_OUT, and RELU_OUT|BITS without a buffer: parameter errors
+    # forward_bits(shape, T, fuse, x, S1s, S2s, U1s, U2s, bias, y, saved, relu_bits, ws, ws_bytes, stream)
+    st = lib.sketched_linear_forward_bits(ctypes.byref(s), 8, skl.FUSE_RELU_BITS, *([dummy] * 8), dummy, None, 0, None)
+    assert st == 2
+    st = lib.sketched_linear_forward_bits(ctypes.byref(s), 8, skl.FUSE_RELU_OUT | skl.FUSE_RELU_BITS,
+                                          *([dummy] * 8), None, None, 0, None)
+    assert st == 2
+    # backward_bits(shape, T, phases, fuse, g, x, saved, S1s, S2s, U1s, U2s, gx, dU1s, dU2s, db, relu_bits, ws, ...)
+    st = lib.sketched_linear_backward_bits(ctypes.byref(s), 8, skl.BWD_ALL, skl.FUSE_RELU_BITS, *([dummy] * 11),
+                                           dummy, None, 0, None)
+    assert st == 2
