@@ -198,6 +198,49 @@ class Oracle:
         self._check(rc, "sk_backward")
         return gx, gu1, gu2, gb
 
+    # -- DenseLinear (nn_layers.cpp:32-59) ------------------------------------
+    def _dense_fn(self, name, argtypes):
+        f = self._fn(name)
+        f.argtypes = argtypes
+        return f
+
+    def dense_init(self, d_in, d_out, seed):
+        """dense_linear_init -> (w [d_out, d_in], b [d_out])."""
+        w, b = np.empty((d_out, d_in)), np.empty(d_out)
+        rc = self._dense_fn("dense_init", [_u64] * 3 + [_dp] * 2)(d_in, d_out, seed, _p(w), _p(b))
+        if self.kind == "reference":
+            self._check(rc, "dense_init")
+        return w, b
+
+    def dense_forward(self, w, b, x):
+        """DenseLinear::forward, column convention: x [d_in, T] -> y [d_out, T]."""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        b = np.ascontiguousarray(b, dtype=np.float64)
+        d_out, d_in = w.shape
+        if x.shape[0] != d_in:
+            raise ShapeError("DenseLinear::forward: input rows != d_in")
+        y = np.empty((d_out, x.shape[1]))
+        rc = self._dense_fn("dense_forward", [_u64] * 3 + [_dp] * 4)(d_in, d_out, x.shape[1], _p(w), _p(b), _p(x),
+                                                                      _p(y))
+        self._check(rc, "dense_forward")
+        return y
+
+    def dense_backward(self, w, x, g):
+        """DenseLinear::backward -> (grad_x [d_in, T], grad_w [d_out, d_in], grad_b [d_out])."""
+        w = np.ascontiguousarray(w, dtype=np.float64)
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        d_out, d_in = w.shape
+        if x.shape[0] != d_in or g.shape[0] != d_out or x.shape[1] != g.shape[1]:
+            raise ShapeError("DenseLinear::backward: shape mismatch")
+        T = x.shape[1]
+        gx, gw, gb = np.empty((d_in, T)), np.empty((d_out, d_in)), np.empty(d_out)
+        rc = self._dense_fn("dense_backward", [_u64] * 3 + [_dp] * 6)(d_in, d_out, T, _p(w), _p(x), _p(g), _p(gx),
+                                                                       _p(gw), _p(gb))
+        self._check(rc, "dense_backward")
+        return gx, gw, gb
+
     # -- reference-only -----------------------------------------------------
     def time_fwd_bwd(self, d_in, d_out, l, k, T, seed=42, threads=1, trials=3, warmup=1):
         """Reference SkLinear fwd+bwd timed by bench::time_op (ms mean, ms std)."""

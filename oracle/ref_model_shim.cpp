@@ -44,7 +44,7 @@ extern "C" {
 const char* ref_model_last_error(void) { return g_merr.c_str(); }
 
 // Build a Linear/ReLU chain with the reference's own constructors and save it.
-// spec: n rows of {type (0 = SKLinear, 1 = ReLU), d_in, d_out, l, k, seed, dist}.
+// spec: n rows of {type (0 = SKLinear, 1 = ReLU, 2 = Linear), d_in, d_out, l, k, seed, dist}.
 // SKLinear layers are sk_linear_fresh(d_in, d_out, l, k, seed, dist) with bias
 // gaussian_matrix(1, d_out, derive_seed(seed, 11)) * 0.5 (a fresh bias is zero).
 int ref_model_save_chain(const char* path, int f32, int n, const std::uint64_t* spec) {
@@ -57,6 +57,11 @@ int ref_model_save_chain(const char* path, int f32, int n, const std::uint64_t* 
             nl.name = "layer" + std::to_string(i);
             if (s[0] == 1) {
                 nl.layer = rnla::nn::Relu{};
+            } else if (s[0] == 2) {  // DenseLinear: dense_linear_init(d_in, d_out, seed), bias as below
+                rnla::nn::DenseLinear d = rnla::nn::dense_linear_init(s[1], s[2], s[5]);
+                const rnla::Matrix b = rnla::sketch::gaussian_matrix(1, s[2], rnla::derive_seed(s[5], 11));
+                for (std::size_t j = 0; j < s[2]; ++j) d.b[j] = 0.5 * b.data()[j];
+                nl.layer = std::move(d);
             } else {
                 rnla::nn::SkLinear l = rnla::nn::sk_linear_fresh(
                     s[1], s[2], s[3], s[4], s[5], s[6] ? rnla::sketch::SketchDist::Rademacher

@@ -165,6 +165,38 @@ int ref_sk_backward(std::uint64_t d_in, std::uint64_t d_out, std::uint64_t l, st
     });
 }
 
+// DenseLinear (nn_layers.cpp:32-59) through the reference's own API.
+int ref_dense_init(std::uint64_t d_in, std::uint64_t d_out, std::uint64_t seed, double* w, double* b) {
+    return guard([&] {
+        const auto layer = rnla::nn::dense_linear_init(d_in, d_out, seed);
+        to_ptr(layer.w, w);
+        std::memcpy(b, layer.b.data(), d_out * sizeof(double));
+    });
+}
+
+int ref_dense_forward(std::uint64_t d_in, std::uint64_t d_out, std::uint64_t T, const double* w, const double* b,
+                      const double* x, double* y) {
+    return guard([&] {
+        rnla::nn::DenseLinear layer;
+        layer.w = from_ptr(d_out, d_in, w);
+        layer.b.assign(b, b + d_out);
+        to_ptr(layer.forward(from_ptr(d_in, T, x)), y);
+    });
+}
+
+int ref_dense_backward(std::uint64_t d_in, std::uint64_t d_out, std::uint64_t T, const double* w, const double* x,
+                       const double* g, double* gx, double* gw, double* gb) {
+    return guard([&] {
+        rnla::nn::DenseLinear layer;
+        layer.w = from_ptr(d_out, d_in, w);
+        layer.b.assign(d_out, 0.0);
+        const auto grads = layer.backward(from_ptr(d_in, T, x), from_ptr(d_out, T, g));
+        to_ptr(grads.grad_x, gx);
+        to_ptr(grads.grad_w, gw);
+        std::memcpy(gb, grads.grad_b.data(), d_out * sizeof(double));
+    });
+}
+
 // CPU baseline: the reference's own SkLinear forward+backward timed by the
 // reference's own harness (bench::time_op, bench.cpp:28-76) on `threads`
 // OpenMP workers.  Inputs follow BASELINE.md §3: layer sk_linear_fresh(seed),

@@ -256,3 +256,40 @@ done:
     free(gx1); free(u2t); free(u2tg); free(u2tgt); free(gx2);
     return rc;
 }
+
+/* ---- nn_layers.cpp:51-59 dense_linear_init: w = gaussian_matrix(d_out, d_in,
+ * seed) stream order times sqrt(2/(d_in+d_out)); zero bias ---------------- */
+void orc_dense_init(uint64_t d_in, uint64_t d_out, uint64_t seed, double* w, double* b) {
+    orc_gauss g; gauss_init(&g, seed);
+    const double std_dev = sqrt(2.0 / (double)(d_in + d_out));
+    for (uint64_t i = 0; i < d_out * d_in; ++i) w[i] = gauss_next(&g) * std_dev;
+    for (uint64_t i = 0; i < d_out; ++i) b[i] = 0.0;
+}
+
+/* ---- nn_layers.cpp:32-37 DenseLinear::forward: y = w x + b (column convention) */
+int orc_dense_forward(uint64_t d_in, uint64_t d_out, uint64_t T, const double* w, const double* b,
+                      const double* x, double* y) {
+    gemm_rows(w, x, y, d_out, d_in, T);
+    for (uint64_t i = 0; i < d_out; ++i)                              /* add_bias_columns :15-21 */
+        for (uint64_t j = 0; j < T; ++j) y[i * T + j] += b[i];
+    return ORC_OK;
+}
+
+/* ---- nn_layers.cpp:39-49 DenseLinear::backward ------------------------- */
+int orc_dense_backward(uint64_t d_in, uint64_t d_out, uint64_t T, const double* w, const double* x,
+                       const double* g, double* gx, double* gw, double* gb) {
+    double* xt = (double*)malloc(T * d_in * sizeof(double));
+    double* wt = (double*)malloc(d_in * d_out * sizeof(double));
+    if (!xt || !wt) { free(xt); free(wt); return ORC_ERR_ALLOC; }
+    transpose(x, d_in, T, xt);
+    gemm_rows(g, xt, gw, d_out, T, d_in);                             /* :44 grad_w = G x^T */
+    transpose(w, d_out, d_in, wt);
+    gemm_rows(wt, g, gx, d_in, d_out, T);                             /* :45 grad_x = w^T G */
+    for (uint64_t i = 0; i < d_out; ++i) {                            /* :46 row_sums */
+        double s = 0.0;
+        for (uint64_t j = 0; j < T; ++j) s += g[i * T + j];
+        gb[i] = s;
+    }
+    free(xt); free(wt);
+    return ORC_OK;
+}

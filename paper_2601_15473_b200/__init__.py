@@ -39,7 +39,8 @@ ABI_SYMBOLS = (
     "sketched_linear_forward_ex", "sketched_linear_backward_ex", "skl_from_dense", "skl_from_dense_workspace_size",
     "skl_conv_workspace_size", "sketched_conv2d_forward", "sketched_conv2d_backward",
     "sketched_linear_forward_bits", "sketched_linear_backward_bits", "skl_relu_bits_row_words",
-    "skl_relu_bits_supported",
+    "skl_relu_bits_supported", "skl_dense_workspace_size", "skl_dense_init", "dense_linear_forward",
+    "dense_linear_backward",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
 FUSE_RELU_OUT, FUSE_RELU_IN, FUSE_RELU_BITS = 1, 2, 4
@@ -66,6 +67,10 @@ class LoadError(SklError):
 class _Shape(ctypes.Structure):
     _fields_ = [("d_in", ctypes.c_int64), ("d_out", ctypes.c_int64), ("num_terms", ctypes.c_int64),
                 ("low_rank", ctypes.c_int64), ("dtype", ctypes.c_int)]
+
+
+class _DenseShape(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_int64), ("d_out", ctypes.c_int64), ("dtype", ctypes.c_int)]
 
 
 class _ParamCount(ctypes.Structure):
@@ -130,6 +135,11 @@ def lib() -> ctypes.CDLL:
     L.skl_relu_bits_row_words.argtypes = [i64]
     L.skl_relu_bits_supported.argtypes = [sp]
     L.skl_allreduce_grads.argtypes = [vp, vp, sz, vp]
+    dp = ctypes.POINTER(_DenseShape)
+    L.skl_dense_workspace_size.argtypes = [dp, i64, ctypes.POINTER(sz), ctypes.POINTER(sz)]
+    L.skl_dense_init.argtypes = [dp, u64, vp, vp, vp]
+    L.dense_linear_forward.argtypes = [dp, i64, ctypes.c_uint] + [vp] * 4 + [vp, sz, vp]
+    L.dense_linear_backward.argtypes = [dp, i64, ctypes.c_uint] + [vp] * 6 + [vp, sz, vp]
     L.skl_launch_count.restype = u64
     L.skl_profile_enable.argtypes = [ctypes.c_int]
     L.skl_profile_enable.restype = ctypes.c_int
@@ -211,9 +221,34 @@ def init_params(s: _Shape, seed, U1s, U2s, stream=None):
     _check(lib().skl_init_params(ctypes.byref(s), seed, _ptr(U1s), _ptr(U2s), _stream(stream)))
 
 
+def _validate(s: _Shape, elem=(), f32=(), device=None):
+    """The C-ABI takes raw device pointers: reject what it would misread.  `elem`
+    are (name, tensor) pairs in the layer's element type, `f32` fp32 gradients;
+    None entries are skipped.  Every tensor must be a contiguous CUDA tensor on
+    one device."""
+    import torch
+    want = torch_dtype(s.dtype)
+    for group, dt in ((elem, want), (f32, torch.float32)):
+        for name, t in group:
+            if t is None:
+                continue
+            if not isinstance(t, torch.Tensor) or not t.is_cuda:
+                raise ParameterError(2, f"{name}: expected a CUDA tensor")
+            if t.dtype != dt:
+                raise ParameterError(2, f"{name}: dtype {t.dtype}, expected {dt}")
+            if not t.is_contiguous():
+                raise ParameterError(2, f"{name}: tensor must be contiguous")
+            if device is None:
+                device = t.device
+            elif t.device != device:
+                raise ParameterError(2, f"{name}: on {t.device}, expected {device}")
+
+
 def forward(s: _Shape, x, S1s, S2s, U1s, U2s, bias, y, saved, workspace, stream=None, fuse=0, relu_bits=None):
     """sketched_linear_forward(_ex/_bits): fuse = FUSE_RELU_OUT applies the following ReLU;
     with relu_bits (int32 [T, relu_bits_row_words(d_out)]) it also writes the 1-bit ReLU mask."""
+    _validate(s, (("x", x), ("S1s", S1s), ("S2s", S2s), ("U1s", U1s), ("U2s", U2s), ("bias", bias), ("y", y),
+                  ("saved", saved)))
     T = x.shape[0]
     if relu_bits is not None:
         _check(lib().sketched_linear_forward_bits(ctypes.byref(s), T, fuse | FUSE_RELU_BITS, _ptr(x), _ptr(S1s),
@@ -237,6 +272,8 @@ def relu_bits_supported(s: _Shape) -> bool:
 
 
 def backward(s: _Shape, g, x, saved, S1s, S2s, U1s, U2s, grad_x, dU1s, dU2s, db, workspace, stream=None):
+    _validate(s, (("g", g), ("x", x), ("saved", saved), ("S1s", S1s), ("S2s", S2s), ("U1s", U1s), ("U2s", U2s),
+                  ("grad_x", grad_x)), (("dU1s", dU1s), ("dU2s", dU2s), ("db", db)))
     T = x.shape[0]
     _check(lib().sketched_linear_backward(ctypes.byref(s), T, _ptr(g), _ptr(x), _ptr(saved), _ptr(S1s), _ptr(S2s),
                                           _ptr(U1s), _ptr(U2s), _ptr(grad_x), _ptr(dU1s), _ptr(dU2s), _ptr(db),
@@ -249,6 +286,8 @@ def backward_phase(s: _Shape, phases, g, x, saved, S1s, S2s, U1s, U2s, grad_x, d
     """sketched_linear_backward_ex/_bits: phases BWD_DU1_DB (dU1s, db) / BWD_DX_DU2 (grad_x, dU2s) / BWD_ALL;
     fuse = FUSE_RELU_IN masks grad_x by (x > 0) (the preceding ReLU's backward), read from
     relu_bits (the previous layer's 1-bit mask) when given."""
+    _validate(s, (("g", g), ("x", x), ("saved", saved), ("S1s", S1s), ("S2s", S2s), ("U1s", U1s), ("U2s", U2s),
+                  ("grad_x", grad_x)), (("dU1s", dU1s), ("dU2s", dU2s), ("db", db)))
     T = x.shape[0]
     if relu_bits is not None:
         _check(lib().sketched_linear_backward_bits(ctypes.byref(s), T, phases, fuse | FUSE_RELU_BITS, _ptr(g), _ptr(x),
@@ -399,3 +438,102 @@ class SkLinear:
         backward(self.shape, g, x, saved, self.S1s, self.S2s, self.U1s, self.U2s, gx, du1, du2, db,
                  self.workspace(T))
         return Grads(gx, du1, du2, db)
+
+
+# --------------------------------------------------------------------------- DenseLinear
+def dense_shape(d_in, d_out, dtype=BF16) -> _DenseShape:
+    return _DenseShape(d_in, d_out, dtype)
+
+
+def dense_workspace_size(s: _DenseShape, T: int):
+    f, b = ctypes.c_size_t(), ctypes.c_size_t()
+    _check(lib().skl_dense_workspace_size(ctypes.byref(s), T, ctypes.byref(f), ctypes.byref(b)))
+    return f.value, b.value
+
+
+def dense_forward(s: _DenseShape, x, W, bias, y, workspace, stream=None, fuse=0):
+    """dense_linear_forward: y = x·Wᵀ + b (fuse = FUSE_RELU_OUT applies a following ReLU)."""
+    _validate(s, (("x", x), ("W", W), ("bias", bias), ("y", y)))
+    _check(lib().dense_linear_forward(ctypes.byref(s), x.shape[0], fuse, _ptr(x), _ptr(W), _ptr(bias), _ptr(y),
+                                      _ptr(workspace), workspace.numel() if workspace is not None else 0,
+                                      _stream(stream)))
+
+
+def dense_backward(s: _DenseShape, g, x, W, grad_x, dW, db, workspace, stream=None, fuse=0):
+    """dense_linear_backward: grad_x = G·W (× (x > 0) with FUSE_RELU_IN), dW = Gᵀ·x, db = Σ_t G."""
+    _validate(s, (("g", g), ("x", x), ("W", W), ("grad_x", grad_x)), (("dW", dW), ("db", db)))
+    _check(lib().dense_linear_backward(ctypes.byref(s), x.shape[0], fuse, _ptr(g), _ptr(x), _ptr(W), _ptr(grad_x),
+                                       _ptr(dW), _ptr(db), _ptr(workspace),
+                                       workspace.numel() if workspace is not None else 0, _stream(stream)))
+
+
+@dataclass
+class DenseGrads:
+    """DenseLinear::Grads (layers.hpp:42-46), row convention."""
+
+    grad_x: object  # [T, d_in]
+    grad_w: object  # [d_out, d_in] fp32
+    grad_b: object  # [d_out] fp32
+
+
+class DenseLinear:
+    """Device-resident rnla::nn::DenseLinear (layers.hpp:33-48): W [d_out, d_in]
+    (the reference's w), bias [d_out].  Construction follows dense_linear_init
+    (nn_layers.cpp:51-59), generated on the GPU from `seed`."""
+
+    def __init__(self, d_in, d_out, seed=0, dtype=BF16, device="cuda", _init=True):
+        import torch
+        if d_in < 1 or d_out < 1:
+            raise ShapeError(1, "DenseLinear: d_in and d_out must be >= 1")
+        self.d_in, self.d_out, self.dtype, self.seed = d_in, d_out, dtype, seed
+        self.shape = dense_shape(d_in, d_out, dtype)
+        td = torch_dtype(dtype)
+        self.W = torch.empty(d_out, d_in, dtype=td, device=device)
+        self.bias = torch.zeros(d_out, dtype=td, device=device)
+        if _init:
+            _check(lib().skl_dense_init(ctypes.byref(self.shape), seed, _ptr(self.W), _ptr(self.bias),
+                                        _stream(None)))
+        self._ws = None
+
+    @classmethod
+    def from_parts(cls, w, b, dtype=BF16, device="cuda"):
+        """A layer from explicit w [d_out, d_in] and b [d_out] (numpy or torch)."""
+        import numpy as np
+        import torch
+        w = np.asarray(w, dtype=np.float64)
+        lyr = cls(w.shape[1], w.shape[0], dtype=dtype, device=device, _init=False)
+        td = torch_dtype(dtype)
+        lyr.W.copy_(torch.from_numpy(np.ascontiguousarray(w)).to(device=device, dtype=td))
+        lyr.bias.copy_(torch.from_numpy(np.asarray(b, dtype=np.float64)).to(device=device, dtype=td))
+        return lyr
+
+    def params(self):
+        """(learnable, total_stored, dense_equivalent) -- all d_in*d_out + d_out for a dense layer."""
+        n = self.d_in * self.d_out + self.d_out
+        return n, n, n
+
+    def workspace(self, T):
+        import torch
+        need = max(dense_workspace_size(self.shape, T))
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.W.device)
+        return self._ws
+
+    def forward(self, x):
+        import torch
+        if x.dim() != 2 or x.shape[1] != self.d_in:
+            raise ShapeError(1, "DenseLinear::forward: input rows != d_in")
+        y = torch.empty(x.shape[0], self.d_out, dtype=x.dtype, device=x.device)
+        dense_forward(self.shape, x, self.W, self.bias, y, self.workspace(x.shape[0]))
+        return y
+
+    def backward(self, x, g) -> DenseGrads:
+        import torch
+        if x.shape[1] != self.d_in or g.shape[1] != self.d_out or x.shape[0] != g.shape[0]:
+            raise ShapeError(1, "DenseLinear::backward: shape mismatch")
+        T = x.shape[0]
+        gx = torch.empty(T, self.d_in, dtype=x.dtype, device=x.device)
+        dW = torch.empty(self.d_out, self.d_in, dtype=torch.float32, device=x.device)
+        db = torch.empty(self.d_out, dtype=torch.float32, device=x.device)
+        dense_backward(self.shape, g, x, self.W, gx, dW, db, self.workspace(T))
+        return DenseGrads(gx, dW, db)

@@ -296,7 +296,7 @@ cudaError_t launch_pack2(const SklDims& d, int elem, const void* S1s, const void
 // both ways).  Used once per conversion by skl_from_dense (W -> Wᵀ).
 template <typename T>
 __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t rows,
-                                                        int64_t cols) {
+                                                        int64_t cols, int64_t ld_out) {
     __shared__ T tile[32][33];
     const int64_t tr = (rows + 31) / 32, tc = (cols + 31) / 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -312,19 +312,55 @@ __global__ void __launch_bounds__(256) transpose_kernel(const T* __restrict__ in
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const int64_t c = c0 + ty + 8 * i, r = r0 + tx;
-            if (r < rows && c < cols) out[c * rows + r] = tile[tx][ty + 8 * i];
+            if (r < rows && c < cols) out[c * ld_out + r] = tile[tx][ty + 8 * i];
         }
     }
 }
 
-cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st) {
+cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st,
+                             int64_t ld_out) {
     ProfScope ps_("transpose", st);
     const int64_t tiles = ((rows + 31) / 32) * ((cols + 31) / 32);
     const int grid = (int)std::min<int64_t>(tiles, 148 * 8);
+    if (ld_out <= 0) ld_out = rows;
     if (elem == ELEM_BF16)
-        transpose_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, rows, cols);
+        transpose_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)in, (__nv_bfloat16*)out, rows, cols,
+                                                              ld_out);
     else
-        transpose_kernel<float><<<grid, 256, 0, st>>>((const float*)in, (float*)out, rows, cols);
+        transpose_kernel<float><<<grid, 256, 0, st>>>((const float*)in, (float*)out, rows, cols, ld_out);
+    return cudaGetLastError();
+}
+
+// DenseLinear init (dense_linear_init, nn_layers.cpp:51-59): w = the first
+// rows*cols entries of GaussianStream(seed) (row-major) times `scale`.
+cudaError_t launch_gaussian_scaled(int64_t rows, int64_t cols, uint64_t seed, double scale, int elem, void* out,
+                                   cudaStream_t st) {
+    ProfScope ps_("realize", st);
+    const uint64_t n = (uint64_t)rows * cols;
+    if (elem == ELEM_BF16)
+        realize_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>(0, rows, cols, seed, scale, 0, 0, out);
+    else if (elem == ELEM_F32)
+        realize_kernel<float><<<grid_for(n), 256, 0, st>>>(0, rows, cols, seed, scale, 0, 0, out);
+    else
+        realize_kernel<double><<<grid_for(n), 256, 0, st>>>(0, rows, cols, seed, scale, 0, 0, out);
+    return cudaGetLastError();
+}
+
+// out[i] = tf32_rna(in[i]) (operands a TF32 GEMM reads; in place allowed), or,
+// with to_f32 set, out[i] = float(in[i]) for an element-type vector (bias).
+__global__ void __launch_bounds__(256) convert_kernel(const void* in, int in_bf16, float* out, int64_t n, int rna) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        float v = in == nullptr ? 0.f
+                  : in_bf16     ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(in)[i])
+                                : reinterpret_cast<const float*>(in)[i];
+        out[i] = rna ? dev::tf32_rna(v) : v;
+    }
+}
+
+cudaError_t launch_to_f32(const void* in, int elem, int64_t n, float* out, int round_tf32, cudaStream_t st) {
+    if (n <= 0) return cudaSuccess;
+    ProfScope ps_("convert", st);
+    convert_kernel<<<grid_for((uint64_t)n), 256, 0, st>>>(in, elem == ELEM_BF16, out, n, round_tf32);
     return cudaGetLastError();
 }
 
@@ -436,6 +472,35 @@ cudaError_t launch_col2im(const void* cols, int elem, const ConvGeom& g, void* i
         col2im_gather_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)cols, (__nv_bfloat16*)img, g);
     else
         col2im_gather_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)cols, (float*)img, g);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- row padding
+// dst[b][r][c] = (r < R && c < C) ? src[b][r][c] : 0 for a [B][R2][C2] dst:
+// pads (R2 >= R, C2 >= C) or crops (R2 <= R, C2 <= C) the two inner dims of a
+// row-major stack.  Shapes whose rows are not 16-byte multiples go through the
+// TMA-fed kernels on zero-padded copies (skl.cu, padded dispatch); zero rank or
+// feature columns contribute nothing to any product, so the cropped results
+// equal the unpadded computation.  Elements move as raw bits (2 or 4 bytes).
+template <typename T>
+__global__ void __launch_bounds__(256) repad_kernel(const T* __restrict__ src, int64_t R, int64_t C,
+                                                    T* __restrict__ dst, int64_t R2, int64_t C2, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = i % C2, rest = i / C2;
+        const int64_t r = rest % R2, b = rest / R2;
+        dst[i] = (r < R && c < C) ? src[(b * R + r) * C + c] : T(0);
+    }
+}
+
+cudaError_t launch_repad(const void* src, int elem_bytes, int64_t B, int64_t R, int64_t C, void* dst, int64_t R2,
+                         int64_t C2, cudaStream_t st) {
+    const uint64_t n = (uint64_t)B * R2 * C2;
+    if (n == 0) return cudaSuccess;
+    ProfScope ps_("repad", st);
+    if (elem_bytes == 2)
+        repad_kernel<uint16_t><<<grid_for(n), 256, 0, st>>>((const uint16_t*)src, R, C, (uint16_t*)dst, R2, C2, n);
+    else
+        repad_kernel<uint32_t><<<grid_for(n), 256, 0, st>>>((const uint32_t*)src, R, C, (uint32_t*)dst, R2, C2, n);
     return cudaGetLastError();
 }
 

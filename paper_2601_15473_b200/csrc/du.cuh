@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256, 1)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
-            if (args.dbg) {
+            if (args.dbg && blockIdx.x < 296) {
                 g_du_prof[blockIdx.x][0] = w_empty;
                 g_du_prof[blockIdx.x][1] = (unsigned long long)(clock64() - t_beg);
             }
@@ -316,7 +316,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
                 mma_commit_pair(&tfull[acc], pair_mask);
             }
-            if (args.dbg) {
+            if (args.dbg && blockIdx.x < 296) {
                 g_du_prof[blockIdx.x][2] = w_full;
                 g_du_prof[blockIdx.x][3] = (unsigned long long)(clock64() - t_beg);
             }
@@ -485,7 +485,7 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
                 named_bar_sync(2, 128);
-                if (args.dbg && t == 0) g_du_wait[blockIdx.x][0] = (unsigned long long)(clock64() - e_t);
+                if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][0] = (unsigned long long)(clock64() - e_t);
                 const int z = 2 * x.split + (int)rank;
                 row_lo = z * 256 / parts;
                 row_hi = (z + 1) * 256 / parts;
@@ -500,7 +500,7 @@ __global__ void __launch_bounds__(256, 1)
                 col_lo = 0; col_hi = last ? kDuBN : 0;
             }
             __threadfence();
-            if (args.dbg && t == 0) g_du_wait[blockIdx.x][1] = (unsigned long long)(clock64() - e_t);
+            if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][1] = (unsigned long long)(clock64() - e_t);
             const float* pbase = args.part + (long long)x.slot * 256 * kDuBN;
             const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
                              (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
@@ -579,7 +579,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             }
-            if (args.dbg && t == 0) g_du_wait[blockIdx.x][2] = (unsigned long long)(clock64() - e_t);
+            if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][2] = (unsigned long long)(clock64() - e_t);
             if (x.colsum) {
                 for (int c = col_lo + t; c < col_hi; c += 128) {
                     const int n = n0 + c;
@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         lap(e_red);
-        if (args.dbg && warp == 4 && lane == 0) {
+        if (args.dbg && warp == 4 && lane == 0 && blockIdx.x < 296) {
             g_du_prof[blockIdx.x][4] = e_cs;
             g_du_prof[blockIdx.x][5] = e_acc;
             g_du_prof[blockIdx.x][6] = e_part;

@@ -14,6 +14,7 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -73,13 +74,13 @@ DevInfo dev_info() {
 
 // SMs left free for concurrently running communication kernels (NCCL) --
 // skl_set_reserved_sms; kept even so CTA pairs still tile the grid.
-int g_reserved_sms = 0;
+std::atomic<int> g_reserved_sms{0};
 
 skl_status check_device(DevInfo& di) {
     di = dev_info();
     if (di.sms == 0) return fail(SKL_ERR_CUDA, "no CUDA device available (libskl has no CPU fallback)");
     if (di.major != 10) return fail(SKL_ERR_CUDA, "libskl requires an sm_100 (B200) device, found sm_%d", di.major);
-    di.sms = std::max(2, (di.sms - g_reserved_sms) & ~1);
+    di.sms = std::max(2, (di.sms - g_reserved_sms.load(std::memory_order_relaxed)) & ~1);
     return SKL_OK;
 }
 
@@ -134,6 +135,20 @@ void add_pdl(cudaLaunchAttribute* attrs, unsigned& n) {
     ++n;
 }
 
+// Dynamic shared memory (and cluster-size) attributes are per device: set them
+// once per (kernel, device).  `done` is the kernel's own device bitmask.
+template <typename F>
+skl_status ensure_attrs(F kern, int smem_bytes, std::atomic<uint64_t>& done, bool nonportable_cluster = false) {
+    int dev = 0;
+    SKL_CUDA(cudaGetDevice(&dev));
+    const uint64_t bit = 1ull << (dev & 63);
+    if (done.load(std::memory_order_acquire) & bit) return SKL_OK;
+    SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes));
+    if (nonportable_cluster) SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    done.fetch_or(bit, std::memory_order_acq_rel);
+    return SKL_OK;
+}
+
 // ---------------------------------------------------------------- GEMM launch
 // Operand view: element (row-major storage) pointer, storage rows x cols, ld.
 struct View {
@@ -167,11 +182,8 @@ skl_status run_gemm(const char* name, const View& A, const View& B, int M, int N
     const int tiles = args.num_m_tiles * args.num_n_tiles;
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
     auto kern = dev::gemm_kernel<kCG, kKind, kBN, kStages>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(256);
@@ -246,11 +258,8 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     if (grid_cap > 0) sms = std::min(sms, grid_cap);
     int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
     auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost>;
-    static bool attr_set = false;
-    if (!attr_set) {
-        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(384);  // 4 control warps + 2 epilogue warpgroups
@@ -282,11 +291,8 @@ skl_status run_b2b_tf32_wide(const char* name, const B2BSrc& src, B2BArgs a, int
     SKL_TRY(make_tmap(&ty, a.out, 4, a.N2, a.T, a.ldo, C::kBK, 128));
     const int tiles = (a.T + 255) / 256;
     const int grid = std::max(1, std::min(sms / 2, tiles)) * 2;
-    static bool attr_set = false;
-    if (!attr_set) {
-        SKL_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem));
-        attr_set = true;
-    }
+    static std::atomic<uint64_t> attr_done{0};
+    SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(384);
@@ -414,21 +420,35 @@ skl_status get_dims(const skl_shape* s, SklDims& d) {
 int elem_of(skl_dtype t) { return t == SKL_BF16 ? ELEM_BF16 : ELEM_F32; }
 int ebytes(skl_dtype t) { return t == SKL_BF16 ? 2 : 4; }
 
-// Shapes the TMA-fed kernels accept: every row stride a multiple of 16 B.
-skl_status check_alignment(const SklDims& d, skl_dtype t) {
-    const int e = ebytes(t);
-    if ((d.d_in * e) % 16 || (d.d_out * e) % 16 || (d.Lk * e) % 16)
-        return fail(SKL_ERR_UNSUPPORTED,
-                    "unsupported shape: d_in, d_out and L*k must be multiples of %d elements for %s (got %lld, %lld, "
-                    "%lld)",
-                    16 / e, t == SKL_BF16 ? "bf16" : "tf32", (long long)d.d_in, (long long)d.d_out,
-                    (long long)d.Lk);
-    return SKL_OK;
+// The TMA-fed kernels need every row stride to be a multiple of 16 B.  Shapes
+// whose d_in / d_out rows are not (the reference accepts any shape,
+// nn_layers.cpp:61-101) run on zero-padded copies staged in the workspace
+// (padded dispatch below): zero feature columns add nothing to any product,
+// so the cropped outputs are those of the unpadded layer.
+int64_t round_to(int64_t v, int64_t a) { return (v + a - 1) / a * a; }
+int64_t row_align(skl_dtype t) { return 16 / ebytes(t); }  // elements per 16 B
+bool needs_pad(const SklDims& d, skl_dtype t) {
+    const int64_t a = row_align(t);
+    return d.d_in % a || d.d_out % a;
+}
+SklDims pad_dims(const SklDims& d, skl_dtype t, bool pad_k) {
+    const int64_t a = row_align(t);
+    SklDims p = d;
+    p.d_in = round_to(d.d_in, a);
+    p.d_out = round_to(d.d_out, a);
+    if (pad_k) {
+        p.k = round_to(d.k, a);
+        p.Lk = p.L * p.k;
+        p.R = 2 * p.Lk;
+        p.R_pad = (p.R + 63) / 64 * 64;
+    }
+    return p;
 }
 
 // SKL_FORCE_UNFUSED=1 routes every shape through the unfused GEMM chain
 // (testing aid: both paths are parity-checked against the oracle).
 bool use_fused(const SklDims& d, skl_dtype t) {
+    read_b2b_env();
     static const bool force_unfused = [] {
         const char* e = getenv("SKL_FORCE_UNFUSED");
         return e && atoi(e) != 0;
@@ -442,6 +462,7 @@ bool use_fused(const SklDims& d, skl_dtype t) {
 // 1-bit ReLU masks are implemented in the CTA-pair b2b kernel only (not in the
 // wide-rank TF32 kernel or the unfused GEMM chain).
 bool relu_bits_ok(const SklDims& d, skl_dtype t) {
+    read_b2b_env();
     static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
     if (!use_fused(d, t) || g_b2b_cg != 2) return false;
     return !(t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad));
@@ -529,6 +550,26 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     return s;
 }
 
+// du split partials / column-sum partials / tickets, sized for every phase's
+// split choice AND independently of the SM count the call will see
+// (skl_set_reserved_sms may change it after the size query): one-wave searches
+// keep t0*s0 + t1*s1 <= pairs unless every split is 1, and several waves use
+// S <= 2, so units <= max(pairs, 2 * tiles) and s0 <= max(pairs, 2) for any
+// pair count up to the device's full one.
+void du_ws_sizes(const SklDims& d, skl_dtype t, int64_t T, int sms, size_t& part, size_t& cpart, size_t& tickets) {
+    const int full_pairs = std::max(74, dev_info().sms / 2);
+    const DuShape all = du_shape(d, T, 2 * full_pairs, t == SKL_BF16 ? 0 : 1, 3);
+    part = (size_t)std::max(full_pairs, 2 * all.tiles()) * 256 * 256 * 4;
+    cpart = (size_t)all.n0t * std::max(full_pairs, 2) * 256 * 4;
+    tickets = (size_t)all.tiles() * 4;
+    for (int which = 1; which <= 3; ++which) {  // explicit SKL_DU_SPLITS overrides
+        const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1, which);
+        part = std::max(part, (size_t)u.units * 256 * 256 * 4);
+        cpart = std::max(cpart, (size_t)u.n0t * u.s0 * 256 * 4);
+        tickets = std::max(tickets, (size_t)u.tiles() * 4);
+    }
+}
+
 // Offsets into the caller's workspace (1 KiB aligned).
 Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     const size_t e = ebytes(t);
@@ -549,14 +590,9 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.inter = take(!fused ? (size_t)T * d.R_pad * e : 0);
     p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
     p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
-    if (bwd) {  // sized for every phase's split choice
-        size_t part = 0, cpart = 0, tickets = 0;
-        for (int which = 1; which <= 3; ++which) {
-            const DuShape u = du_shape(d, T, sms, t == SKL_BF16 ? 0 : 1, which);
-            part = std::max(part, (size_t)u.units * 256 * 256 * 4);
-            cpart = std::max(cpart, (size_t)u.n0t * u.s0 * 256 * 4);
-            tickets = std::max(tickets, (size_t)u.tiles() * 4);
-        }
+    if (bwd) {
+        size_t part, cpart, tickets;
+        du_ws_sizes(d, t, T, sms, part, cpart, tickets);
         p.du_part = take(part);
         p.du_cpart = take(cpart);
         p.du_tickets = take(tickets);
@@ -571,15 +607,60 @@ Tp* at(void* ws, size_t off) {
     return reinterpret_cast<Tp*>(reinterpret_cast<uint8_t*>(ws) + off);
 }
 
+// Workspace of the padded dispatch: the padded layer's own plan first, then the
+// zero-padded copies of the operands whose rows change and the padded outputs.
+struct PadPlan {
+    size_t inner, x, yg, dx, s1, u2, u1, s2, bias, du1, du2, db, total;
+};
+PadPlan pad_plan(const SklDims& d, const SklDims& dp, skl_dtype t, int64_t T, bool bwd, int sms) {
+    const size_t e = ebytes(t);
+    PadPlan q = {};
+    const bool pin = dp.d_in != d.d_in, pout = dp.d_out != d.d_out;
+    size_t off = align_up(plan(dp, t, T, bwd, sms).total);
+    q.inner = off;
+    auto take = [&](bool need, size_t bytes) {
+        size_t o = off;
+        if (need) off += align_up(bytes ? bytes : 1);
+        return o;
+    };
+    q.x = take(pin, (size_t)T * dp.d_in * e);
+    q.yg = take(pout, (size_t)T * dp.d_out * e);
+    q.dx = take(bwd && pin, (size_t)T * dp.d_in * e);
+    q.s1 = take(pin, (size_t)dp.Lk * dp.d_in * e);
+    q.u2 = take(pin, (size_t)dp.Lk * dp.d_in * e);
+    q.u1 = take(pout, (size_t)dp.Lk * dp.d_out * e);
+    q.s2 = take(pout, (size_t)dp.Lk * dp.d_out * e);
+    q.bias = take(pout, (size_t)dp.d_out * e);
+    q.du1 = take(bwd && pout, (size_t)dp.Lk * dp.d_out * 4);
+    q.du2 = take(bwd && pin, (size_t)dp.Lk * dp.d_in * 4);
+    q.db = take(bwd && pout, (size_t)dp.d_out * 4);
+    q.total = off;
+    return q;
+}
+
+// [B][R][C] stack -> zero-padded [B][R2][C2] copy in the workspace (or the
+// source itself when nothing changes).
+skl_status repad_in(const void* src, int eb, int64_t B, int64_t R, int64_t C, void* ws, size_t off, int64_t R2,
+                    int64_t C2, cudaStream_t st, const void** out) {
+    if (!src || (R == R2 && C == C2)) {
+        *out = src;
+        return SKL_OK;
+    }
+    void* dst = at<void>(ws, off);
+    SKL_CUDA(launch_repad(src, eb, B, R, C, dst, R2, C2, st));
+    *out = dst;
+    return SKL_OK;
+}
+
 // dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
 // ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.  `which`:
 // bit 0 = dU1s (+ db), bit 1 = dU2s; one grouped persistent launch.
 skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* saved, const void* grad_y,
                   const void* p2t, const void* x, float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
-                  const Plan& p, int sms, cudaStream_t st) {
+                  const Plan& p, int sms, cudaStream_t st, float alpha = 0.f) {
     const int eb = kind == 0 ? 2 : 4;
     const int64_t ldt = t8(T);
-    const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    const float inv = alpha != 0.f ? alpha : (float)(1.0 / (2.0 * (double)d.L));
     const DuShape u = du_shape(d, T, sms, kind, which);
     DuArgs a = {};
     a.k_blocks = u.kb;
@@ -620,12 +701,8 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     tb1 = tu2b;
     if (!u.cr) SKL_CUDA(cudaMemsetAsync(a.tickets, 0, (size_t)u.tiles() * 4, st));
     auto du_kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[kind]) {
-        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem));
-        SKL_CUDA(cudaFuncSetAttribute(du_kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));  // 2S up to 16
-        attr_set[kind] = true;
-    }
+    static std::atomic<uint64_t> attr_done[2];
+    SKL_TRY(ensure_attrs(du_kern, dev::kDuSmem, attr_done[kind], /*clusters of 2S up to 16*/ true));
     const int units = u.units;  // CTA-pair work units
     a.relay = colsum ? 1 : 0;
     if (u.cr) {
@@ -762,6 +839,12 @@ skl_status skl_workspace_size(const skl_shape* s, int64_t T, size_t* fwd_bytes, 
     if (T < 0) return fail(SKL_ERR_SHAPE, "T must be >= 0");
     DevInfo di = dev_info();
     const int sms = di.sms ? di.sms : 148;
+    if (needs_pad(d, s->dtype)) {  // padded dispatch: the padded layer's plan + staged copies
+        const SklDims dp = pad_dims(d, s->dtype, false);
+        if (fwd_bytes) *fwd_bytes = pad_plan(d, dp, s->dtype, T, false, sms).total;
+        if (bwd_bytes) *bwd_bytes = pad_plan(d, dp, s->dtype, T, true, sms).total;
+        return SKL_OK;
+    }
     if (fwd_bytes) *fwd_bytes = plan(d, s->dtype, T, false, sms).total;  // saved_proj: [L*k][round8(T)]
     if (bwd_bytes) *bwd_bytes = plan(d, s->dtype, T, true, sms).total;
     return SKL_OK;
@@ -806,9 +889,34 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
     if (T < 0) return fail(SKL_ERR_SHAPE, "SkLinear::forward: T must be >= 0");
     if (T == 0) return SKL_OK;
     if (!x || !S1s || !S2s || !U1s || !U2s || !y) return fail(SKL_ERR_PARAM, "null tensor argument");
-    SKL_TRY(check_alignment(d, s->dtype));
     DevInfo di;
     SKL_TRY(check_device(di));
+    if (needs_pad(d, s->dtype)) {
+        // Rows that are not 16-byte multiples: the same kernels on zero-padded
+        // copies (x, the four stacks, the bias), y cropped back.  The 1-bit
+        // ReLU mask keeps its layout: padding to 16 B never crosses a 64-column group.
+        const int eb = ebytes(s->dtype);
+        const SklDims dp = pad_dims(d, s->dtype, false);
+        const PadPlan q = pad_plan(d, dp, s->dtype, T, false, di.sms);
+        if (!workspace || ws_bytes < q.total)
+            return fail(SKL_ERR_WORKSPACE, "forward workspace too small: need %zu bytes, got %zu", q.total, ws_bytes);
+        cudaStream_t st = (cudaStream_t)stream;
+        const void *xp, *s1p, *u2p, *u1p, *s2p, *bp;
+        SKL_TRY(repad_in(x, eb, 1, T, d.d_in, workspace, q.x, T, dp.d_in, st, &xp));
+        SKL_TRY(repad_in(S1s, eb, d.L, d.d_in, d.k, workspace, q.s1, dp.d_in, d.k, st, &s1p));
+        SKL_TRY(repad_in(U2s, eb, d.L, d.d_in, d.k, workspace, q.u2, dp.d_in, d.k, st, &u2p));
+        SKL_TRY(repad_in(U1s, eb, d.L, d.k, d.d_out, workspace, q.u1, d.k, dp.d_out, st, &u1p));
+        SKL_TRY(repad_in(S2s, eb, d.L, d.k, d.d_out, workspace, q.s2, d.k, dp.d_out, st, &s2p));
+        SKL_TRY(repad_in(bias, eb, 1, 1, d.d_out, workspace, q.bias, 1, dp.d_out, st, &bp));
+        void* yp = dp.d_out != d.d_out ? at<void>(workspace, q.yg) : y;
+        skl_shape sp = *s;
+        sp.d_in = dp.d_in;
+        sp.d_out = dp.d_out;
+        SKL_TRY(sketched_linear_forward_bits(&sp, T, fuse, xp, s1p, s2p, u1p, u2p, bp, yp, saved_proj, relu_bits,
+                                             workspace, q.inner, stream));
+        if (yp != y) SKL_CUDA(launch_repad(yp, eb, 1, T, dp.d_out, y, T, d.d_out, st));
+        return SKL_OK;
+    }
     const Plan p = plan(d, s->dtype, T, false, di.sms);
     if (!workspace || ws_bytes < p.total)
         return fail(SKL_ERR_WORKSPACE, "forward workspace too small: need %zu bytes, got %zu", p.total, ws_bytes);
@@ -922,7 +1030,6 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
     const bool ph_u1 = (phases & SKL_BWD_DU1_DB) != 0, ph_data = (phases & SKL_BWD_DX_DU2) != 0;
     if ((ph_u1 && !grad_U1s) || (ph_data && !grad_U2s)) return fail(SKL_ERR_PARAM, "null gradient argument");
     if (T > 0 && (!grad_y || !x || !S1s || !S2s || !U1s || !U2s)) return fail(SKL_ERR_PARAM, "null tensor argument");
-    SKL_TRY(check_alignment(d, s->dtype));
     DevInfo di;
     SKL_TRY(check_device(di));
     const Plan p = plan(d, s->dtype, T, true, di.sms);
@@ -933,6 +1040,39 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         if (ph_u1) SKL_CUDA(cudaMemsetAsync(grad_U1s, 0, (size_t)d.Lk * d.d_out * 4, st));
         if (ph_data) SKL_CUDA(cudaMemsetAsync(grad_U2s, 0, (size_t)d.Lk * d.d_in * 4, st));
         if (ph_u1 && grad_bias) SKL_CUDA(cudaMemsetAsync(grad_bias, 0, (size_t)d.d_out * 4, st));
+        return SKL_OK;
+    }
+    if (needs_pad(d, s->dtype)) {
+        // Rows that are not 16-byte multiples: zero-padded copies of G, x and the
+        // stacks; gradients of the padded layer cropped back.  Padded feature
+        // columns of x / G are zero, so they add nothing to dU1s / dU2s / db,
+        // and the padded columns of dX / dU / db are dropped.
+        const int eb = ebytes(s->dtype);
+        const SklDims dp = pad_dims(d, s->dtype, false);
+        const PadPlan q = pad_plan(d, dp, s->dtype, T, true, di.sms);
+        if (ws_bytes < q.total)
+            return fail(SKL_ERR_WORKSPACE, "backward workspace too small: need %zu bytes, got %zu", q.total, ws_bytes);
+        const bool pin = dp.d_in != d.d_in, pout = dp.d_out != d.d_out;
+        const void *xp, *gp, *s1p, *u2p, *u1p, *s2p;
+        SKL_TRY(repad_in(x, eb, 1, T, d.d_in, workspace, q.x, T, dp.d_in, st, &xp));
+        SKL_TRY(repad_in(grad_y, eb, 1, T, d.d_out, workspace, q.yg, T, dp.d_out, st, &gp));
+        SKL_TRY(repad_in(S1s, eb, d.L, d.d_in, d.k, workspace, q.s1, dp.d_in, d.k, st, &s1p));
+        SKL_TRY(repad_in(U2s, eb, d.L, d.d_in, d.k, workspace, q.u2, dp.d_in, d.k, st, &u2p));
+        SKL_TRY(repad_in(U1s, eb, d.L, d.k, d.d_out, workspace, q.u1, d.k, dp.d_out, st, &u1p));
+        SKL_TRY(repad_in(S2s, eb, d.L, d.k, d.d_out, workspace, q.s2, d.k, dp.d_out, st, &s2p));
+        void* gxp = (pin && grad_x) ? at<void>(workspace, q.dx) : grad_x;
+        float* du1p = (pout && grad_U1s) ? at<float>(workspace, q.du1) : grad_U1s;
+        float* du2p = (pin && grad_U2s) ? at<float>(workspace, q.du2) : grad_U2s;
+        float* dbp = (pout && grad_bias) ? at<float>(workspace, q.db) : grad_bias;
+        skl_shape sp = *s;
+        sp.d_in = dp.d_in;
+        sp.d_out = dp.d_out;
+        SKL_TRY(sketched_linear_backward_bits(&sp, T, phases, fuse, gp, xp, saved_proj, s1p, s2p, u1p, u2p, gxp, du1p,
+                                              du2p, dbp, relu_bits, workspace, q.inner, stream));
+        if (ph_u1 && du1p != grad_U1s) SKL_CUDA(launch_repad(du1p, 4, d.L, d.k, dp.d_out, grad_U1s, d.k, d.d_out, st));
+        if (ph_u1 && dbp != grad_bias) SKL_CUDA(launch_repad(dbp, 4, 1, 1, dp.d_out, grad_bias, 1, d.d_out, st));
+        if (ph_data && du2p != grad_U2s) SKL_CUDA(launch_repad(du2p, 4, d.L, dp.d_in, d.k, grad_U2s, d.d_in, d.k, st));
+        if (ph_data && gxp != grad_x) SKL_CUDA(launch_repad(gxp, eb, 1, T, dp.d_in, grad_x, T, d.d_in, st));
         return SKL_OK;
     }
     const int elem = elem_of(s->dtype);
@@ -1032,40 +1172,21 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
                   di.sms, st);
 }
 
-skl_status skl_from_dense_workspace_size(const skl_shape* s, size_t* bytes) {
-    SklDims d;
-    SKL_TRY(get_dims(s, d));
-    const size_t e = ebytes(s->dtype);
-    *bytes = align_up((size_t)d.R_pad * d.d_in * e) + align_up((size_t)d.d_in * d.d_out * e);
-    return SKL_OK;
+namespace skl {
+namespace {
+size_t from_dense_core_bytes(const SklDims& d, size_t e) {
+    return align_up((size_t)d.R_pad * d.d_in * e) + align_up((size_t)d.d_in * d.d_out * e);
 }
+bool from_dense_needs_pad(const SklDims& d, skl_dtype t) { return needs_pad(d, t) || d.k % row_align(t); }
 
-// sk_linear_from_dense (nn_layers.cpp:149-160) on the device.  Reference:
-// u1_i = s1_i·W [k, d_in], u2_i = W·s2_iᵀ [d_out, k].  In the ABI stacks
-// (S2s[i] = s1_i, S1s[i] = s2_iᵀ):  U1s[i] = u2_iᵀ = S1s[i]ᵀ·Wᵀ  and
-// U2s[i] = u1_iᵀ = Wᵀ·S2s[i]ᵀ -- two tcgen05 GEMMs (all terms of U1s in one).
-skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed, const void* W,
-                          const void* bias_in, void* S1s, void* S2s, void* U1s, void* U2s, void* bias_out,
-                          void* workspace, size_t ws_bytes, void* stream) {
-    SklDims d;
-    SKL_TRY(get_dims(s, d));
-    if (!W || !S1s || !S2s || !U1s || !U2s) return fail(SKL_ERR_PARAM, "null tensor argument");
-    if (dist != SKL_DIST_GAUSSIAN && dist != SKL_DIST_RADEMACHER) return fail(SKL_ERR_PARAM, "unknown dist %d", dist);
-    SKL_TRY(check_alignment(d, s->dtype));
-    const int eb = ebytes(s->dtype), elem = elem_of(s->dtype), kind = s->dtype == SKL_BF16 ? 0 : 1;
-    if ((d.k * eb) % 16)
-        return fail(SKL_ERR_UNSUPPORTED, "sk_linear_from_dense: low_rank must be a multiple of %d", 16 / eb);
-    DevInfo di;
-    SKL_TRY(check_device(di));
-    size_t need = 0;
-    SKL_TRY(skl_from_dense_workspace_size(s, &need));
-    if (!workspace || ws_bytes < need)
-        return fail(SKL_ERR_WORKSPACE, "from_dense workspace too small: need %zu bytes, got %zu", need, ws_bytes);
-    cudaStream_t st = (cudaStream_t)stream;
-    void* acatT = workspace;                                                        // rows < Lk: S1s[i]ᵀ
-    void* wT = at<void>(workspace, align_up((size_t)d.R_pad * d.d_in * eb));       // Wᵀ [d_in][d_out]
-    SKL_CUDA(launch_gen_sketches((int)dist, layer_seed, d, elem, S1s, S2s, st));  // sk_linear_shell seeds
-    SKL_CUDA(cudaMemsetAsync(U2s, 0, (size_t)d.Lk * d.d_in * eb, st));            // (pack reads the U2 half)
+// U from W for sketches already in S1s / S2s (aligned shape): U1s = S1sᵀ·Wᵀ for
+// all terms in one GEMM, U2s[i] = Wᵀ·S2s[i]ᵀ per term.
+skl_status from_dense_core(const SklDims& d, skl_dtype t, const void* W, const void* S1s, const void* S2s, void* U1s,
+                           void* U2s, void* workspace, int sms, cudaStream_t st) {
+    const int eb = ebytes(t), elem = elem_of(t), kind = t == SKL_BF16 ? 0 : 1;
+    void* acatT = workspace;                                                   // rows < Lk: S1s[i]ᵀ
+    void* wT = at<void>(workspace, align_up((size_t)d.R_pad * d.d_in * eb));  // Wᵀ [d_in][d_out]
+    SKL_CUDA(cudaMemsetAsync(U2s, 0, (size_t)d.Lk * d.d_in * eb, st));       // (pack reads the U2 half)
     SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, nullptr, nullptr, nullptr, st));
     SKL_CUDA(launch_transpose(W, elem, d.d_out, d.d_in, wT, st));
     GemmArgs g = {};
@@ -1074,7 +1195,7 @@ skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed
     g.ldo = d.d_out;
     g.out_f32 = eb == 4;
     View va{acatT, d.Lk, d.d_in, d.d_in}, vw{W, d.d_out, d.d_in, d.d_in};
-    SKL_TRY(gemm_any(kind, "from_dense_U1", va, vw, (int)d.Lk, (int)d.d_out, (int)d.d_in, g, di.sms, st));
+    SKL_TRY(gemm_any(kind, "from_dense_U1", va, vw, (int)d.Lk, (int)d.d_out, (int)d.d_in, g, sms, st));
     for (int64_t i = 0; i < d.L; ++i) {
         GemmArgs g2 = {};
         g2.alpha = 1.f;
@@ -1083,7 +1204,68 @@ skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed
         g2.out_f32 = eb == 4;
         View vwt{wT, d.d_in, d.d_out, d.d_out};
         View vs2{static_cast<const uint8_t*>(S2s) + (size_t)i * d.k * d.d_out * eb, d.k, d.d_out, d.d_out};
-        SKL_TRY(gemm_any(kind, "from_dense_U2", vwt, vs2, (int)d.d_in, (int)d.k, (int)d.d_out, g2, di.sms, st));
+        SKL_TRY(gemm_any(kind, "from_dense_U2", vwt, vs2, (int)d.d_in, (int)d.k, (int)d.d_out, g2, sms, st));
+    }
+    return SKL_OK;
+}
+}  // namespace
+}  // namespace skl
+
+skl_status skl_from_dense_workspace_size(const skl_shape* s, size_t* bytes) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (!bytes) return fail(SKL_ERR_PARAM, "null size pointer");
+    const size_t e = ebytes(s->dtype);
+    if (!from_dense_needs_pad(d, s->dtype)) {
+        *bytes = from_dense_core_bytes(d, e);
+        return SKL_OK;
+    }
+    // padded: core + S1s, S2s, W, U1s, U2s at the padded (d_in, d_out, k)
+    const SklDims p = pad_dims(d, s->dtype, true);
+    *bytes = from_dense_core_bytes(p, e) + 4 * align_up((size_t)p.Lk * std::max(p.d_in, p.d_out) * e) +
+             align_up((size_t)p.d_in * p.d_out * e);
+    return SKL_OK;
+}
+
+// sk_linear_from_dense (nn_layers.cpp:149-160) on the device.  Reference:
+// u1_i = s1_i·W [k, d_in], u2_i = W·s2_iᵀ [d_out, k].  In the ABI stacks
+// (S2s[i] = s1_i, S1s[i] = s2_iᵀ):  U1s[i] = u2_iᵀ = S1s[i]ᵀ·Wᵀ  and
+// U2s[i] = u1_iᵀ = Wᵀ·S2s[i]ᵀ -- two tcgen05 GEMMs (all terms of U1s in one).
+// Any shape: rows that are not 16-byte multiples (d_in, d_out or k) are
+// computed on zero-padded copies of W and the sketches, then cropped.
+skl_status skl_from_dense(const skl_shape* s, skl_dist dist, uint64_t layer_seed, const void* W,
+                          const void* bias_in, void* S1s, void* S2s, void* U1s, void* U2s, void* bias_out,
+                          void* workspace, size_t ws_bytes, void* stream) {
+    SklDims d;
+    SKL_TRY(get_dims(s, d));
+    if (!W || !S1s || !S2s || !U1s || !U2s) return fail(SKL_ERR_PARAM, "null tensor argument");
+    if (dist != SKL_DIST_GAUSSIAN && dist != SKL_DIST_RADEMACHER) return fail(SKL_ERR_PARAM, "unknown dist %d", dist);
+    const int eb = ebytes(s->dtype), elem = elem_of(s->dtype);
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    size_t need = 0;
+    SKL_TRY(skl_from_dense_workspace_size(s, &need));
+    if (!workspace || ws_bytes < need)
+        return fail(SKL_ERR_WORKSPACE, "from_dense workspace too small: need %zu bytes, got %zu", need, ws_bytes);
+    cudaStream_t st = (cudaStream_t)stream;
+    SKL_CUDA(launch_gen_sketches((int)dist, layer_seed, d, elem, S1s, S2s, st));  // sk_linear_shell seeds
+    if (!from_dense_needs_pad(d, s->dtype)) {
+        SKL_TRY(from_dense_core(d, s->dtype, W, S1s, S2s, U1s, U2s, workspace, di.sms, st));
+    } else {
+        const SklDims p = pad_dims(d, s->dtype, true);
+        size_t off = from_dense_core_bytes(p, eb);
+        const size_t slot = align_up((size_t)p.Lk * std::max(p.d_in, p.d_out) * eb);
+        void* s1p = at<void>(workspace, off);
+        void* s2p = at<void>(workspace, off + slot);
+        void* u1p = at<void>(workspace, off + 2 * slot);
+        void* u2p = at<void>(workspace, off + 3 * slot);
+        void* wp = at<void>(workspace, off + 4 * slot);
+        SKL_CUDA(launch_repad(S1s, eb, d.L, d.d_in, d.k, s1p, p.d_in, p.k, st));
+        SKL_CUDA(launch_repad(S2s, eb, d.L, d.k, d.d_out, s2p, p.k, p.d_out, st));
+        SKL_CUDA(launch_repad(W, eb, 1, d.d_out, d.d_in, wp, p.d_out, p.d_in, st));
+        SKL_TRY(from_dense_core(p, s->dtype, wp, s1p, s2p, u1p, u2p, workspace, di.sms, st));
+        SKL_CUDA(launch_repad(u1p, eb, d.L, p.k, p.d_out, U1s, d.k, d.d_out, st));
+        SKL_CUDA(launch_repad(u2p, eb, d.L, p.d_in, p.k, U2s, d.d_in, d.k, st));
     }
     if (bias_out) {
         if (bias_in) SKL_CUDA(cudaMemcpyAsync(bias_out, bias_in, (size_t)d.d_out * eb, cudaMemcpyDeviceToDevice, st));
@@ -1194,6 +1376,239 @@ skl_status sketched_conv2d_backward(const skl_shape* s, const skl_conv_shape* cs
     SKL_TRY(sketched_linear_backward(s, T, gtok, cols, saved_proj, S1s, S2s, U1s, U2s, dcols, grad_U1s, grad_U2s,
                                      grad_bias, at<void>(workspace, p.inner), p.total - p.inner, stream));
     if (grad_x) SKL_CUDA(launch_col2im(dcols, elem, g, grad_x, st));
+    return SKL_OK;
+}
+
+// ---------------------------------------------------------------- DenseLinear
+// DenseLinear::forward / backward (nn_layers.cpp:32-49) in row convention:
+//   y = x·Wᵀ + b       one tcgen05 GEMM (A = x, B = W, both K-major), bias /
+//                      ReLU in the epilogue;
+//   dX = G·W           one GEMM (B = Wᵀ, a small transposed copy);
+//   dW = Gᵀ·x, db = Σ_t G   the du kernel's token reduction: it computes
+//                      dWᵀ = xᵀ·G from a transposed copy of x (K-major A, like
+//                      Savedᵀ) and G (MN-major B), with db from the staged G
+//                      tiles; dWᵀ is transposed into W's layout.
+namespace skl {
+namespace {
+skl_status dense_dims(const skl_dense_shape* s, SklDims& d) {
+    if (!s) return fail(SKL_ERR_PARAM, "null shape");
+    if (s->d_in < 1 || s->d_out < 1) return fail(SKL_ERR_SHAPE, "DenseLinear: d_in and d_out must be >= 1");
+    if (s->dtype != SKL_BF16 && s->dtype != SKL_F32_TF32) return fail(SKL_ERR_PARAM, "unknown dtype %d", s->dtype);
+    // du's problem 0 ("dU1" slot) with M = d_in rows of xᵀ and N = d_out columns of G
+    d.d_in = s->d_in;
+    d.d_out = s->d_out;
+    d.L = 1;
+    d.k = s->d_in;
+    d.Lk = s->d_in;
+    d.R = 2 * d.Lk;
+    d.R_pad = (d.R + 63) / 64 * 64;
+    return SKL_OK;
+}
+struct DensePlan {
+    size_t wr, bias32, xT, wT, dwT, part, cpart, tickets, total;
+};
+DensePlan dense_plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
+    const size_t e = ebytes(t);
+    DensePlan q = {};
+    size_t off = 0;
+    auto take = [&](bool need, size_t bytes) {
+        size_t o = off;
+        if (need) off += align_up(bytes ? bytes : 1);
+        return o;
+    };
+    q.wr = take(!bwd && t != SKL_BF16, (size_t)d.d_out * d.d_in * 4);  // TF32-rounded W (forward B operand)
+    q.bias32 = take(!bwd, (size_t)d.d_out * 4);
+    q.xT = take(bwd, (size_t)d.d_in * t8(T) * e);                      // xᵀ [d_in][round8(T)]
+    q.wT = take(bwd, (size_t)d.d_in * d.d_out * e);                    // Wᵀ [d_in][d_out]
+    q.dwT = take(bwd, (size_t)d.d_in * d.d_out * 4);                   // dWᵀ [d_in][d_out] fp32
+    if (bwd) {
+        size_t part, cpart, tickets;
+        du_ws_sizes(d, t, T, sms, part, cpart, tickets);
+        q.part = take(true, part);
+        q.cpart = take(true, cpart);
+        q.tickets = take(true, tickets);
+    }
+    q.total = off;
+    return q;
+}
+struct DensePad {
+    size_t inner, x, yg, dx, w, bias, dw, db, total;
+};
+DensePad dense_pad_plan(const SklDims& d, const SklDims& dp, skl_dtype t, int64_t T, bool bwd, int sms) {
+    const size_t e = ebytes(t);
+    DensePad q = {};
+    size_t off = align_up(dense_plan(dp, t, T, bwd, sms).total);
+    q.inner = off;
+    auto take = [&](bool need, size_t bytes) {
+        size_t o = off;
+        if (need) off += align_up(bytes ? bytes : 1);
+        return o;
+    };
+    const bool pin = dp.d_in != d.d_in, pout = dp.d_out != d.d_out;
+    q.x = take(pin, (size_t)T * dp.d_in * e);
+    q.yg = take(pout, (size_t)T * dp.d_out * e);
+    q.dx = take(bwd && pin, (size_t)T * dp.d_in * e);
+    q.w = take(true, (size_t)dp.d_out * dp.d_in * e);
+    q.bias = take(!bwd && pout, (size_t)dp.d_out * e);
+    q.dw = take(bwd, (size_t)dp.d_out * dp.d_in * 4);
+    q.db = take(bwd && pout, (size_t)dp.d_out * 4);
+    q.total = off;
+    return q;
+}
+}  // namespace
+}  // namespace skl
+
+skl_status skl_dense_workspace_size(const skl_dense_shape* s, int64_t T, size_t* fwd_bytes, size_t* bwd_bytes) {
+    SklDims d;
+    SKL_TRY(dense_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "T must be >= 0");
+    const int sms = std::max(2, dev_info().sms ? dev_info().sms : 148);
+    if (needs_pad(d, s->dtype)) {
+        SklDims dp = pad_dims(d, s->dtype, false);
+        dp.k = dp.Lk = dp.d_in;
+        if (fwd_bytes) *fwd_bytes = dense_pad_plan(d, dp, s->dtype, T, false, sms).total;
+        if (bwd_bytes) *bwd_bytes = dense_pad_plan(d, dp, s->dtype, T, true, sms).total;
+        return SKL_OK;
+    }
+    if (fwd_bytes) *fwd_bytes = dense_plan(d, s->dtype, T, false, sms).total;
+    if (bwd_bytes) *bwd_bytes = dense_plan(d, s->dtype, T, true, sms).total;
+    return SKL_OK;
+}
+
+skl_status skl_dense_init(const skl_dense_shape* s, uint64_t seed, void* W, void* bias, void* stream) {
+    SklDims d;
+    SKL_TRY(dense_dims(s, d));
+    if (!W) return fail(SKL_ERR_PARAM, "null tensor argument");
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    cudaStream_t st = (cudaStream_t)stream;
+    const double std_dev = std::sqrt(2.0 / (double)(d.d_in + d.d_out));  // nn_layers.cpp:55
+    SKL_CUDA(launch_gaussian_scaled(d.d_out, d.d_in, seed, std_dev, elem_of(s->dtype), W, st));
+    if (bias) SKL_CUDA(cudaMemsetAsync(bias, 0, (size_t)d.d_out * ebytes(s->dtype), st));
+    return SKL_OK;
+}
+
+skl_status dense_linear_forward(const skl_dense_shape* s, int64_t T, unsigned fuse, const void* x, const void* W,
+                                const void* bias, void* y, void* workspace, size_t ws_bytes, void* stream) {
+    if (fuse & ~(unsigned)SKL_FUSE_RELU_OUT) return fail(SKL_ERR_PARAM, "dense forward: unsupported fuse flags %u", fuse);
+    SklDims d;
+    SKL_TRY(dense_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "DenseLinear::forward: T must be >= 0");
+    if (T == 0) return SKL_OK;
+    if (!x || !W || !y) return fail(SKL_ERR_PARAM, "null tensor argument");
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int eb = ebytes(s->dtype), kind = s->dtype == SKL_BF16 ? 0 : 1;
+    if (needs_pad(d, s->dtype)) {
+        SklDims dp = pad_dims(d, s->dtype, false);
+        dp.k = dp.Lk = dp.d_in;
+        const DensePad q = dense_pad_plan(d, dp, s->dtype, T, false, di.sms);
+        if (!workspace || ws_bytes < q.total)
+            return fail(SKL_ERR_WORKSPACE, "dense forward workspace too small: need %zu bytes, got %zu", q.total,
+                        ws_bytes);
+        const void *xp, *wp, *bp;
+        SKL_TRY(repad_in(x, eb, 1, T, d.d_in, workspace, q.x, T, dp.d_in, st, &xp));
+        SKL_TRY(repad_in(W, eb, 1, d.d_out, d.d_in, workspace, q.w, dp.d_out, dp.d_in, st, &wp));
+        SKL_TRY(repad_in(bias, eb, 1, 1, d.d_out, workspace, q.bias, 1, dp.d_out, st, &bp));
+        void* yp = dp.d_out != d.d_out ? at<void>(workspace, q.yg) : y;
+        skl_dense_shape sp = *s;
+        sp.d_in = dp.d_in;
+        sp.d_out = dp.d_out;
+        SKL_TRY(dense_linear_forward(&sp, T, fuse, xp, wp, bp, yp, workspace, q.inner, stream));
+        if (yp != y) SKL_CUDA(launch_repad(yp, eb, 1, T, dp.d_out, y, T, d.d_out, st));
+        return SKL_OK;
+    }
+    const DensePlan q = dense_plan(d, s->dtype, T, false, di.sms);
+    if (!workspace || ws_bytes < q.total)
+        return fail(SKL_ERR_WORKSPACE, "dense forward workspace too small: need %zu bytes, got %zu", q.total, ws_bytes);
+    float* bias32 = at<float>(workspace, q.bias32);
+    SKL_CUDA(launch_to_f32(bias, elem_of(s->dtype), d.d_out, bias32, 0, st));
+    const void* wop = W;
+    if (kind == 1) {  // W as RN-rounded TF32 words (the activation is truncated by the tensor core)
+        SKL_CUDA(launch_to_f32(W, ELEM_F32, d.d_out * d.d_in, at<float>(workspace, q.wr), 1, st));
+        wop = at<void>(workspace, q.wr);
+    }
+    GemmArgs g = {};
+    g.alpha = 1.f;
+    g.bias = bias32;
+    g.relu = (fuse & SKL_FUSE_RELU_OUT) ? 1 : 0;
+    g.out = y;
+    g.ldo = d.d_out;
+    g.out_f32 = eb == 4;
+    View vx{x, T, d.d_in, d.d_in}, vw{wop, d.d_out, d.d_in, d.d_in};
+    return gemm_any(kind, "dense_fwd", vx, vw, (int)T, (int)d.d_out, (int)d.d_in, g, di.sms, st);
+}
+
+skl_status dense_linear_backward(const skl_dense_shape* s, int64_t T, unsigned fuse, const void* grad_y,
+                                 const void* x, const void* W, void* grad_x, float* grad_W, float* grad_b,
+                                 void* workspace, size_t ws_bytes, void* stream) {
+    if (fuse & ~(unsigned)SKL_FUSE_RELU_IN) return fail(SKL_ERR_PARAM, "dense backward: unsupported fuse flags %u", fuse);
+    SklDims d;
+    SKL_TRY(dense_dims(s, d));
+    if (T < 0) return fail(SKL_ERR_SHAPE, "DenseLinear::backward: T must be >= 0");
+    if (!grad_W) return fail(SKL_ERR_PARAM, "null gradient argument");
+    if (T > 0 && (!grad_y || !x || !W)) return fail(SKL_ERR_PARAM, "null tensor argument");
+    DevInfo di;
+    SKL_TRY(check_device(di));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int eb = ebytes(s->dtype), kind = s->dtype == SKL_BF16 ? 0 : 1;
+    if (T == 0) {
+        SKL_CUDA(cudaMemsetAsync(grad_W, 0, (size_t)d.d_out * d.d_in * 4, st));
+        if (grad_b) SKL_CUDA(cudaMemsetAsync(grad_b, 0, (size_t)d.d_out * 4, st));
+        return SKL_OK;
+    }
+    if (needs_pad(d, s->dtype)) {
+        SklDims dp = pad_dims(d, s->dtype, false);
+        dp.k = dp.Lk = dp.d_in;
+        const DensePad q = dense_pad_plan(d, dp, s->dtype, T, true, di.sms);
+        if (!workspace || ws_bytes < q.total)
+            return fail(SKL_ERR_WORKSPACE, "dense backward workspace too small: need %zu bytes, got %zu", q.total,
+                        ws_bytes);
+        const void *xp, *gp, *wp;
+        SKL_TRY(repad_in(x, eb, 1, T, d.d_in, workspace, q.x, T, dp.d_in, st, &xp));
+        SKL_TRY(repad_in(grad_y, eb, 1, T, d.d_out, workspace, q.yg, T, dp.d_out, st, &gp));
+        SKL_TRY(repad_in(W, eb, 1, d.d_out, d.d_in, workspace, q.w, dp.d_out, dp.d_in, st, &wp));
+        void* gxp = (grad_x && dp.d_in != d.d_in) ? at<void>(workspace, q.dx) : grad_x;
+        float* dwp = at<float>(workspace, q.dw);
+        float* dbp = (grad_b && dp.d_out != d.d_out) ? at<float>(workspace, q.db) : grad_b;
+        skl_dense_shape sp = *s;
+        sp.d_in = dp.d_in;
+        sp.d_out = dp.d_out;
+        SKL_TRY(dense_linear_backward(&sp, T, fuse, gp, xp, wp, gxp, dwp, dbp, workspace, q.inner, stream));
+        SKL_CUDA(launch_repad(dwp, 4, 1, dp.d_out, dp.d_in, grad_W, d.d_out, d.d_in, st));
+        if (dbp != grad_b) SKL_CUDA(launch_repad(dbp, 4, 1, 1, dp.d_out, grad_b, 1, d.d_out, st));
+        if (gxp != grad_x) SKL_CUDA(launch_repad(gxp, eb, 1, T, dp.d_in, grad_x, T, d.d_in, st));
+        return SKL_OK;
+    }
+    const DensePlan q = dense_plan(d, s->dtype, T, true, di.sms);
+    if (!workspace || ws_bytes < q.total)
+        return fail(SKL_ERR_WORKSPACE, "dense backward workspace too small: need %zu bytes, got %zu", q.total, ws_bytes);
+    const int elem = elem_of(s->dtype);
+    if (grad_x) {  // dX = G·W: B = Wᵀ [d_in][d_out] (K-major over d_out)
+        void* wT = at<void>(workspace, q.wT);
+        SKL_CUDA(launch_transpose(W, elem, d.d_out, d.d_in, wT, st));
+        if (kind == 1) SKL_CUDA(launch_to_f32(wT, ELEM_F32, d.d_in * d.d_out, static_cast<float*>(wT), 1, st));
+        GemmArgs g = {};
+        g.alpha = 1.f;
+        g.mask = (fuse & SKL_FUSE_RELU_IN) ? x : nullptr;  // Relu::backward of the preceding ReLU (x = its output)
+        g.ld_mask = d.d_in;
+        g.out = grad_x;
+        g.ldo = d.d_in;
+        g.out_f32 = eb == 4;
+        View vg{grad_y, T, d.d_out, d.d_out}, vwt{wT, d.d_in, d.d_out, d.d_out};
+        SKL_TRY(gemm_any(kind, "dense_dX", vg, vwt, (int)T, (int)d.d_in, (int)d.d_out, g, di.sms, st));
+    }
+    // dWᵀ = xᵀ·G and db = Σ_t G: du problem 0 with A = xᵀ [d_in][round8(T)]
+    void* xT = at<void>(workspace, q.xT);
+    SKL_CUDA(launch_transpose(x, elem, T, d.d_in, xT, st, t8(T)));
+    Plan p = {};
+    p.du_part = q.part;
+    p.du_cpart = q.cpart;
+    p.du_tickets = q.tickets;
+    float* dwT = at<float>(workspace, q.dwT);
+    SKL_TRY(run_du(d, T, kind, 1, xT, grad_y, nullptr, x, dwT, nullptr, grad_b, workspace, p, di.sms, st, 1.f));
+    SKL_CUDA(launch_transpose(dwT, ELEM_F32, d.d_in, d.d_out, grad_W, st));
     return SKL_OK;
 }
 

@@ -34,5 +34,14 @@ cudaError_t launch_im2col(const void* img, int elem, const ConvGeom& g, void* co
 cudaError_t launch_col2im(const void* cols, int elem, const ConvGeom& g, void* img, cudaStream_t st);
 cudaError_t launch_tokens_planes(const void* in, int elem, int64_t B, int64_t P, int64_t C, void* out, int to_planes,
                                  cudaStream_t st);
-cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st);
+// [B][R][C] -> [B][R2][C2], zero fill outside the source (pads or crops the inner dims).
+cudaError_t launch_repad(const void* src, int elem_bytes, int64_t B, int64_t R, int64_t C, void* dst, int64_t R2,
+                         int64_t C2, cudaStream_t st);
+// out[c * ld_out + r] = in[r * cols + c]; ld_out <= 0 means rows.
+cudaError_t launch_transpose(const void* in, int elem, int64_t rows, int64_t cols, void* out, cudaStream_t st,
+                             int64_t ld_out = 0);
+cudaError_t launch_gaussian_scaled(int64_t rows, int64_t cols, uint64_t seed, double scale, int elem, void* out,
+                                   cudaStream_t st);
+// fp32 copy of an element-type vector (NULL in -> zeros), optionally TF32-rounded (cvt.rna).
+cudaError_t launch_to_f32(const void* in, int elem, int64_t n, float* out, int round_tf32, cudaStream_t st);
 }  // namespace skl

@@ -83,6 +83,34 @@ class GradBucket:
         return self._reduce(self.flat, group, async_op)
 
 
+@dataclass
+class DenseBucket:
+    """One flat fp32 buffer holding a DenseLinear's dW [d_out, d_in] | db [d_out]
+    (same all-reduce interface as GradBucket; the whole bucket is the head)."""
+
+    flat: object
+    dW: object
+    db: object
+
+    @staticmethod
+    def numel(d_in, d_out):
+        return d_out * d_in + d_out
+
+    @classmethod
+    def allocate(cls, d_in, d_out, device="cuda", dtype=None):
+        import torch
+        flat = torch.zeros(cls.numel(d_in, d_out), dtype=dtype or torch.float32, device=device)
+        return cls(flat, flat[:d_out * d_in].view(d_out, d_in), flat[d_out * d_in:])
+
+    def allreduce_(self, group=None, async_op=False):
+        return GradBucket._reduce(self.flat, group, async_op)
+
+    allreduce_head = allreduce_
+
+    def allreduce_tail(self, group=None, async_op=False):
+        return None
+
+
 def backward_overlapped(skl, s, g, x, saved, S1s, S2s, U1s, U2s, grad_x, bucket: GradBucket, workspace,
                         group=None):
     """Token-sharded backward of one SKLinear layer with the gradient

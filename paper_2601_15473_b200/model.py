@@ -22,9 +22,9 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import (BF16, BWD_ALL, BWD_DU1_DB, BWD_DX_DU2, FUSE_RELU_IN, FUSE_RELU_OUT, ShapeError, SkLinear,
-               SklError, backward_phase, forward, relu_bits_row_words, relu_bits_supported, torch_dtype,
-               workspace_size)
+from . import (BF16, BWD_ALL, BWD_DU1_DB, BWD_DX_DU2, FUSE_RELU_IN, FUSE_RELU_OUT, DenseLinear, ShapeError,
+               SkLinear, SklError, backward_phase, dense_backward, dense_forward, dense_workspace_size, forward,
+               relu_bits_row_words, relu_bits_supported, torch_dtype, workspace_size)
 
 
 class Relu:
@@ -36,7 +36,7 @@ class Relu:
 
 @dataclass
 class _Step:
-    layer: SkLinear
+    layer: object           # SkLinear or DenseLinear
     relu_out: bool          # a ReLU follows (fused into this layer's forward epilogue)
     relu_in: bool = False   # the input came out of a ReLU (its mask is fused into this layer's dX)
     x: object = None        # saved input (needed by the backward: dU2s, the ReLU mask)
@@ -53,16 +53,17 @@ class ChainGrads:
 
 
 class SkChain:
-    """model_forward over a list of SkLinear / Relu layers, with a training backward."""
+    """model_forward over a list of SkLinear / DenseLinear / Relu layers, with a training backward."""
 
     def __init__(self, layers, relu_bits=True):
         """relu_bits: carry each fused ReLU's mask from the forward to the next
         layer's backward as 1 bit per element (skl.h SKL_FUSE_RELU_BITS) where both
         layers' kernels support it, instead of re-reading the ReLU output."""
         layers = list(layers)
+        self._layers = layers
         self.relu_bits = relu_bits
-        if not layers or not isinstance(layers[0], SkLinear):
-            raise ShapeError(1, "SkChain: a chain starts with an SKLinear layer (a leading ReLU has no "
+        if not layers or not isinstance(layers[0], (SkLinear, DenseLinear)):
+            raise ShapeError(1, "SkChain: a chain starts with a Linear / SKLinear layer (a leading ReLU has no "
                                 "producing layer to fuse into)")
         self.steps: list[_Step] = []
         prev_relu = False
@@ -73,7 +74,7 @@ class SkChain:
                 self.steps[-1].relu_out = True
                 prev_relu = True
                 continue
-            if not isinstance(lyr, SkLinear):
+            if not isinstance(lyr, (SkLinear, DenseLinear)):  # nn_model.cpp:117-119
                 raise ShapeError(1, f"model_forward: layer {i} is not part of a Linear/ReLU chain")
             if self.steps and self.steps[-1].layer.d_out != lyr.d_in:
                 raise ShapeError(1, f"SkChain: layer {i} d_in={lyr.d_in} != previous d_out="
@@ -86,13 +87,9 @@ class SkChain:
         self._ws = None
 
     def layers(self):
-        """The chain as a layer list (SkLinear / Relu), e.g. for model_save."""
-        out = []
-        for st in self.steps:
-            out.append(st.layer)
-            if st.relu_out:
-                out.append(Relu())
-        return out
+        """The chain's layer list as given (SkLinear / DenseLinear / Relu, repeated
+        ReLUs kept), e.g. for model_save with the names model_load returned."""
+        return list(self._layers)
 
     @property
     def d_in(self):
@@ -104,7 +101,8 @@ class SkChain:
 
     def _workspace(self, T, device):
         import torch
-        need = max(max(workspace_size(st.layer.shape, T)) for st in self.steps)
+        need = max(max(dense_workspace_size(st.layer.shape, T) if isinstance(st.layer, DenseLinear)
+                       else workspace_size(st.layer.shape, T)) for st in self.steps)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(need, dtype=torch.uint8, device=device)
         return self._ws
@@ -122,10 +120,19 @@ class SkChain:
         for i, st in enumerate(self.steps):
             L = st.layer
             y = torch.empty(T, L.d_out, dtype=td, device=x.device)
+            if isinstance(L, DenseLinear):
+                dense_forward(L.shape, cur, L.W, L.bias, y, ws, fuse=FUSE_RELU_OUT if st.relu_out else 0)
+                if train:
+                    st.x = cur
+                    if i + 1 < len(self.steps):
+                        self.steps[i + 1].bits = None
+                cur = y
+                continue
             saved = torch.empty(L.num_terms * L.low_rank, (T + 7) // 8 * 8, dtype=td, device=x.device) \
                 if train else None
             bits = None
             if train and st.relu_out and self.relu_bits and i + 1 < len(self.steps) and \
+                    isinstance(self.steps[i + 1].layer, SkLinear) and \
                     relu_bits_supported(L.shape) and relu_bits_supported(self.steps[i + 1].layer.shape):
                 bits = torch.empty(T, relu_bits_row_words(L.d_out), dtype=torch.int32, device=x.device)
             forward(L.shape, cur, L.S1s, L.S2s, L.U1s, L.U2s, L.bias, y, saved, ws,
@@ -138,8 +145,12 @@ class SkChain:
         return cur
 
     def allocate_grads(self, device="cuda"):
-        from .dp import GradBucket
-        return [GradBucket.allocate(st.layer.d_in, st.layer.d_out, st.layer.num_terms, st.layer.low_rank,
+        """Per-layer fp32 gradient buckets: GradBucket (dU1s | db | dU2s) for an
+        SKLinear, DenseBucket (dW | db) for a Linear."""
+        from .dp import DenseBucket, GradBucket
+        return [DenseBucket.allocate(st.layer.d_in, st.layer.d_out, device=device)
+                if isinstance(st.layer, DenseLinear) else
+                GradBucket.allocate(st.layer.d_in, st.layer.d_out, st.layer.num_terms, st.layer.low_rank,
                                     device=device) for st in self.steps]
 
     def backward(self, g, buckets=None, group=None, need_grad_x=True, overlap=None, phased=False):
@@ -171,7 +182,13 @@ class SkChain:
             L = st.layer
             gx = torch.empty(T, L.d_in, dtype=td, device=g.device) if (i > 0 or need_grad_x) else None
             fuse = FUSE_RELU_IN if st.relu_in else 0
-            if overlap and phased:
+            if isinstance(L, DenseLinear):
+                dense_backward(L.shape, cur, st.x, L.W, gx, b.dW, b.db, ws, fuse=fuse)
+                if overlap:
+                    w = b.allreduce_(group, async_op=True)
+                    if w is not None:
+                        works.append(w)
+            elif overlap and phased:
                 backward_phase(L.shape, BWD_DU1_DB, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, None,
                                b.dU1s, None, b.db, ws)
                 w = b.allreduce_head(group, async_op=True)

@@ -8,6 +8,9 @@ model_forward (nn_model.cpp:111-122) of a seeded input through each file.
 
 The chain: SKLinear(64->96, L2, k16, Gaussian) + ReLU + SKLinear(96->48, L1,
 k32, Rademacher) + ReLU + SKLinear(48->40, L1, k8, Gaussian); nonzero biases.
+The mixed chain (ref_model_mixed_*): SKLinear(64->96, L2, k16) + ReLU +
+Linear(96->50, dense_linear_init) + ReLU + SKLinear(50->40, L1, k5) -- a dense
+layer and ragged widths (50, k = 5), as a tuner-produced model has them.
 """
 import ctypes
 import json
@@ -26,6 +29,8 @@ import oracle  # noqa: E402
 SPEC = [(0, 64, 96, 2, 16, 101, 0), (1, 0, 0, 0, 0, 0, 0), (0, 96, 48, 1, 32, 202, 1), (1, 0, 0, 0, 0, 0, 0),
         (0, 48, 40, 1, 8, 303, 0)]
 T = 20
+MIXED = [(0, 64, 96, 2, 16, 101, 0), (1, 0, 0, 0, 0, 0, 0), (2, 96, 50, 0, 0, 202, 0), (1, 0, 0, 0, 0, 0, 0),
+         (0, 50, 40, 1, 5, 303, 0)]
 
 
 def main():
@@ -54,6 +59,22 @@ def main():
         print("wrote", path)
     with open(os.path.join(HERE, "ref_model_forward.json"), "w") as f:
         json.dump(out, f, indent=1)
+    mspec = np.array(MIXED, dtype=np.uint64).ravel()
+    mout = {"generator": "tests/golden/make_golden_model.py", "spec": MIXED, "T": T, "x_seed": 7,
+            "x": out["x"]}
+    for dt in ("f32", "f64"):
+        path = os.path.join(HERE, f"ref_model_mixed_{dt}.json")
+        rc = lib.ref_model_save_chain(path.encode(), 1 if dt == "f32" else 0, len(MIXED),
+                                      mspec.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)))
+        assert rc == 0, lib.ref_model_last_error()
+        y = np.empty((40, T))
+        rc = lib.ref_model_forward_file(path.encode(), 64, T, x.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                        40, y.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        assert rc == 0, lib.ref_model_last_error()
+        mout[f"y_{dt}"] = [float(v).hex() for v in y.ravel()]
+        print("wrote", path)
+    with open(os.path.join(HERE, "ref_model_mixed_forward.json"), "w") as f:
+        json.dump(mout, f, indent=1)
 
 
 if __name__ == "__main__":

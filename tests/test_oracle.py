@@ -214,3 +214,22 @@ def test_gaussian_sketch_rounding_fragility(port):
         flips += int(np.sum(bf16_round(pert) != bf16_round(vals)))
         flips += int(np.sum(tf32_round(pert) != tf32_round(vals)))
     assert flips == 0
+
+
+def test_dense_port_is_bit_exact_with_reference():
+    """DenseLinear init / forward / backward of the port (skl_oracle.c) equal the
+    reference's own DenseLinear (nn_layers.cpp:32-59, oracle/_ref) bit for bit."""
+    import oracle
+    if not oracle.available("reference"):
+        pytest.skip("oracle/_ref not built")
+    po, ro = oracle.Oracle("port"), oracle.Oracle("reference")
+    for d_in, d_out, T, seed in ((6, 8, 2, 31), (37, 13, 11, 5), (96, 50, 20, 202)):
+        w, b = po.dense_init(d_in, d_out, seed)
+        w2, b2 = ro.dense_init(d_in, d_out, seed)
+        assert np.array_equal(w, w2) and np.array_equal(b, b2)
+        b = ro.gaussian_matrix(1, d_out, 9)[0]
+        x = ro.gaussian_matrix(d_in, T, 3)
+        g = ro.gaussian_matrix(d_out, T, 4)
+        assert np.array_equal(po.dense_forward(w, b, x), ro.dense_forward(w, b, x))
+        for a, c in zip(po.dense_backward(w, x, g), ro.dense_backward(w, x, g)):
+            assert np.array_equal(a, c)
