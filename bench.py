@@ -17,8 +17,9 @@ with its own binding-roofline fraction.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/librnla_ref.so: the unmodified reference sources, timed by the
-reference's bench::time_op) on all host threads, over a bounded token slice of
-the same workload per step; rank 0 only.
+reference's bench::time_op) on all host threads, on the same workload (c2 at
+full T per step, OMP_PROC_BIND=close OMP_WAIT_POLICY=active; timed calls capped
+at REF_BUDGET_S); rank 0 only.
 """
 from __future__ import annotations
 
@@ -39,7 +40,6 @@ D_IN, D_OUT, L, K_RANK, T_GPU = 768, 3072, 2, 128, 32768
 SEED = 42
 WORKLOAD = (f"c2: SKLinear fwd+bwd d_in={D_IN} d_out={D_OUT} L={L} k={K_RANK}, "
             f"{T_GPU} tokens per GPU (BERT-base FFN shape)")
-CPU_SAMPLE_T = 1024  # tokens per reference CPU step (bounded sample of the same workload)
 RESERVED_SMS = 8     # SMs left to NCCL when N > 1 (NCCL_MAX_CTAS matches)
 
 
@@ -50,6 +50,22 @@ def peaks():
             d = json.load(f)
         return float(d["bf16_tflops"]), float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json, burst)"
     return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def tf32_peak():
+    """Dense TF32 peak: MEASURED_PEAKS.json when the driver measured it, else the
+    figure tools/measure_tf32_peak.py measured on a B200 (cuBLAS fp32 8192^3 with
+    TF32, burst), committed as profiles/r2_tf32_peak.json."""
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        if "tf32_tflops" in d:
+            return float(d["tf32_tflops"]), "measured (MEASURED_PEAKS.json, burst)"
+    q = os.path.join(ROOT, "profiles", "r2_tf32_peak.json")
+    with open(q) as f:
+        d = json.load(f)
+    return float(d["tf32_tflops"]), "measured (profiles/r2_tf32_peak.json: cuBLAS TF32 8192^3, burst)"
 
 
 def flops_per_token(d_in=D_IN, d_out=D_OUT, l=L, k=K_RANK):
@@ -116,30 +132,57 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_baseline_reference(t_sample=CPU_SAMPLE_T, trials=3, warmup=1):
-    """Reference CPU SkLinear fwd+bwd (oracle/_ref) on all host cores, bounded token slice."""
+OMP_ENV = {"OMP_PROC_BIND": "close", "OMP_WAIT_POLICY": "active"}  # BASELINE.md §3 (set before libgomp loads)
+CPU_SLICE_1T = 1024  # tokens of the single-thread sample (a full-T call takes ~2 min on one core)
+
+
+def _cpu_ref_time(T, threads, trials, warmup):
+    """Reference SkLinear fwd+bwd on the c2 layer (oracle/_ref: the unmodified
+    reference sources, timed by its own bench::time_op) -> (mean ms, std ms)."""
+    import oracle
+    o = oracle.Oracle("reference")
+    return o.time_fwd_bwd(D_IN, D_OUT, L, K_RANK, T, SEED, threads, trials, warmup)
+
+
+def cpu_probe(args):
+    """--impl cpu-probe: the N=1 line's cpu_baseline, in its own process so the
+    OpenMP environment applies: c2 at full T on every host core,
+    plus a single-thread sample.  Prints one JSON object."""
     import oracle
     threads = os.cpu_count() or 1
-    if oracle.available("reference"):
-        o = oracle.Oracle("reference")
-        mean_ms, std_ms = o.time_fwd_bwd(D_IN, D_OUT, L, K_RANK, t_sample, SEED, threads, trials, warmup)
-        kind, cores = "reference", threads
-    else:  # scalar C restatement of the reference (oracle/skl_oracle.c)
+    if not oracle.available("reference"):  # scalar C restatement (oracle/skl_oracle.c), single thread
         o = oracle.Oracle("port")
-        t_sample = min(t_sample, 256)
+        t = 256
         p = o.sk_linear_fresh(D_IN, D_OUT, L, K_RANK, SEED)
-        x, g, b = oracle.inputs(D_IN, D_OUT, t_sample, SEED, o)
-        ts = []
-        for i in range(warmup + trials):
-            t0 = time.perf_counter()
-            o.forward(p, b, x)
-            o.backward(p, x, g)
-            if i >= warmup:
-                ts.append((time.perf_counter() - t0) * 1e3)
-        mean_ms, kind, cores = statistics.mean(ts), "port", 1
-    return {"value": t_sample / (mean_ms / 1e3), "unit": "tokens/s", "cores": cores, "kind": kind,
-            "sample": f"c2 shape, {t_sample}-token slice, fwd+bwd f64, mean of {trials} after {warmup} warm-up "
-                      f"(bench::time_op), {mean_ms:.1f} ms/step"}
+        x, g, b = oracle.inputs(D_IN, D_OUT, t, SEED, o)
+        t0 = time.perf_counter()
+        o.forward(p, b, x)
+        o.backward(p, x, g)
+        ms = (time.perf_counter() - t0) * 1e3
+        print(json.dumps({"value": t / (ms / 1e3), "unit": "tokens/s", "cores": 1, "kind": "port",
+                          "sample": f"c2 shape, {t}-token slice, scalar f64 port, 1 call ({ms:.0f} ms)"}))
+        return
+    full_ms, full_std = _cpu_ref_time(T_GPU, threads, 1, 1)
+    one_ms, _ = _cpu_ref_time(CPU_SLICE_1T, 1, 1, 0)
+    print(json.dumps({
+        "value": T_GPU / (full_ms / 1e3), "unit": "tokens/s", "cores": threads, "kind": "reference",
+        "sample": (f"c2 at full T={T_GPU} (same config as the GPU line), fwd+bwd f64 through the reference's "
+                   f"bench::time_op: 1 warm-up + 1 timed call = {full_ms:.0f} ms on {threads} threads, "
+                   f"OMP_PROC_BIND=close OMP_WAIT_POLICY=active"),
+        "same_config": True,
+        "single_thread": {"value": CPU_SLICE_1T / (one_ms / 1e3), "unit": "tokens/s", "cores": 1,
+                          "sample": f"{CPU_SLICE_1T}-token slice of c2, 1 timed call = {one_ms:.0f} ms"}}))
+
+
+def cpu_baseline_reference():
+    """The N=1 line's cpu_baseline: cpu_probe in a subprocess (own OpenMP env)."""
+    env = dict(os.environ, **OMP_ENV)
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--impl", "cpu-probe"], env=env,
+                       capture_output=True, text=True, timeout=900)
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    if r.returncode != 0 or not lines:
+        raise RuntimeError((r.stderr or r.stdout)[-300:])
+    return json.loads(lines[-1])
 
 
 # Other BASELINE.json configs (parity-tested in tests/; reported, not the headline):
@@ -219,13 +262,15 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
         g = capture(step)
         ms = _time_steps(torch, g.replay, steps)
     peak_bf16, peak_bw, _ = peaks()
-    peak_tf = peak_bf16 if dtype == "bf16" else peak_bf16 / 2  # TF32 dense = bf16 / 2 (not separately measured)
+    peak_tf, tf_src = (peak_bf16, "bf16 burst") if dtype == "bf16" else tf32_peak()
     t_roof, bound, flops, bytes_ = roofline_time(d_in, d_out, l, k, T, 2 if dtype == "bf16" else 4, peak_tf, peak_bw)
+    r_pad = (2 * l * k + 63) // 64 * 64
     return {"workload": name, "dtype": dtype, "tokens": T, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3),
             "bound": bound, "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
             "tflops": flops / (ms / 1e3) / 1e12, "hbm_gbs_alg": bytes_ / (ms / 1e3) / 1e9,
-            "fused": bool((2 * l * k + 63) // 64 * 64 <= (512 if dtype == "bf16" else 256)),
-            "peak_tflops_used": peak_tf, "phased_backward": phased, "cuda_graph": graph,
+            # on-chip H: bf16 b2b kernel (R <= 512), TF32 b2b kernel (R <= 256) or wide-rank TF32 kernel (R <= 512)
+            "fused": bool(r_pad <= 512),
+            "peak_tflops_used": peak_tf, "peak_source": tf_src, "phased_backward": phased, "cuda_graph": graph,
             "ms_per_step_eager": ms_eager}
 
 
@@ -281,17 +326,41 @@ def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers
             "tflops": flops / (ms / 1e3) / 1e12, "n_gpus": world, "cuda_graph": graph, "ms_per_step_eager": ms_eager}
 
 
+REF_BUDGET_S = 150.0  # wall-clock cap of the reference arm's timed calls (full-T calls take seconds each)
+
+
 def run_reference(args, rank):
+    """--impl reference: the reference's CPU implementation (oracle/_ref, all host
+    threads, OMP env of BASELINE.md §3) on THIS arm's workload, c2 at full
+    T = 32768 per step.  Warm-up capped at 1 call and the timed calls at what
+    fits REF_BUDGET_S (each call takes seconds); both counts are in the line."""
     if rank != 0:
         return
-    cb = cpu_baseline_reference(CPU_SAMPLE_T, trials=max(1, args.steps), warmup=max(0, args.warmup))
-    v = cb["value"]
-    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": CPU_SAMPLE_T / v * 1e3, "higher_is_better": True,
+    import oracle
+    threads = os.cpu_count() or 1
+    if not oracle.available("reference"):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/librnla_ref.so not built"}))
+        return
+    warm = min(1, max(0, args.warmup))
+    t0 = time.perf_counter()
+    first_ms, _ = _cpu_ref_time(T_GPU, threads, 1, warm)
+    per_call = (time.perf_counter() - t0) / (1 + warm)
+    extra = max(0, min(args.steps - 1, int(REF_BUDGET_S / max(per_call, 1e-3)) - 1))
+    ms = first_ms
+    if extra > 0:
+        m2, _ = _cpu_ref_time(T_GPU, threads, extra, 0)
+        ms = (first_ms + extra * m2) / (1 + extra)
+    timed = 1 + extra
+    v = T_GPU / (ms / 1e3)
+    cb = {"value": v, "unit": "tokens/s", "cores": threads, "kind": "reference", "same_config": True,
+          "sample": (f"c2 at full T={T_GPU} per step (the GPU arm's workload), fwd+bwd f64 via the reference's "
+                     f"bench::time_op, {timed} timed call(s) after {warm} warm-up (capped at {REF_BUDGET_S:.0f} s; "
+                     f"--steps {args.steps}), OMP_PROC_BIND=close OMP_WAIT_POLICY=active")}
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s", "n_gpus": args.gpus, "steps": timed,
+            "warmup": warm, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": WORKLOAD + f" (reference CPU arm: {CPU_SAMPLE_T}-token slices)",
-                       "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
-                       "tokens_per_step": CPU_SAMPLE_T, "parallelism": "host OpenMP"},
+            "config": {"workload": WORKLOAD, "d_in": D_IN, "d_out": D_OUT, "num_terms": L, "low_rank": K_RANK,
+                       "tokens_per_step": T_GPU, "parallelism": f"host OpenMP, {threads} threads"},
             "impl": "reference", "cpu_baseline": cb,
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -314,7 +383,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference", "cpu-probe"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the other-config workloads at N=1")
     args = ap.parse_args()
@@ -328,7 +397,12 @@ def main():
     if args.impl == "ours" and world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
+    if args.impl == "cpu-probe":
+        cpu_probe(args)
+        return
     if args.impl == "reference":
+        for k_, v_ in OMP_ENV.items():  # before the reference library (libgomp) loads
+            os.environ.setdefault(k_, v_)
         run_reference(args, rank)
         return
 
@@ -431,13 +505,16 @@ def main():
     if dom in alg_flops:
         avg_ms = per_kernel[dom]["avg_ms"]
         achieved = alg_flops[dom] / (avg_ms / 1e3) / 1e12
-        traffic = None
+        # dram__bytes_read.sum + dram__bytes_write.sum of this kernel from one `ncu --set full`
+        # capture (not measured in this run: ncu replays kernels); the capture is named in the line
+        traffic, traffic_src = None, None
         tp = os.path.join(ROOT, "profiles", "traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get(dom)
+                tj = json.load(f)
+            traffic, traffic_src = tj.get(dom), tj.get("_source", "profiles/traffic.json")
         roof = {"bound": "tensor", "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-                "frac": achieved / peak_tf, "traffic": traffic, "kernel": dom,
+                "frac": achieved / peak_tf, "traffic": traffic, "traffic_source": traffic_src, "kernel": dom,
                 "kernel_ms": avg_ms, "peak_source": peak_src}
     step_flops = (fpt["fwd"] + fpt["bwd"]) * T
     step_roof = step_flops / (ms / 1e3) / 1e12

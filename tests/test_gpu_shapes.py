@@ -437,3 +437,62 @@ def test_mixed_chain_with_dense_layer(skl, port, dtype_name):
     check_close("layer0 dU1s", _np(cg.layers[0].dU1s), rgu1, dtype_name)
     check_close("layer0 dU2s", _np(cg.layers[0].dU2s), rgu2, dtype_name)
     check_close("grad_x", _np(cg.grad_x), rgx, dtype_name)
+
+
+# --------------------------------------------------------------------------- seeded generation at scale
+LAYER_SHAPES = [
+    (4096, 4096, 3, 256),   # c3 (6.29 M sketch entries)
+    (4096, 4096, 4, 64),    # c4 L4 k64
+    (4096, 4096, 1, 16),    # c4 L1 k16
+    (768, 768, 1, 128),     # c5 projection
+    (768, 3072, 2, 128),    # c5 FFN1 / c2
+    (3072, 768, 2, 128),    # c5 FFN2
+]
+
+
+@pytest.mark.parametrize("dtype_name", ["bf16", "f32"])
+@pytest.mark.parametrize("d_in,d_out,L,k", LAYER_SHAPES)
+def test_generated_layer_rounds_equal_at_config_shapes(skl, port, dtype_name, d_in, d_out, L, k):
+    """sk_linear_fresh(seed 42) on the device -- Gaussian sketches and U, written
+    into the ABI stacks -- equals the reference stream rounded to the element type
+    on EVERY entry, at the c3 / c4 / c5 layer shapes (CUDA's f64
+    log/sin/cos are within 4 ulp of glibc, so only the rounded values can be
+    exact; this checks they are, everywhere)."""
+    import oracle
+    from tests._util import bf16_round
+    dtype = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    lyr = skl.SkLinear(d_in, d_out, L, k, seed=42, dtype=dtype)
+    torch.cuda.synchronize()
+    abi = oracle.to_abi(port.sk_linear_fresh(d_in, d_out, L, k, 42))
+    rnd = bf16_round if dtype_name == "bf16" else (lambda a: a.astype(np.float32).astype(np.float64))
+    for name in ("S1s", "S2s", "U1s", "U2s"):
+        dev = _np(getattr(lyr, name))
+        ref = rnd(abi[name])
+        bad = int(np.count_nonzero(dev != ref))
+        assert bad == 0, f"{name}: {bad} of {ref.size} entries differ after rounding"
+
+
+def test_c2_full_size_against_reference(skl, ref):
+    """BASELINE config 2 at its FULL 32768 tokens against the reference itself
+    (oracle/_ref, multithreaded f64, ~10-30 s): forward and every gradient of the
+    bf16 device path on the same rounded inputs, at the bf16 gates."""
+    import oracle
+    from tests._util import check_close
+    d_in, d_out, L, k, T = 768, 3072, 2, 128, 32768
+    td = torch.bfloat16
+    layer = skl.SkLinear(d_in, d_out, L, k, seed=42, dtype=skl.BF16)
+    x, g, b = oracle.inputs(d_in, d_out, T, 42, ref)
+    X, G = _tdev(x.T, td), _tdev(g.T, td)
+    layer.bias.copy_(_tdev(b, td))
+    saved = torch.empty(L * k, T, dtype=td, device="cuda")
+    y = layer.forward(X, saved=saved)
+    gr = layer.backward(X, G, saved=saved)
+    torch.cuda.synchronize()
+    P = _layer_f64(skl, layer)
+    x64, g64, b64 = _np(X).T.copy(), _np(G).T.copy(), _np(layer.bias)
+    check_close("c2 full y", _np(y), ref.forward(P, b64, x64).T, "bf16", regress=True)
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*ref.backward(P, x64, g64))
+    check_close("c2 full grad_x", _np(gr.grad_x), rgx, "bf16", regress=True)
+    check_close("c2 full dU1s", _np(gr.grad_u1), rgu1, "bf16", regress=True)
+    check_close("c2 full dU2s", _np(gr.grad_u2), rgu2, "bf16", regress=True)
+    check_close("c2 full db", _np(gr.grad_b), rgb, "bf16", regress=True)
