@@ -20,6 +20,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -52,6 +53,21 @@ inline void check_cuda(cudaError_t e, const char* what) {
 }
 
 inline size_t elem_bytes(skl_dtype t) { return t == SKL_BF16 ? 2 : 4; }
+
+// Host value -> element i of an array of the variant's element type (fp32, or
+// bf16 rounded to nearest even from the fp32 value).
+inline void put_elem(uint8_t* dst, size_t i, double v, skl_dtype t) {
+    float f = (float)v;
+    if (t != SKL_BF16) {
+        std::memcpy(dst + 4 * i, &f, 4);
+        return;
+    }
+    uint32_t u;
+    std::memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    const uint16_t h = (uint16_t)(u >> 16);
+    std::memcpy(dst + 2 * i, &h, 2);
+}
 
 // ---------------------------------------------------------------- device memory (RAII)
 class DeviceBuffer {
@@ -144,6 +160,49 @@ class SkLinear {
         s.U2s_.upload(U2s, (size_t)(l * d_in * k) * e, st);
         if (bias) s.bias_.upload(bias, (size_t)d_out * e, st);
         else s.bias_.zero(st);
+        return s;
+    }
+
+    // A layer from sketch DESCRIPTORS and explicit U / bias in the reference's
+    // layout (sk_linear_from_json, nn_model.cpp:290-311): descs = [s1_0, s2_0,
+    // s1_1, ...] (dist, seed) re-realised on the device -- bit-identical to
+    // SketchOp::realized -- and host f64 u1 [L][k][d_in], u2 [L][d_out][k], bias
+    // [d_out] rounded to the element type and transposed into U2s / U1s.
+    struct SketchDesc {
+        skl_dist dist;
+        int64_t rows, cols;
+        uint64_t seed;
+    };
+    static SkLinear from_parts(int64_t d_in, int64_t d_out, int64_t l, int64_t k, skl_dtype dtype,
+                               const std::vector<SketchDesc>& descs, const double* u1, const double* u2,
+                               const double* bias, cudaStream_t st = nullptr) {
+        SkLinear s(d_in, d_out, l, k, dtype);
+        if ((int64_t)descs.size() != 2 * l) throw shape_error("SKLinear: expected 2*num_terms sketches");
+        const size_t e = elem_bytes(dtype);
+        const skl_out_type ot = dtype == SKL_BF16 ? SKL_OUT_BF16 : SKL_OUT_F32;
+        for (int64_t i = 0; i < l; ++i) {
+            const SketchDesc& s1 = descs[2 * i];
+            const SketchDesc& s2 = descs[2 * i + 1];
+            if (s1.rows != k || s1.cols != d_out || s2.rows != k || s2.cols != d_in)
+                throw shape_error("SKLinear: sketch shape disagrees with the layer");
+            check(skl_realize_sketch(s1.dist, k, d_out, s1.seed, 0, 0, ot,
+                                     static_cast<uint8_t*>(s.S2s_.get()) + (size_t)(i * k * d_out) * e, st));
+            check(skl_realize_sketch(s2.dist, k, d_in, s2.seed, 0, 1, ot,
+                                     static_cast<uint8_t*>(s.S1s_.get()) + (size_t)(i * d_in * k) * e, st));
+        }
+        std::vector<uint8_t> U1((size_t)(l * k * d_out) * e), U2((size_t)(l * d_in * k) * e), b((size_t)d_out * e);
+        for (int64_t i = 0; i < l; ++i)
+            for (int64_t j = 0; j < k; ++j) {
+                for (int64_t c = 0; c < d_in; ++c)  // U2s[i][c][j] = u1[i][j][c]
+                    put_elem(U2.data(), (size_t)((i * d_in + c) * k + j), u1[(i * k + j) * d_in + c], dtype);
+                for (int64_t o = 0; o < d_out; ++o)  // U1s[i][j][o] = u2[i][o][j]
+                    put_elem(U1.data(), (size_t)((i * k + j) * d_out + o), u2[(i * d_out + o) * k + j], dtype);
+            }
+        for (int64_t o = 0; o < d_out; ++o) put_elem(b.data(), (size_t)o, bias ? bias[o] : 0.0, dtype);
+        s.U1s_.upload(U1.data(), U1.size(), st);
+        s.U2s_.upload(U2.data(), U2.size(), st);
+        s.bias_.upload(b.data(), b.size(), st);
+        check_cuda(cudaStreamSynchronize(st), "sync");  // host staging is released on return
         return s;
     }
 
@@ -265,6 +324,86 @@ class SkLinear {
 
     skl_shape shape_{};
     DeviceBuffer S1s_, S2s_, U1s_, U2s_, bias_;
+    mutable DeviceBuffer ws_;
+};
+
+// ---------------------------------------------------------------- DenseLinear
+// rnla::nn::DenseLinear (layers.hpp:33-48; nn_layers.cpp:32-59), device-resident,
+// row convention: y = x·Wᵀ + b with W [d_out, d_in] (the reference's w).
+class DenseLinear {
+  public:
+    // dense_linear_init (nn_layers.cpp:51-59): W = gaussian_matrix(d_out, d_in,
+    // seed) * sqrt(2/(d_in+d_out)) generated on the device; zero bias.
+    static DenseLinear fresh(int64_t d_in, int64_t d_out, uint64_t seed, skl_dtype dtype = SKL_BF16,
+                             cudaStream_t st = nullptr) {
+        DenseLinear d(d_in, d_out, dtype);
+        check(skl_dense_init(&d.shape_, seed, d.W_.get(), d.bias_.get(), st));
+        return d;
+    }
+    // Explicit W [d_out, d_in] and bias [d_out] (host arrays, element type of the variant).
+    static DenseLinear with_params(int64_t d_in, int64_t d_out, skl_dtype dtype, const void* W, const void* bias,
+                                   cudaStream_t st = nullptr) {
+        DenseLinear d(d_in, d_out, dtype);
+        d.W_.upload(W, d.W_.bytes(), st);
+        if (bias) d.bias_.upload(bias, d.bias_.bytes(), st);
+        else d.bias_.zero(st);
+        return d;
+    }
+
+    // From host f64 w [d_out][d_in] and b [d_out] (a model file's Linear record).
+    static DenseLinear from_parts(int64_t d_in, int64_t d_out, skl_dtype dtype, const double* w, const double* b,
+                                  cudaStream_t st = nullptr) {
+        const size_t e = elem_bytes(dtype);
+        std::vector<uint8_t> W((size_t)(d_out * d_in) * e), B((size_t)d_out * e);
+        for (int64_t i = 0; i < d_out * d_in; ++i) put_elem(W.data(), (size_t)i, w[i], dtype);
+        for (int64_t o = 0; o < d_out; ++o) put_elem(B.data(), (size_t)o, b ? b[o] : 0.0, dtype);
+        DenseLinear d = with_params(d_in, d_out, dtype, W.data(), B.data(), st);
+        check_cuda(cudaStreamSynchronize(st), "sync");
+        return d;
+    }
+
+    int64_t d_in() const { return shape_.d_in; }
+    int64_t d_out() const { return shape_.d_out; }
+    skl_dtype dtype() const { return shape_.dtype; }
+    const skl_dense_shape& shape() const { return shape_; }
+    void* W() const { return W_.get(); }
+    void* bias() const { return bias_.get(); }
+
+    // DenseLinear::forward: x [T, d_in] -> y [T, d_out]; fuse = SKL_FUSE_RELU_OUT.
+    void forward(const void* x, int64_t T, void* y, cudaStream_t st = nullptr, unsigned fuse = 0) const {
+        if (T < 0) throw shape_error("DenseLinear::forward: negative token count");
+        void* ws = workspace(T, st);
+        check(dense_linear_forward(&shape_, T, fuse, x, W_.get(), bias_.get(), y, ws, ws_.bytes(), st));
+    }
+    // DenseLinear::backward into caller buffers: grad_x [T, d_in] (nullable),
+    // dW [d_out, d_in] and db [d_out] fp32 (db nullable); fuse = SKL_FUSE_RELU_IN.
+    void backward_into(const void* x, const void* grad_out, int64_t T, void* grad_x, float* dW, float* db,
+                       cudaStream_t st = nullptr, unsigned fuse = 0) const {
+        if (T < 0) throw shape_error("DenseLinear::backward: negative token count");
+        void* ws = workspace(T, st);
+        check(dense_linear_backward(&shape_, T, fuse, grad_out, x, W_.get(), grad_x, dW, db, ws, ws_.bytes(), st));
+    }
+
+  private:
+    DenseLinear(int64_t d_in, int64_t d_out, skl_dtype dtype) {
+        if (d_in < 1 || d_out < 1) throw shape_error("DenseLinear: d_in and d_out must be >= 1");
+        shape_ = skl_dense_shape{d_in, d_out, dtype};
+        W_ = DeviceBuffer((size_t)(d_out * d_in) * elem_bytes(dtype));
+        bias_ = DeviceBuffer((size_t)d_out * elem_bytes(dtype));
+    }
+    void* workspace(int64_t T, cudaStream_t st) const {
+        size_t f = 0, b = 0;
+        check(skl_dense_workspace_size(&shape_, T, &f, &b));
+        const size_t need = f > b ? f : b;
+        if (ws_.bytes() < need) {
+            check_cuda(cudaStreamSynchronize(st), "sync");
+            ws_ = DeviceBuffer(need);
+        }
+        return ws_.get();
+    }
+
+    skl_dense_shape shape_{};
+    DeviceBuffer W_, bias_;
     mutable DeviceBuffer ws_;
 };
 

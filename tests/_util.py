@@ -48,12 +48,24 @@ GATES = {
 }
 
 
-# Regression bounds: about 2x the rel_fro the kernels measure on the large parity
-# shapes (tests/golden/parity_errors.json, written by a GPU run with
-# SKL_PARITY_LOG set).  Far inside the gates above, so a numerics regression
-# that stays within tolerance -- e.g. truncating H to bf16 / TF32 instead of
-# rounding to nearest -- still fails.  Applied with check_close(..., regress=True).
-REGRESS = {"bf16": 5e-3, "tf32": 1.7e-3}
+# Regression bounds: about 2x the rel_fro the kernels measure on the parity
+# shapes (per output, from a GPU run with SKL_PARITY_LOG set:
+# tests/golden/parity_errors_r2.json).  Far inside the gates above, so a
+# numerics regression that stays within tolerance -- e.g. truncating H to bf16
+# / TF32 instead of rounding to nearest -- still fails.  Applied with
+# check_close(..., regress=True).
+REGRESS = {
+    "bf16": {"y": 4.1e-3, "saved": 3.4e-3, "grad_x": 4.8e-3, "dU": 3.5e-3, "db": 1e-6},
+    "tf32": {"y": 8e-4, "saved": 8e-4, "grad_x": 1.2e-3, "dU": 1.7e-3, "db": 1e-6},
+}
+
+
+def _kind(name: str) -> str:
+    n = name.lower()
+    for key, kind in (("grad_x", "grad_x"), ("du1", "dU"), ("du2", "dU"), ("saved", "saved"), ("db", "db")):
+        if key in n:
+            return kind
+    return "y"
 
 
 def check_close(name, approx, exact, variant="bf16", regress=False):
@@ -67,5 +79,6 @@ def check_close(name, approx, exact, variant="bf16", regress=False):
     assert rf <= g["rel_fro"] and ma <= g["max_abs"], (
         f"{name}: rel_fro={rf:.3e} (gate {g['rel_fro']:.0e}), max_abs/max|ref|={ma:.3e} (gate {g['max_abs']:.0e})")
     if regress:
-        assert rf <= REGRESS[variant], f"{name}: rel_fro={rf:.3e} above the regression bound {REGRESS[variant]:.1e}"
+        bound = REGRESS[variant][_kind(name)]
+        assert rf <= bound, f"{name}: rel_fro={rf:.3e} above the regression bound {bound:.1e}"
     return rf, ma

@@ -1,0 +1,263 @@
+// test_chain_dp.cpp -- C++ host (no PyTorch) tests of the chain, model files
+// and data-parallel plumbing: include/skl_chain.hpp, skl_model.hpp, skl_dp.hpp.
+//
+//   * a model file the REFERENCE wrote (tests/golden/ref_model_mixed_*.json:
+//     SKLinear + ReLU + Linear + ReLU + SKLinear, ragged widths) loads through
+//     skl::model_load and reproduces the reference's model_forward
+//     (nn_model.cpp:111-122) at the bf16 / TF32 gates;
+//   * Chain::backward (fused ReLU masks, 1-bit masks, Linear layers) equals the
+//     same layers called one by one, bitwise;
+//   * the overlapped data-parallel schedule over a real NCCL
+//     communicator made from a unique-id file: DU1_DB -> all-reduce(dU1s|db) on
+//     the comm stream while DX_DU2 runs, and per-layer bucket all-reduces in a
+//     chain, with ncclCommGetAsyncError polling; at world size 1 the reduced
+//     buckets equal the local gradients bitwise.
+// One PASS/FAIL line per criterion; exit code = failures (77 = no GPU).
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <fstream>
+#include <string>
+#include <vector>
+
+#include <unistd.h>
+
+#include "skl_model.hpp"
+
+namespace {
+
+int g_fail = 0;
+void report(const std::string& name, bool ok, const std::string& detail = "") {
+    std::printf("%s %s%s%s\n", ok ? "PASS" : "FAIL", name.c_str(), detail.empty() ? "" : "  ", detail.c_str());
+    if (!ok) ++g_fail;
+}
+
+using vec = std::vector<double>;
+
+vec download(const void* p, size_t n, skl_dtype t) {
+    std::vector<uint8_t> h(n * skl::elem_bytes(t));
+    skl::check_cuda(cudaMemcpy(h.data(), p, h.size(), cudaMemcpyDeviceToHost), "download");
+    vec out(n);
+    for (size_t i = 0; i < n; ++i) {
+        if (t == SKL_BF16) {
+            uint16_t b;
+            std::memcpy(&b, h.data() + 2 * i, 2);
+            uint32_t u = (uint32_t)b << 16;
+            float f;
+            std::memcpy(&f, &u, 4);
+            out[i] = f;
+        } else {
+            float f;
+            std::memcpy(&f, h.data() + 4 * i, 4);
+            out[i] = f;
+        }
+    }
+    return out;
+}
+
+bool gate(const vec& a, const vec& b, skl_dtype t, std::string& detail) {
+    double num = 0, den = 0, m = 0, r = 0;
+    for (size_t i = 0; i < a.size(); ++i) {
+        num += (a[i] - b[i]) * (a[i] - b[i]);
+        den += b[i] * b[i];
+        m = std::fmax(m, std::fabs(a[i] - b[i]));
+        r = std::fmax(r, std::fabs(b[i]));
+    }
+    const double rf = std::sqrt(num) / std::sqrt(den > 0 ? den : 1.0), ma = m / (r > 0 ? r : 1.0);
+    char buf[128];
+    std::snprintf(buf, sizeof buf, "rel_fro=%.3e max_abs/max|ref|=%.3e", rf, ma);
+    detail = buf;
+    return t == SKL_BF16 ? (rf <= 1e-2 && ma <= 2e-2) : (rf <= 2e-3 && ma <= 2e-3);
+}
+
+bool same_bytes(const void* a, const void* b, size_t n) {
+    std::vector<uint8_t> x(n), y(n);
+    skl::check_cuda(cudaMemcpy(x.data(), a, n, cudaMemcpyDeviceToHost), "d2h");
+    skl::check_cuda(cudaMemcpy(y.data(), b, n, cudaMemcpyDeviceToHost), "d2h");
+    return x == y;
+}
+
+std::string g_root;
+
+// ---------------------------------------------------------------- model files
+void test_reference_model_file() {
+    nlohmann::json g;
+    std::ifstream(g_root + "/tests/golden/ref_model_mixed_forward.json") >> g;
+    const int64_t T = g.at("T"), d_in = 64, d_out = 40;
+    vec x;
+    for (const auto& v : g.at("x")) x.push_back(std::strtod(v.get<std::string>().c_str(), nullptr));  // [64 x T]
+    for (const char* dt : {"f32", "f64"}) {
+        vec yref;
+        for (const auto& v : g.at(std::string("y_") + dt)) yref.push_back(std::strtod(v.get<std::string>().c_str(), nullptr));
+        for (skl_dtype t : {SKL_F32_TF32, SKL_BF16}) {
+            skl::Model m = skl::model_load(g_root + "/tests/golden/ref_model_mixed_" + dt + ".json", t);
+            bool types = m.names.size() == 5 && std::holds_alternative<skl::DenseLinear>(m.chain->layer(2)) &&
+                         std::holds_alternative<skl::Relu>(m.chain->layer(1));
+            std::vector<uint8_t> xa((size_t)(T * d_in) * skl::elem_bytes(t));
+            for (int64_t r = 0; r < d_in; ++r)
+                for (int64_t c = 0; c < T; ++c) skl::put_elem(xa.data(), (size_t)(c * d_in + r), x[r * T + c], t);
+            skl::DeviceBuffer X(xa.size());
+            X.upload(xa.data(), xa.size());
+            const void* y = m.forward(X.get(), T);
+            skl::check_cuda(cudaDeviceSynchronize(), "sync");
+            const vec yd = download(y, (size_t)(T * d_out), t);
+            vec yc(yd.size());
+            for (int64_t o = 0; o < d_out; ++o)
+                for (int64_t c = 0; c < T; ++c) yc[o * T + c] = yd[c * d_out + o];
+            std::string d;
+            report(std::string("reference-saved mixed model (") + dt + ") -> model_forward " +
+                       (t == SKL_BF16 ? "bf16" : "tf32"),
+                   types && gate(yc, yref, t, d), d);
+        }
+    }
+    bool threw = false;
+    try {
+        skl::model_load(g_root + "/tests/golden/does_not_exist.json");
+    } catch (const skl::load_error&) {
+        threw = true;
+    }
+    report("model_load of a missing file throws load_error", threw);
+}
+
+// ---------------------------------------------------------------- chain vs layer by layer
+void test_chain_matches_layers(skl_dtype t) {
+    const int64_t T = 300;
+    const size_t e = skl::elem_bytes(t);
+    std::vector<skl::Chain::Layer> ls;
+    ls.emplace_back(skl::SkLinear::fresh(256, 512, 2, 64, 1, SKL_DIST_GAUSSIAN, t));
+    ls.emplace_back(skl::Relu{});
+    ls.emplace_back(skl::SkLinear::fresh(512, 128, 1, 64, 2, SKL_DIST_GAUSSIAN, t));
+    ls.emplace_back(skl::Relu{});
+    ls.emplace_back(skl::DenseLinear::fresh(128, 72, 3, t));
+    ls.emplace_back(skl::Relu{});
+    ls.emplace_back(skl::SkLinear::fresh(72, 40, 1, 16, 4, SKL_DIST_GAUSSIAN, t));
+    skl::Chain ch(std::move(ls));
+    std::vector<uint8_t> xh((size_t)(T * 256) * e), gh((size_t)(T * 40) * e);
+    for (size_t i = 0; i < (size_t)(T * 256); ++i) skl::put_elem(xh.data(), i, std::sin(0.37 * (double)i), t);
+    for (size_t i = 0; i < (size_t)(T * 40); ++i) skl::put_elem(gh.data(), i, std::cos(0.11 * (double)i), t);
+    skl::DeviceBuffer X(xh.size()), G(gh.size()), GX((size_t)(T * 256) * e);
+    X.upload(xh.data(), xh.size());
+    G.upload(gh.data(), gh.size());
+    const void* y = ch.forward(X.get(), T);
+    ch.backward(G.get(), T, nullptr, GX.get());
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+
+    // the same layers one by one, x-mask form of every fused ReLU
+    const auto& A = std::get<skl::SkLinear>(ch.layer(0));
+    const auto& B = std::get<skl::SkLinear>(ch.layer(2));
+    const auto& D = std::get<skl::DenseLinear>(ch.layer(4));
+    const auto& C = std::get<skl::SkLinear>(ch.layer(6));
+    skl::DeviceBuffer a1((size_t)(T * 512) * e), a2((size_t)(T * 128) * e), a3((size_t)(T * 72) * e),
+        y4((size_t)(T * 40) * e);
+    skl::DeviceBuffer sA(A.saved_bytes(T)), sB(B.saved_bytes(T)), sC(C.saved_bytes(T));
+    A.forward(X.get(), T, a1.get(), sA.get(), nullptr, SKL_FUSE_RELU_OUT);
+    B.forward(a1.get(), T, a2.get(), sB.get(), nullptr, SKL_FUSE_RELU_OUT);
+    D.forward(a2.get(), T, a3.get(), nullptr, SKL_FUSE_RELU_OUT);
+    C.forward(a3.get(), T, y4.get(), sC.get());
+    const skl::SkBucket kC = skl::SkBucket::of(C), kB = skl::SkBucket::of(B), kA = skl::SkBucket::of(A);
+    skl::DeviceBuffer bC(kC.count() * 4), bB(kB.count() * 4), bA(kA.count() * 4), bD((size_t)(72 * 128 + 72) * 4);
+    skl::DeviceBuffer g3((size_t)(T * 72) * e), g2((size_t)(T * 128) * e), g1((size_t)(T * 512) * e),
+        g0((size_t)(T * 256) * e);
+    float* pC = bC.as<float>();
+    C.backward_into(a3.get(), G.get(), T, sC.get(), g3.get(), kC.dU1s(pC), kC.dU2s(pC), kC.db(pC), nullptr,
+                    SKL_BWD_ALL, SKL_FUSE_RELU_IN);
+    D.backward_into(a2.get(), g3.get(), T, g2.get(), bD.as<float>(), bD.as<float>() + 72 * 128, nullptr,
+                    SKL_FUSE_RELU_IN);
+    float* pB = bB.as<float>();
+    B.backward_into(a1.get(), g2.get(), T, sB.get(), g1.get(), kB.dU1s(pB), kB.dU2s(pB), kB.db(pB), nullptr,
+                    SKL_BWD_ALL, SKL_FUSE_RELU_IN);
+    float* pA = bA.as<float>();
+    A.backward_into(X.get(), g1.get(), T, sA.get(), g0.get(), kA.dU1s(pA), kA.dU2s(pA), kA.db(pA));
+    skl::check_cuda(cudaDeviceSynchronize(), "sync");
+    const char* tn = t == SKL_BF16 ? " (bf16)" : " (tf32)";
+    report(std::string("chain forward == layer by layer, bitwise") + tn, same_bytes(y, y4.get(), y4.bytes()));
+    const bool grads = same_bytes(ch.grads(3).get(), bC.get(), bC.bytes()) &&
+                       same_bytes(ch.grads(2).get(), bD.get(), bD.bytes()) &&
+                       same_bytes(ch.grads(1).get(), bB.get(), bB.bytes()) &&
+                       same_bytes(ch.grads(0).get(), bA.get(), bA.bytes()) && same_bytes(GX.get(), g0.get(), g0.bytes());
+    report(std::string("chain backward (fused / 1-bit ReLU masks, Linear) == layer by layer, bitwise") + tn, grads);
+}
+
+// ---------------------------------------------------------------- data parallel over NCCL
+void test_dp_overlapped() {
+    const std::string id_file = "/tmp/skl_dp_test_" + std::to_string(::getpid()) + ".id";
+    skl::Dp dp = skl::Dp::from_id_file(id_file, 0, 1, 0);
+    std::remove(id_file.c_str());
+    const int64_t T = 4096;
+    skl::SkLinear L = skl::SkLinear::fresh(768, 3072, 2, 128, 42);
+    std::vector<uint8_t> xh((size_t)(T * 768) * 2), gh((size_t)(T * 3072) * 2);
+    for (size_t i = 0; i < (size_t)(T * 768); ++i) skl::put_elem(xh.data(), i, std::sin(0.01 * (double)i), SKL_BF16);
+    for (size_t i = 0; i < (size_t)(T * 3072); ++i) skl::put_elem(gh.data(), i, std::cos(0.02 * (double)i), SKL_BF16);
+    skl::DeviceBuffer X(xh.size()), G(gh.size()), Y((size_t)(T * 3072) * 2), S(L.saved_bytes(T));
+    X.upload(xh.data(), xh.size());
+    G.upload(gh.data(), gh.size());
+    cudaStream_t st;
+    skl::check_cuda(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking), "stream");
+    L.forward(X.get(), T, Y.get(), S.get(), st);
+    const skl::SkBucket k = skl::SkBucket::of(L);
+    skl::DeviceBuffer ref(k.count() * 4), red(k.count() * 4), gx1((size_t)(T * 768) * 2), gx2((size_t)(T * 768) * 2);
+    float* pr = ref.as<float>();
+    L.backward_into(X.get(), G.get(), T, S.get(), gx1.get(), k.dU1s(pr), k.dU2s(pr), k.db(pr), st);
+    skl::backward_overlapped(L, dp, X.get(), G.get(), T, S.get(), gx2.get(), red.as<float>(), st);
+    dp.join(st);
+    dp.synchronize();
+    skl::check_cuda(cudaStreamSynchronize(st), "sync");
+    report("overlapped DP backward over NCCL (world 1): all-reduced bucket == local gradients, bitwise",
+           same_bytes(ref.get(), red.get(), ref.bytes()) && same_bytes(gx1.get(), gx2.get(), gx1.bytes()) &&
+               dp.collectives_issued() == 2);
+
+    // chain with per-layer bucket all-reduces overlapping the layers below
+    std::vector<skl::Chain::Layer> ls;
+    ls.emplace_back(skl::SkLinear::fresh(768, 3072, 2, 128, 5));
+    ls.emplace_back(skl::Relu{});
+    ls.emplace_back(skl::SkLinear::fresh(3072, 768, 2, 128, 6));
+    skl::Chain ch(std::move(ls));
+    skl::DeviceBuffer G2((size_t)(T * 768) * 2);
+    G2.upload(xh.data(), xh.size());
+    ch.forward(X.get(), T, st);
+    ch.backward(G2.get(), T, st);
+    skl::check_cuda(cudaStreamSynchronize(st), "sync");
+    std::vector<std::vector<uint8_t>> local;
+    for (size_t j = 0; j < ch.num_steps(); ++j) {
+        local.emplace_back(ch.grads(j).bytes());
+        ch.grads(j).download(local.back().data(), local.back().size());
+    }
+    ch.forward(X.get(), T, st);
+    ch.backward(G2.get(), T, st, nullptr, &dp);
+    dp.join(st);
+    dp.synchronize();
+    skl::check_cuda(cudaStreamSynchronize(st), "sync");
+    bool ok = dp.collectives_issued() == 4;
+    for (size_t j = 0; j < ch.num_steps(); ++j) {
+        std::vector<uint8_t> h(ch.grads(j).bytes());
+        ch.grads(j).download(h.data(), h.size());
+        skl::check_cuda(cudaDeviceSynchronize(), "sync");
+        ok = ok && h == local[j];
+    }
+    report("chain backward with per-layer bucket all-reduce over NCCL == local, bitwise", ok);
+    const auto r = skl::shard_range(32768, 3, 8);
+    report("shard_range balanced and contiguous", r.first == 12288 && r.second == 16384 &&
+                                                     skl::shard_range(10, 2, 3).first == 7);
+    cudaStreamDestroy(st);
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+        std::printf("SKIP no CUDA device\n");
+        return 77;
+    }
+    g_root = argc > 1 ? argv[1] : ".";
+    try {
+        test_reference_model_file();
+        test_chain_matches_layers(SKL_BF16);
+        test_chain_matches_layers(SKL_F32_TF32);
+        test_dp_overlapped();
+    } catch (const std::exception& e) {
+        report(std::string("uncaught exception: ") + e.what(), false);
+    }
+    std::printf("%d failure(s)\n", g_fail);
+    return g_fail;
+}
