@@ -197,7 +197,10 @@ void test_dp_overlapped() {
     const skl::SkBucket k = skl::SkBucket::of(L);
     skl::DeviceBuffer ref(k.count() * 4), red(k.count() * 4), gx1((size_t)(T * 768) * 2), gx2((size_t)(T * 768) * 2);
     float* pr = ref.as<float>();
-    L.backward_into(X.get(), G.get(), T, S.get(), gx1.get(), k.dU1s(pr), k.dU2s(pr), k.db(pr), st);
+    // the same two phases without the collectives (the phase split changes du's
+    // split-T order, so the fused single-launch backward is not the bitwise reference)
+    L.backward_into(X.get(), G.get(), T, S.get(), nullptr, k.dU1s(pr), nullptr, k.db(pr), st, SKL_BWD_DU1_DB);
+    L.backward_into(X.get(), G.get(), T, S.get(), gx1.get(), nullptr, k.dU2s(pr), nullptr, st, SKL_BWD_DX_DU2);
     skl::backward_overlapped(L, dp, X.get(), G.get(), T, S.get(), gx2.get(), red.as<float>(), st);
     dp.join(st);
     dp.synchronize();
