@@ -28,6 +28,17 @@
 // (two warpgroups splitting the columns of every tile).
 // kCG == 2 runs cta_group::2 (M = 256 tokens per CTA pair, each CTA keeps
 // its 128 rows of H in its own TMEM, B operands are split across the pair).
+//
+// R-split (kRS, R > 512, e.g. BASELINE c3: R = 1536).  A CTA pair holds at most
+// R = 512 of bf16 H next to its GEMM2 accumulators, so a cluster of nsplit
+// pairs (2 * nsplit CTAs) shares one 256-token tile: pair p computes the
+// R-slice H_p = X · Acat[:, p*r_loc, +r_loc) (GEMM1, as above) and the partial
+// D_p = H_p · Bcat[p*r_loc, +r_loc) of every output tile (GEMM2).  The partials
+// are summed over DSMEM along the chain 0 -> 1 -> ... -> nsplit-1 (each pair
+// adds the running sum it receives to its own accumulator and forwards it, in
+// 32-column halves through one 16 KB slot per epilogue warpgroup), so the sum
+// order is fixed (deterministic) and only the last pair applies alpha / bias
+// and stores the tile.  H still never leaves the chip.
 #pragma once
 
 #include "sm100.cuh"
@@ -35,13 +46,6 @@
 #ifndef SKL_FWD_BIAS_TAB
 #define SKL_FWD_BIAS_TAB 1  // 0 measured: 96 -> 106 us at c2 (per-tile bias loads cost more than the 6th stage)
 #endif
-#ifndef SKL_SPLIT_RING
-#define SKL_SPLIT_RING 0  // measured at c2: fwd 96 -> 100-115 us, bwd 106 -> 105-133 us (off)
-#endif
-#ifndef SKL_FWD_SINGLE_PASS
-#define SKL_FWD_SINGLE_PASS 0  // measured: 99 -> 116 us at c2 (3 stages starve GEMM2)
-#endif
-
 namespace skl {
 
 struct B2BArgs {
@@ -54,10 +58,9 @@ struct B2BArgs {
     int save_col0, save_cols;
     int Lk, k, dS;      // direct modes: L*k, k, and the term row stride of the [L*d][k] views
     int bias_bf16;      // bias pointer holds bf16 (direct modes skip the fp32 copy)
-    int b2tall;         // kMode 1: B2 maps use {64, 64*kKbPerStage2} boxes (one load per stage)
     int b1rows;         // rows per K-major B1 TMA box (largest that tiles every chunk; big boxes
                         // matter: per-SM TMA ingest grows ~2.5x from 4 KB to 16 KB boxes)
-    int dbg;            // perf-bisection switches (SKL_B2B_DEBUG): 1 skip GEMM2 epilogue math/stores, 4 skip GEMM2 MMAs
+    int nsplit, r_loc;  // R-split (kRS): pairs per cluster and R columns per pair (else 1, R_pad)
     long long ld_save;
     // Fused neighbours of the layer in a Linear/ReLU chain (nn_model.cpp:111-122):
     int relu;           // forward: out = max(0, ·)  (Relu::forward, nn_layers.cpp:341-345)
@@ -107,46 +110,24 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-// Per-CTA cycle accounting for perf analysis (SKL_B2B_DEBUG bit 32):
-// [0] MMA waits on GEMM1 stages, [1] on GEMM2 stages, [2] on TMEM slots,
-// [3] on bf16-H readiness, [4] MMA loop total, [5] producer waits (GEMM1),
-// [6] producer waits (GEMM2), [7] producer total.
-__device__ unsigned long long g_b2b_prof[296][8];
-// Epilogue (warp 4 lane 0): [0] waits on GEMM2 accumulators, [1] bulk-store
-// buffer reuse, [2]/[3] epilogue named barriers, [4] waits on GEMM1 chunks,
-// [5] epilogue total.
-__device__ unsigned long long g_b2b_eprof[296][8];
-// SKL_B2B_DEBUG & 64: %globaltimer (ns) per CTA at [0] entry, [1] after the
-// prologue, [2] epilogue done (stores drained), [3] exit.
-__device__ unsigned long long g_b2b_ts[296][4];
-#define SKL_TIMED(slot, call)                                                  \
-    do {                                                                       \
-        if (args.dbg & 32) {                                                   \
-            const long long t0_ = clock64();                                   \
-            call;                                                              \
-            prof[slot] += (unsigned long long)(clock64() - t0_);               \
-        } else {                                                               \
-            call;                                                              \
-        }                                                                      \
-    } while (0)
-
-template <int kCG, int kMode, int kKind = 0, bool kMask = false>
+template <int kCG, int kMode, int kKind = 0, bool kMask = false, bool kRS = false>
 struct B2BCfg {
     // kKind 1 (TF32, fp32 I/O): a k-block is 32 fp32 (still 128 B per row, so
     // every smem tile / descriptor has the bf16 byte geometry); the output
     // staging doubles (fp32 tiles) and costs one stage.
     static_assert(kKind == 0 || kMode == 0, "the TF32 fused kernel streams packed panels (kMode 0)");
+    static_assert(!kRS || (kCG == 2 && kKind == 0 && !kMask), "the R-split runs bf16 CTA pairs, no fused mask");
     static constexpr int kElem = kKind == 0 ? 2 : 4;
     static constexpr int kBK = 128 / kElem;                  // elements per k-block
     static constexpr int kOutBytes = kKind == 0 ? 16384 : 32768;  // per epilogue group
     // The backward's GEMM1 (K = d_out, 80% of its MMAs) runs single-pass: one
     // A1 tile feeds both 256-wide chunks, so G is read once instead of twice;
     // its stages therefore hold A1 + B1 for all of R (48 KB).
-    static constexpr bool kSinglePassG1 = (kMode == 2 || (kMode == 1 && SKL_FWD_SINGLE_PASS)) && kCG == 2;
+    static constexpr bool kSinglePassG1 = kMode == 2 && kCG == 2;
     static constexpr int kStageBytes = (kCG == 1 || kSinglePassG1) ? 48 * 1024 : 32 * 1024;
     // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
-    static constexpr bool kBiasTab = kMode == 1 && SKL_FWD_BIAS_TAB;
+    static constexpr bool kBiasTab = kMode == 1 && !kRS;
     static constexpr int kBiasTabBytes = kBiasTab ? 32 * 1024 : 0;
     static constexpr int kMaxBiasTab = kBiasTabBytes / 4;
     // kMask (backward with a fused ReLU mask): the mask tile of the next output
@@ -154,35 +135,20 @@ struct B2BCfg {
     // epilogue group); the ring gives up the stages that space takes.
     static constexpr bool kMaskStage = kMask;
     static constexpr int kMaskBytes = kMask ? 2 * kOutBytes : 0;
-    static constexpr int kStages0 = (kSinglePassG1 ? (kMode == 1 ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind) -
-                                    (kMaskBytes + kStageBytes - 1) / kStageBytes;
-    // Split rings (kSplit, experiment, off): the activation tiles of GEMM1 (x /
-    // G, from HBM) get their own ring fed by a second producer warp, the
-    // L2-resident weight tiles (B1 chunks, B2) the main ring.  Tested because
-    // the MMA waits on full GEMM1 stages while the producer waits on empty
-    // ones; no split of the same smem beat the combined ring, and dropping a
-    // third of GEMM1's bytes (SKL_B2B_DEBUG & 128) gained only 3 %, so GEMM1
-    // is neither ingest- nor simply ring-depth-bound.
-    static constexpr bool kSplit = SKL_SPLIT_RING && kKind == 0 && kCG == 2;
-    static constexpr int kAOff = kSplit ? 0 : 16384;  // B1 offset inside a main-ring stage
-    static constexpr int kStageA = 16384;
-#ifndef SKL_SPLIT_A2
-#define SKL_SPLIT_A2 6
-#endif
-#ifndef SKL_SPLIT_A1
-#define SKL_SPLIT_A1 4
-#endif
-    static constexpr int kStagesA = !kSplit ? 0 : (kMode == 2 ? SKL_SPLIT_A2 : (kMode == 1 ? SKL_SPLIT_A1 : 5));
-    static constexpr int kStages = !kSplit ? kStages0 : (kMode == 2 ? (12 - SKL_SPLIT_A2) / 2 : (kMode == 1 ? 10 - SKL_SPLIT_A1 : 7));
-    static constexpr int kStageBytesW = !kSplit ? 0 : (kSinglePassG1 ? 32 * 1024 : 16 * 1024);
-    static constexpr int kStageMain = kSplit ? kStageBytesW : kStageBytes;
-    static constexpr int kRingBytes = kStages * kStageMain + kStagesA * kStageA;
+    // kRS: one 16 KB receive slot per epilogue warpgroup ([128 rows][32 fp32],
+    // chunk-swizzled) for the running GEMM2 partial of the previous pair.
+    static constexpr int kRecvBytes = kRS ? 2 * 16384 : 0;
+    static constexpr int kStages = (kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind) -
+                                   (kMaskBytes + kRecvBytes + kStageBytes - 1) / kStageBytes;
+    static constexpr int kAOff = 16384;                      // B1 offset inside a GEMM1 stage
+    static constexpr int kRingBytes = kStages * kStageBytes;
     static constexpr int kB2Rows = 128 / kCG;               // B2 rows per CTA per 128-wide N tile
     static constexpr int kB2KbBytes = kB2Rows * 128;         // one 64-wide k-block of B2
-    static constexpr int kKbPerStage2 = kStageMain / kB2KbBytes;
+    static constexpr int kKbPerStage2 = kStageBytes / kB2KbBytes;
     static constexpr int kB1BoxRows = 32;
-    static constexpr int kSmem =
-        kRingBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + kMaskBytes + 1024 /*align*/ + 512;
+    static constexpr int kSmem = kRingBytes + 2 * kOutBytes + 1024 /*bias ring*/ + kBiasTabBytes + kMaskBytes +
+                                 kRecvBytes + 1024 /*align*/ + 512;
+    static_assert(kStages >= 3, "operand ring too shallow");
     static_assert(kSmem <= 232448, "exceeds the 227 KB dynamic shared memory limit");
 };
 
@@ -195,37 +161,48 @@ struct B2BCfg {
 // kPost: 1 = the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
 // mask), 2 = the same with 1-bit masks (relu_bits / mask_bits); separate
 // instantiations so the plain layer keeps its register budget.
-template <int kCG, int kMode, int kKind, int kPost>
+template <int kCG, int kMode, int kKind, int kPost, bool kRS = false>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
                const __grid_constant__ CUtensorMap tmM, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1>;
-    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][0] = gtimer();
+    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
-    uint8_t* ringA = smem + C::kStages * C::kStageMain;       // kSplit: activation ring
     uint8_t* stage_out = smem + C::kRingBytes;                  // 2 x kOutBytes output staging
     float* bias_s = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes);  // 2 slots x 128 bias values
     float* bias_tab = reinterpret_cast<float*>(stage_out + 2 * C::kOutBytes + 1024);  // kMode 1: bias[N2]
     uint8_t* mask_s = stage_out + 2 * C::kOutBytes + 1024 + C::kBiasTabBytes;  // kMask: [2 groups][kOutBytes]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(mask_s + C::kMaskBytes);
+    uint8_t* recv_s = mask_s + C::kMaskBytes;                   // kRS: [2 groups][128 rows][32 fp32]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(recv_s + C::kRecvBytes);
     uint64_t* full = bars;                            // [kStages]
     uint64_t* empty = bars + C::kStages;              // [kStages]
     uint64_t* tfull1 = bars + 2 * C::kStages;         // [2] GEMM1 chunk accumulated
     uint64_t* hready = tfull1 + 2;                    // [2] chunk converted to bf16 H
     uint64_t* tfull2 = hready + 2;                    // [2] GEMM2 slot accumulated
     uint64_t* tempty2 = tfull2 + 2;                   // [2] GEMM2 slot drained
-    uint64_t* fullA = tempty2 + 2;                    // [kStagesA] (kSplit)
-    uint64_t* emptyA = fullA + C::kStagesA;           // [kStagesA]
-    uint64_t* mfull = emptyA + C::kStagesA;           // [2] kMask: this group's mask tile landed
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mfull + 2);
+    uint64_t* mfull = tempty2 + 2;                    // [2] kMask: this group's mask tile landed
+    uint64_t* rfull = mfull + 2;                      // [2] kRS: this group's receive slot holds a partial
+    uint64_t* sfree = rfull + 2;                      // [2] kRS: the next pair's receive slot is free
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
 
     const uint32_t warp = warp_id();
-    const uint32_t rank = kCG == 2 ? cluster_ctarank() : 0;
+    // Cluster layout: pairs are CTA ranks (2p, 2p+1); kRS clusters hold nsplit pairs.
+    const uint32_t crank = kCG == 2 ? cluster_ctarank() : 0;
+    const uint32_t rank = crank & 1u;                 // rank inside the MMA pair
+    const uint32_t lead = crank & ~1u;                // cluster rank of the pair's leader
+    const uint16_t pmask = (uint16_t)(3u << lead);
     const bool leader = rank == 0;
+    const int nsplit = kRS ? args.nsplit : 1;
+    const int sp = kRS ? (int)(crank >> 1) : 0;       // this pair's R-slice
+    const int r_loc = kRS ? args.r_loc : args.R_pad;  // R columns of this pair
+    const int r_off = sp * r_loc;                     // ... starting at this rank index
+    auto commit = [&](uint64_t* bar) {  // MMA completion -> both CTAs of this pair
+        if constexpr (kCG == 2) mma_commit_pair(bar, pmask);
+        else mma_commit<1>(bar);
+    };
 
     if (warp == 0 && elect_one()) {
         prefetch_tmap(&tmA1);
@@ -245,13 +222,10 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&hready[i], 8 * kCG);   // 8 epilogue warps per CTA
             mbar_init(&tfull2[i], 1);
             mbar_init(&tempty2[i], 8 * kCG);
+            mbar_init(&mfull[i], 1);
+            mbar_init(&rfull[i], 4);          // the 4 sender warps of the previous pair's group
+            mbar_init(&sfree[i], 4);          // the 4 receiver warps of the next pair's group
         }
-        for (int s = 0; s < C::kStagesA; ++s) {
-            mbar_init(&fullA[s], kCG);
-            mbar_init(&emptyA[s], 1);
-        }
-        mbar_init(&mfull[0], 1);
-        mbar_init(&mfull[1], 1);
         if constexpr (C::kMaskStage) prefetch_tmap(&tmM);
         fence_barrier_init();
     }
@@ -265,32 +239,29 @@ __global__ void __launch_bounds__(384, 1)
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // inputs of this launch may come from the previous kernel in the stream
     pdl_launch_dependents();  // after the wait: a dependent starts only once our predecessor completed
-    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][1] = gtimer();
 
     const int tile_rows = 128 * kCG;
     const int num_tiles = (args.T + tile_rows - 1) / tile_rows;
-    const int cluster_id = blockIdx.x / kCG;
-    const int num_clusters = gridDim.x / kCG;
-    const int nch = (args.R_pad + 255) / 256;
+    const int cluster_id = blockIdx.x / (kCG * nsplit);
+    const int num_clusters = gridDim.x / (kCG * nsplit);
+    const int nch = (r_loc + 255) / 256;
     const int nkb1 = (args.K1 + C::kBK - 1) / C::kBK;
-    const int nkb2 = args.R_pad / C::kBK;
+    const int nkb2 = r_loc / C::kBK;
     const int nst2 = (nkb2 + C::kKbPerStage2 - 1) / C::kKbPerStage2;
     const int n2_tiles = (args.N2 + 127) / 128;
     // Ping-pong H (R_pad <= 128): tile t's H lives in TMEM region (t & 1) * 128, so
     // GEMM1 of the next tile is issued BEFORE GEMM2 of this one and its HBM reads
     // overlap this tile's output drain (the epilogue's stores) instead of
     // alternating with it.  Producer, MMA issuer and epilogue all follow this order.
-    const bool pp = !C::kSplit && nch == 1 && args.R_pad <= 128 && !(args.dbg & 256);
+    const bool pp = nch == 1 && r_loc <= 128;
 
     if (warp == 0) {
         // ---------------------------------------------------------------- producer
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            const long long tp0 = clock64();
             // activations (x / G) stream through L2 once; the weight panels are re-read by every tile
-            // (SKL_B2B_L2HINT bit 0: activations evict_first when GEMM1 reads them once, bit 1: weights
+            // (l2hint bit 0: activations evict_first when GEMM1 reads them once, bit 1: weights
             // evict_last; a two-pass GEMM1 re-reads its activation tile from L2, so it keeps the default)
             const int hint = args.l2hint;
             const uint64_t pol_norm = l2_evict_normal();
@@ -304,20 +275,18 @@ __global__ void __launch_bounds__(384, 1)
                 const int npass = C::kSinglePassG1 ? 1 : nch;
                 for (int pass = 0; pass < npass; ++pass) {
                     const int c_lo = C::kSinglePassG1 ? 0 : pass, c_hi = C::kSinglePassG1 ? nch : pass + 1;
-                    uint32_t bytes = C::kSplit ? 0 : 16384;
-                    // perf experiment (SKL_B2B_DEBUG & 128): skip chunk 1's B1 bytes (wrong results)
-                    const int c_ld = (args.dbg & 128) ? min(c_hi, c_lo + 1) : c_hi;
-                    for (int c = c_lo; c < c_ld; ++c) bytes += (min(256, args.R_pad - 256 * c) / kCG) * 128;
+                    uint32_t bytes = 16384;
+                    for (int c = c_lo; c < c_hi; ++c) bytes += (min(256, r_loc - 256 * c) / kCG) * 128;
                     for (int kb = 0; kb < nkb1; ++kb) {
-                        SKL_TIMED(5, mbar_wait(&empty[stage], phase ^ 1));
-                        uint8_t* st = smem + stage * C::kStageMain;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
-                        else mbar_arrive_cluster(&full[stage], 0);
-                        if constexpr (!C::kSplit) tma_load_2d_hint<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am, pol_act);
-                        for (int c = c_lo; c < c_ld; ++c) {
-                            const int wc = min(256, args.R_pad - 256 * c);
+                        else mbar_arrive_cluster(&full[stage], lead);
+                        tma_load_2d_hint<kCG>(&tmA1, &full[stage], st, kb * C::kBK, am, pol_act);
+                        for (int c = c_lo; c < c_hi; ++c) {
+                            const int wc = min(256, r_loc - 256 * c);
                             const int brows = wc / kCG;
-                            const int b0 = 256 * c + (int)rank * brows;
+                            const int b0 = r_off + 256 * c + (int)rank * brows;  // global rank index
                             uint8_t* bst = st + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
                             if constexpr (kMode == 0) {
                                 for (int r = 0; r < brows; r += args.b1rows)
@@ -347,21 +316,12 @@ __global__ void __launch_bounds__(384, 1)
                     for (int s = 0; s < nst2; ++s) {
                         const int kb0 = s * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
-                        SKL_TIMED(6, mbar_wait(&empty[stage], phase ^ 1));
-                        uint8_t* st = smem + stage * C::kStageMain;
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
-                        else mbar_arrive_cluster(&full[stage], 0);
-                        if (kMode == 1 && args.b2tall) {
-                            // whole stage (kKbPerStage2 k-blocks, one source half) in one
-                            // {64 x 64*kKbPerStage2} box; layouts coincide for 64-wide N.
-                            const int r0 = kb0 * 64;
-                            tma_load_2d_hint<kCG>(r0 < args.Lk ? &tmB2 : &tmB2b, &full[stage], st, brow,
-                                             r0 < args.Lk ? r0 : r0 - args.Lk, pol_w);
-                            next();
-                            continue;
-                        }
+                        else mbar_arrive_cluster(&full[stage], lead);
                         for (int q = 0; q < nk; ++q) {
-                            const int r0 = (kb0 + q) * C::kBK;  // rank index of this k-block
+                            const int r0 = r_off + (kb0 + q) * C::kBK;  // global rank index of this k-block
                             if constexpr (kMode == 0) {
                                 tma_load_2d_hint<kCG>(&tmB2, &full[stage], st + q * C::kB2KbBytes, r0, brow, pol_w);
                             } else if constexpr (kMode == 1) {  // MN-major rows of [U1s ; S2s]
@@ -385,39 +345,12 @@ __global__ void __launch_bounds__(384, 1)
                 else if (t + num_clusters < num_tiles) load_g1(t + num_clusters);
                 load_g2();
             }
-            if (args.dbg & 32) {
-                prof[7] = (unsigned long long)(clock64() - tp0);
-                for (int i = 5; i < 8; ++i) g_b2b_prof[blockIdx.x][i] = prof[i];
-            }
-        }
-    } else if (warp == 3) {
-        // ---------------------------------------------------------------- producer A (kSplit)
-        if (C::kSplit && elect_one()) {
-            int sa = 0;
-            uint32_t pa = 0;
-            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
-                const int am = t * tile_rows + (int)rank * 128;
-                const int npass = C::kSinglePassG1 ? 1 : nch;
-                for (int pass = 0; pass < npass; ++pass) {
-                    for (int kb = 0; kb < nkb1; ++kb) {
-                        mbar_wait(&emptyA[sa], pa ^ 1);
-                        if (leader) mbar_arrive_expect_tx(&fullA[sa], (uint32_t)C::kStageA * kCG);
-                        else mbar_arrive_cluster(&fullA[sa], 0);
-                        tma_load_2d<kCG>(&tmA1, &fullA[sa], ringA + sa * C::kStageA, kb * C::kBK, am);
-                        if (++sa == C::kStagesA) { sa = 0; pa ^= 1; }
-                    }
-                }
-            }
         }
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer
         if (leader && elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            int sa = 0;
-            uint32_t pa = 0;
-            unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            const long long tm0 = clock64();
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
             uint32_t slot_seq = 0;
             const uint32_t idesc2 = make_idesc(kKind, 128 * kCG, 128, 0, kMode == 1 ? 1 : 0);
@@ -429,20 +362,18 @@ __global__ void __launch_bounds__(384, 1)
                     const int c_lo = C::kSinglePassG1 ? 0 : pass, c_hi = C::kSinglePassG1 ? nch : pass + 1;
                     if (c_hi > 1 && c_lo <= 1) {  // chunk 1 overlays both GEMM2 slots
                         for (int u = 0; u < 2; ++u, ++slot_seq)
-                            SKL_TIMED(2, mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1));
+                            mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1);
                         tc_fence_after();
                     }
                     for (int kb = 0; kb < nkb1; ++kb) {
-                        if constexpr (C::kSplit) SKL_TIMED(0, mbar_wait(&fullA[sa], pa));
-                        SKL_TIMED(0, mbar_wait(&full[stage], phase));
+                        mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint32_t w_addr = smem_u32(smem + stage * C::kStageMain);
-                        const uint32_t a_addr = C::kSplit ? smem_u32(ringA + sa * C::kStageA) : w_addr;
+                        const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int c = c_lo; c < c_hi; ++c) {
-                            const int wc = min(256, args.R_pad - 256 * c);
+                            const int wc = min(256, r_loc - 256 * c);
                             const uint32_t idesc1 = make_idesc(kKind, 128 * kCG, wc, 0, kMode == 1 ? 1 : 0);
                             const uint32_t d = tmem_base + 256 * c + hoff;
-                            const uint32_t b_addr = w_addr + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
+                            const uint32_t b_addr = a_addr + C::kAOff + (c - c_lo) * (256 / kCG) * 128;
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
                                 mma_ss<kCG, kKind>(d, make_sdesc(a_addr + k * 32, 0, 1024),
@@ -450,31 +381,26 @@ __global__ void __launch_bounds__(384, 1)
                                                           : make_sdesc(b_addr + k * 32, 0, 1024),
                                                idesc1, (kb > 0 || k > 0) ? 1u : 0u);
                         }
-                        mma_commit<kCG>(&empty[stage]);
+                        commit(&empty[stage]);
                         next();
-                        if constexpr (C::kSplit) {
-                            mma_commit<kCG>(&emptyA[sa]);
-                            if (++sa == C::kStagesA) { sa = 0; pa ^= 1; }
-                        }
                     }
-                    for (int c = c_lo; c < c_hi; ++c) mma_commit<kCG>(&tfull1[pp ? r : c]);
+                    for (int c = c_lo; c < c_hi; ++c) commit(&tfull1[pp ? r : c]);
                 }
             };
             auto issue_g2 = [&](uint32_t hoff) {
                 // ---- GEMM2: 128-wide output tiles, A = H from TMEM
                 for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                     const uint32_t s = slot_seq & 1;
-                    SKL_TIMED(2, mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1));
+                    mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1);
                     tc_fence_after();
                     const uint32_t d = tmem_base + 256 + 128 * s;
                     for (int st2 = 0; st2 < nst2; ++st2) {
                         const int kb0 = st2 * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
-                        SKL_TIMED(1, mbar_wait(&full[stage], phase));
+                        mbar_wait(&full[stage], phase);
                         tc_fence_after();
-                        const uint32_t b_addr = smem_u32(smem + stage * C::kStageMain);
+                        const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int q = 0; q < nk; ++q) {
-                            if (args.dbg & 4) break;  // perf bisection: skip GEMM2 MMAs
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const uint32_t a_t = tmem_base + hoff + (uint32_t)((kb0 + q) * 32 + k * 8);
@@ -484,10 +410,10 @@ __global__ void __launch_bounds__(384, 1)
                                 mma_ts<kCG, kKind>(d, a_t, bdesc, idesc2, (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
                             }
                         }
-                        mma_commit<kCG>(&empty[stage]);
+                        commit(&empty[stage]);
                         next();
                     }
-                    mma_commit<kCG>(&tfull2[s]);
+                    commit(&tfull2[s]);
                 }
             };
             if (pp && cluster_id < num_tiles) issue_g1(0, 0);
@@ -495,14 +421,10 @@ __global__ void __launch_bounds__(384, 1)
                 if (!pp) issue_g1(0, 0);
                 else if (t + num_clusters < num_tiles) issue_g1(128u * ((it + 1) & 1), (it + 1) & 1);
                 // ---- wait for the bf16 H of this tile (both CTAs)
-                if (pp) SKL_TIMED(3, mbar_wait(&hready[it & 1], (it >> 1) & 1));
-                else for (int c = 0; c < nch; ++c) SKL_TIMED(3, mbar_wait(&hready[c], it & 1));
+                if (pp) mbar_wait(&hready[it & 1], (it >> 1) & 1);
+                else for (int c = 0; c < nch; ++c) mbar_wait(&hready[c], it & 1);
                 tc_fence_after();
                 issue_g2(pp ? 128u * (it & 1) : 0u);
-            }
-            if (args.dbg & 32) {
-                prof[4] = (unsigned long long)(clock64() - tm0);
-                for (int i = 0; i < 5; ++i) g_b2b_prof[blockIdx.x][i] = prof[i];
             }
         }
     } else if (warp >= 4) {
@@ -518,6 +440,7 @@ __global__ void __launch_bounds__(384, 1)
         const uint32_t srow = q * 32 + lane;  // TMEM lane == tile row
         uint32_t slot_seq = 0;
         uint32_t tf_par0 = 0, tf_par1 = 0;
+        uint32_t xch = 0;                     // kRS: partial hand-offs of this group so far
         const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
         uint8_t* buf = stage_out + wg * C::kOutBytes;  // this group's output staging buffer
         uint8_t* mbuf = mask_s + wg * C::kOutBytes;    // kMask: this group's mask tile (same layout as buf)
@@ -534,8 +457,6 @@ __global__ void __launch_bounds__(384, 1)
             if constexpr (kKind == 1) tma_load_2d<1>(&tmM, &mfull[wg], mbuf + 16384, mn0 + 32, mr0);
         };
         float* bias_g = bias_s + wg * 128;            // [2 slots][64]
-        unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SKL_B2B_DEBUG & 32
-        const long long te0 = clock64();
         auto load_bias_col = [&](int col) -> float {
             if (args.bias == nullptr || col >= args.N2) return 0.f;
             return args.bias_bf16 ? __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(args.bias)[col])
@@ -553,7 +474,7 @@ __global__ void __launch_bounds__(384, 1)
         const float alpha = args.alpha;
         auto arrive_leader = [&](uint64_t* bar) {
             if (leader) mbar_arrive(bar);
-            else mbar_arrive_cluster(bar, 0);
+            else mbar_arrive_cluster(bar, lead);
         };
         // The backward's single-pass GEMM1 finishes both H chunks at once, so the
         // MMA idles while they convert: there the saved columns (P_S2) are written
@@ -571,7 +492,8 @@ __global__ void __launch_bounds__(384, 1)
         // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
         // The warp's [32 tokens x 16 cols] block is transposed through a 1 KB smem
         // scratch so every lane writes two 16-B chunks (8 tokens of one column)
-        // instead of 16 scattered 2-B stores (8 % of the kernel).
+        // instead of 16 scattered 2-B stores (8 % of the kernel).  `col` is the
+        // global rank index (r_off + the pair-local column).
         auto save_cols16 = [&](const uint32_t (&p)[8], int col) {
             const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
             __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(buf + q * 1024);  // [16 cols][32 tokens]
@@ -591,6 +513,39 @@ __global__ void __launch_bounds__(384, 1)
             }
             __syncwarp();
         };
+        // kRS: add the running partial of the previous pair (if any) to this
+        // group's 32 accumulator columns `r`, then pass the sum to the next pair
+        // (if any).  Partials move fp32 through one [128 rows][32] slot per
+        // group, 16-B chunk j of row srow at j ^ (srow & 7): each thread reads
+        // back exactly the row the same-index thread of the previous pair wrote.
+        auto chain_reduce = [&](uint32_t (&r)[32]) {
+            const uint32_t slot = smem_u32(recv_s) + wg * 16384 + srow * 128;
+            if (sp > 0) {
+                mbar_wait_cluster(&rfull[wg], xch & 1);
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    uint32_t v[4];
+                    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                                 : "r"(slot + ((uint32_t)(jj ^ (srow & 7)) << 4)));
+#pragma unroll
+                    for (int i = 0; i < 4; ++i)  // (D_0 + ... + D_{sp-1}) + D_sp
+                        r[4 * jj + i] = __float_as_uint(__uint_as_float(v[i]) + __uint_as_float(r[4 * jj + i]));
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote_release(&sfree[wg], crank - 2);  // slot consumed
+            }
+            if (sp + 1 < nsplit) {
+                mbar_wait_cluster(&sfree[wg], (xch & 1) ^ 1);  // the next pair's slot is free
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj)
+                    st_dsmem_v4(slot + ((uint32_t)(jj ^ (srow & 7)) << 4), crank + 2, r[4 * jj], r[4 * jj + 1],
+                                r[4 * jj + 2], r[4 * jj + 3]);
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote_release(&rfull[wg], crank + 2);
+            }
+            ++xch;
+        };
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             cur_t = t;
@@ -606,7 +561,7 @@ __global__ void __launch_bounds__(384, 1)
             if (use_bits_in) mbits_next = load_bits(0);
             // ---- convert GEMM1 chunks: fp32 -> bf16 H in TMEM (+ saved columns)
             for (int c = 0; c < nch; ++c) {
-                const int wc = min(256, args.R_pad - 256 * c);
+                const int wc = min(256, r_loc - 256 * c);
                 // In-place fp32 -> bf16 compaction, split over both warpgroups in
                 // two rounds of quarter-chunks (W = wc/4 columns each).  Quarter qi
                 // lands in fp32 columns [qi*W/2, (qi+1)*W/2), i.e. inside quarters
@@ -615,9 +570,8 @@ __global__ void __launch_bounds__(384, 1)
                 const int W = wc / 4;
                 const int hb = pp ? (int)(it & 1) : c;            // tfull1 / hready index
                 const uint32_t hoff = pp ? 128u * (it & 1) : 0u;  // TMEM column of this tile's H
-                SKL_TIMED(4, mbar_wait(&tfull1[hb], pp ? ((it >> 1) & 1) : (it & 1)));
+                mbar_wait(&tfull1[hb], pp ? ((it >> 1) & 1) : (it & 1));
                 tc_fence_after();
-                const long long tc0 = clock64();
                 if constexpr (kKind == 1) {
                     // TF32: H stays one fp32 word per column; round in place with
                     // cvt.rna, group wg owns columns [wg*wc/2, (wg+1)*wc/2).
@@ -633,7 +587,7 @@ __global__ void __launch_bounds__(384, 1)
                         for (int i = 0; i < 8; ++i) { lo[i] = r[i]; hi[i] = r[8 + i]; }
                         tmem_st8(tmem_base + lane_base + hoff + 256 * c + cl, lo);
                         tmem_st8(tmem_base + lane_base + hoff + 256 * c + cl + 8, hi);
-                        const int col = 256 * c + cl;
+                        const int col = r_off + 256 * c + cl;
                         if (args.save && row_ok && col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols) {
                             float* dst = reinterpret_cast<float*>(args.save) + row;
 #pragma unroll
@@ -670,7 +624,7 @@ __global__ void __launch_bounds__(384, 1)
                             p[i] = pack_bf16x2(__uint_as_float(r[2 * i]), __uint_as_float(r[2 * i + 1]));
                         const int cl = qi * W + 16 * g;  // chunk-local fp32 column
                         tmem_st8(tmem_base + lane_base + hoff + 128 * c + cl / 2, p);
-                        const int col = 256 * c + cl;  // H column (R order)
+                        const int col = r_off + 256 * c + cl;  // H column (global R order)
                         if (args.save && !defer_save && col + 16 > args.save_col0 &&
                             col < args.save_col0 + args.save_cols)
                             save_cols16(p, col);
@@ -678,7 +632,6 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 }  // bf16 conversion
                 tmem_st_wait();
-                if (args.dbg & 32) prof[6] += (unsigned long long)(clock64() - tc0);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
@@ -694,13 +647,13 @@ __global__ void __launch_bounds__(384, 1)
                 if (issuer) bulk_wait_read<0>();  // buf is the transpose scratch
                 named_bar_sync(1 + wg, 128);
                 for (int c = 0; c < nch; ++c) {
-                    const int W = min(256, args.R_pad - 256 * c) / 4;
+                    const int W = min(256, r_loc - 256 * c) / 4;
 #pragma unroll 1
                     for (int rd = 0; rd < 2; ++rd) {
                         const int qi = 2 * rd + (int)wg;
 #pragma unroll 1
                         for (int g = 0; g < 4 && 16 * g < W; ++g) {
-                            const int cl = qi * W + 16 * g, col = 256 * c + cl;
+                            const int cl = qi * W + 16 * g, col = r_off + 256 * c + cl;
                             if (!(col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols)) continue;
                             uint32_t p[8];
                             tmem_ld8(tmem_base + lane_base + (pp ? 128u * (it & 1) : 0u) + 128 * c + cl / 2, p);
@@ -722,38 +675,35 @@ __global__ void __launch_bounds__(384, 1)
                 }
                 // tfull2[s] completes once per GEMM2 job on slot s (chunk-1
                 // acquisitions never commit it), so count its phases per slot.
-                SKL_TIMED(0, mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0));
+                mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
                 if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
                 tc_fence_after();
                 if (!C::kBiasTab && srow < 64) bias_g[s * 64 + srow] = bval;  // published by the barrier below
-                if (args.dbg & 1) {  // perf bisection: release the slot without reading it
-                    tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) arrive_leader(&tempty2[s]);
-                    continue;
-                }
                 uint32_t ra[32], rb[32];
-                const long long tl0 = clock64();
                 tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg, ra);
                 tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg + 32, rb);
                 tmem_ld_wait();
-                if (args.dbg & 32) prof[7] += (unsigned long long)(clock64() - tl0);
                 // every TMEM read of this slot by this warp has completed
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) arrive_leader(&tempty2[s]);
-                if (args.dbg & 16) continue;  // perf bisection: TMEM reads only
+                if constexpr (kRS) {
+                    if (nsplit > 1) {
+                        chain_reduce(ra);
+                        chain_reduce(rb);
+                        if (sp + 1 < nsplit) continue;  // only the last pair of the chain writes the tile
+                    }
+                }
                 const int n0 = j * 128 + 64 * (int)wg;
                 if (use_bits_in) {  // this tile's bits were loaded one tile ago; fetch the next tile's
                     mbits = mbits_next;
                     if (j + 1 < n2_tiles) mbits_next = load_bits(j + 1);
                 }
                 uint32_t bo0 = 0u, bo1 = 0u;  // use_bits_out: this row's bits of the group's 64 columns
-                if (issuer) SKL_TIMED(2, bulk_wait_read<0>());  // our previous store has read `buf`
-                SKL_TIMED(3, named_bar_sync(1 + wg, 128));
+                if (issuer) bulk_wait_read<0>();  // our previous store has read `buf`
+                named_bar_sync(1 + wg, 128);
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
                 const uint32_t mrow_addr = smem_u32(mbuf) + srow * 128;
-                const long long tm0 = clock64();
                 if (use_mask) {
                     mbar_wait(&mfull[wg], mph);
                     mph ^= 1u;
@@ -867,9 +817,8 @@ __global__ void __launch_bounds__(384, 1)
                     *reinterpret_cast<uint2*>(args.relu_bits + (long long)row * args.bits_ld + n0 / 32) =
                         make_uint2(bo0, bo1);
                 fence_proxy_async_smem();
-                if (args.dbg & 32) prof[1] += (unsigned long long)(clock64() - tm0);
                 named_bar_sync(1 + wg, 128);
-                if (issuer && !(args.dbg & 8)) {
+                if (issuer) {
                     tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
                     bulk_commit();
                 }
@@ -877,11 +826,6 @@ __global__ void __launch_bounds__(384, 1)
             }
         }
         if (issuer) bulk_wait<0>();
-        if ((args.dbg & 64) && issuer && wg == 0) g_b2b_ts[blockIdx.x][2] = gtimer();
-        if ((args.dbg & 32) && issuer && wg == 0) {
-            prof[5] = (unsigned long long)(clock64() - te0);
-            for (int i = 0; i < 8; ++i) g_b2b_eprof[blockIdx.x][i] = prof[i];
-        }
     }
 
     tc_fence_before();
@@ -890,14 +834,18 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<kCG>(tmem_base, 512);
     }
-    if ((args.dbg & 64) && threadIdx.x == 0) g_b2b_ts[blockIdx.x][3] = gtimer();
 }
 
 }  // namespace dev
 
 // Host side (skl.cu): whether the fused path handles this rank / dtype.
-// bf16: H compacts to R/2 TMEM columns, R <= 512.  TF32: H keeps one column
-// per rank index next to the two 128-column GEMM2 slots, R <= 256.
-inline bool b2b_supported(long long R_pad, int kind) { return kind == 0 ? R_pad <= 512 : R_pad <= 256; }
+// bf16: H compacts to R/2 TMEM columns, R <= 512 per CTA pair, and the R-split
+// cluster (kRS) of up to 4 pairs takes R <= 2048.  TF32: H keeps one column per
+// rank index next to the two 128-column GEMM2 slots, R <= 256.
+constexpr int kMaxSplit = 4;
+inline int b2b_split(long long R_pad) { return (int)((R_pad + 511) / 512); }  // pairs per cluster
+inline bool b2b_supported(long long R_pad, int kind) {
+    return kind == 0 ? b2b_split(R_pad) <= kMaxSplit : R_pad <= 256;
+}
 
 }  // namespace skl

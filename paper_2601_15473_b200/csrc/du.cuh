@@ -54,9 +54,7 @@ struct DuArgs {
     int* tickets;    // [num_tiles], zero on entry, left zero on exit
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
-    int dbg;         // SKL_DU_DEBUG=1: per-CTA cycle accounting into g_du_prof (perf analysis)
     int l2hint;      // L2 cache-hint policy bits for the operand loads (see the producer)
-    int early;       // 1: dU1 units skip the PDL wait (see du_kernel); needs cr and a dU2 problem in p[1]
     int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); each CTA
                      // bulk-stores its partial, the cluster barrier publishes it, each CTA bulk-loads its slice
 };
@@ -79,15 +77,6 @@ struct DuKind {
     static constexpr int kUK = kKind == 0 ? 16 : 8;  // K per MMA instruction
 };
 
-// Per-CTA cycle accounting (DuArgs::dbg): [0] producer waits on empty stages,
-// [1] producer total, [2] MMA waits on full stages, [3] MMA total, [4] epilogue
-// colsum phase, [5] epilogue waits on the accumulator, [6] partial write,
-// [7] reduction (ticket wait + sum).
-__device__ unsigned long long g_du_prof[296][8];
-__device__ unsigned long long g_du_ts[296][12];
-__device__ unsigned long long g_du_wend[296][16];  // SKL_DU_DEBUG&2: per-warp reduce-loop end / kernel end  // SKL_DU_DEBUG&2: globaltimer at entry / exit / prologue done / reduce start
-__device__ unsigned long long g_du_wait[296][4];  // [cta]: fence+ticket wait, +fence, +sum, +colsum/release
-
 // Cluster-reduce tail parameters, precomputed at kernel start into shared memory:
 // the tail runs once per CTA with a cold instruction cache (ncu: stall_no_inst),
 // so it is kept short and free of the unit decode.
@@ -108,7 +97,6 @@ __global__ void __launch_bounds__(256, 1)
     du_kernel(const __grid_constant__ CUtensorMap tmA0, const __grid_constant__ CUtensorMap tmB0,
               const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1, DuArgs args) {
     using KT = DuKind<kKind>;
-    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][0] = gtimer();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -157,19 +145,8 @@ __global__ void __launch_bounds__(256, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    // early (cluster-reduce launches right after this backward's dX kernel): dU1
-    // units read only Savedᵀ and G, produced before that kernel, so they start on
-    // the SMs its last wave leaves idle.  They do not trigger dependents; the
-    // dU2 units wait, then trigger, which keeps the chain invariant above.
-    const bool early_cta = args.early && args.cr && (int)(blockIdx.x >> 1) < args.p[1].unit0;
-    if (!early_cta) {
-        pdl_wait();
-        pdl_launch_dependents();
-    }
-    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) {
-        g_du_ts[blockIdx.x][2] = gtimer();
-        g_du_ts[blockIdx.x][4] = (unsigned long long)clock64();
-    }
+    pdl_wait();
+    pdl_launch_dependents();
 
     const int units = args.num_units;
     const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
@@ -230,8 +207,6 @@ __global__ void __launch_bounds__(256, 1)
         if (elect_one()) {
             int stage = 0;
             uint32_t phase = 0;
-            unsigned long long w_empty = 0;
-            const long long t_beg = clock64();
             // A (Savedᵀ / P_S2ᵀ) is re-read by every N tile of the same split; B (G / X) once
             // (DuArgs::l2hint bit 0: A evict_last, bit 1: B evict_first; 0 = the default policy)
             const uint64_t pol_norm = l2_evict_normal();
@@ -243,13 +218,7 @@ __global__ void __launch_bounds__(256, 1)
                 const CUtensorMap* mb = x.p ? &tmB1 : &tmB0;
                 const int m0 = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256 + (int)rank * 128;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                    if (args.dbg) {
-                        const long long t0 = clock64();
-                        mbar_wait(&empty[stage], phase ^ 1);
-                        w_empty += (unsigned long long)(clock64() - t0);
-                    } else {
-                        mbar_wait(&empty[stage], phase ^ 1);
-                    }
+                    mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
                     const int k0 = kb * KT::kBK;
@@ -272,10 +241,6 @@ __global__ void __launch_bounds__(256, 1)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
             }
-            if (args.dbg && blockIdx.x < 296) {
-                g_du_prof[blockIdx.x][0] = w_empty;
-                g_du_prof[blockIdx.x][1] = (unsigned long long)(clock64() - t_beg);
-            }
         }
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (leader)
@@ -284,8 +249,6 @@ __global__ void __launch_bounds__(256, 1)
             int stage = 0;
             uint32_t phase = 0;
             int iter = 0;
-            unsigned long long w_full = 0;
-            const long long t_beg = clock64();
             for (int u = pair; u < units; u += npairs, ++iter) {
                 const Unit x = decode(u);
                 const int acc = iter & 1;
@@ -293,13 +256,7 @@ __global__ void __launch_bounds__(256, 1)
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kDuBN;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
-                    if (args.dbg) {
-                        const long long t0 = clock64();
-                        mbar_wait(&full[stage], phase);
-                        w_full += (unsigned long long)(clock64() - t0);
-                    } else {
-                        mbar_wait(&full[stage], phase);
-                    }
+                    mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * kDuABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
@@ -315,10 +272,6 @@ __global__ void __launch_bounds__(256, 1)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
                 }
                 mma_commit_pair(&tfull[acc], pair_mask);
-            }
-            if (args.dbg && blockIdx.x < 296) {
-                g_du_prof[blockIdx.x][2] = w_full;
-                g_du_prof[blockIdx.x][3] = (unsigned long long)(clock64() - t_beg);
             }
         }
     } else if (warp == 3) {
@@ -343,20 +296,10 @@ __global__ void __launch_bounds__(256, 1)
         uint32_t phase = 0;
         uint32_t red_phase = 0;
         int iter = 0;
-        unsigned long long e_cs = 0, e_acc = 0, e_part = 0, e_red = 0;
-        long long e_t = clock64();
-        auto lap = [&](unsigned long long& slot) {
-            if (args.dbg) {
-                const long long now = clock64();
-                slot += (unsigned long long)(now - e_t);
-                e_t = now;
-            }
-        };
         for (int u = pair; u < units; u += npairs, ++iter) {
             const Unit x = decode(u);
             const DuProblem& P = args.p[x.p];
             const int m0 = x.mt * 256, n0 = x.nt * 256;
-            lap(e_red);
             if (x.colsum) {
                 // ---- column sums of this CTA's 128 staged G columns: thread ->
                 // one 16-B chunk (kCPC columns) of one kW-column block, 8 token rows.
@@ -411,13 +354,10 @@ __global__ void __launch_bounds__(256, 1)
                 for (int kb = x.kb0; kb < x.kb1; ++kb)
                     if (++stage == kDuStages) { stage = 0; phase ^= 1; }
             }
-            lap(e_cs);
             // ---- accumulator -> fp32 partial [tile][split][256][256], our 128 rows
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
             tc_fence_after();
-            if ((args.dbg & 2) && t == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][9] = gtimer();
-            lap(e_acc);
             if (args.cr) {
                 // accumulator -> this CTA's smem (the operand ring is idle now); the
                 // cluster sums it with its peers' after the kernel-wide cluster barrier
@@ -466,7 +406,6 @@ __global__ void __launch_bounds__(256, 1)
                 else mbar_arrive_cluster(&tempty[acc], lead_cta);
             }
 
-            lap(e_part);
             // ---- deterministic split reduction (sum in split order 0..S-1)
             __threadfence();
             named_bar_sync(2, 128);
@@ -485,7 +424,6 @@ __global__ void __launch_bounds__(256, 1)
                     }
                 }
                 named_bar_sync(2, 128);
-                if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][0] = (unsigned long long)(clock64() - e_t);
                 const int z = 2 * x.split + (int)rank;
                 row_lo = z * 256 / parts;
                 row_hi = (z + 1) * 256 / parts;
@@ -500,7 +438,6 @@ __global__ void __launch_bounds__(256, 1)
                 col_lo = 0; col_hi = last ? kDuBN : 0;
             }
             __threadfence();
-            if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][1] = (unsigned long long)(clock64() - e_t);
             const float* pbase = args.part + (long long)x.slot * 256 * kDuBN;
             const bool vec = P.ns == 1 && (P.ms & 3) == 0 && (P.mbs & 3) == 0 &&
                              (reinterpret_cast<uintptr_t>(P.out) & 15) == 0;
@@ -579,7 +516,6 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
             }
-            if (args.dbg && t == 0 && blockIdx.x < 296) g_du_wait[blockIdx.x][2] = (unsigned long long)(clock64() - e_t);
             if (x.colsum) {
                 for (int c = col_lo + t; c < col_hi; c += 128) {
                     const int n = n0 + c;
@@ -600,13 +536,6 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
         }
-        lap(e_red);
-        if (args.dbg && warp == 4 && lane == 0 && blockIdx.x < 296) {
-            g_du_prof[blockIdx.x][4] = e_cs;
-            g_du_prof[blockIdx.x][5] = e_acc;
-            g_du_prof[blockIdx.x][6] = e_part;
-            g_du_prof[blockIdx.x][7] = e_red;
-        }
     }
     if (args.cr && pair < units) {
         // ---- cluster reduction.  Every CTA bulk-stores its (chunk-swizzled) smem
@@ -617,7 +546,6 @@ __global__ void __launch_bounds__(256, 1)
         // 0..S-1.  Few, large copies: per-copy TMA overhead and the cold tail code
         // (ncu: stall_no_inst) are what this phase costs.
         __syncthreads();
-        if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][10] = gtimer();
         if (threadIdx.x == 0) {
             fence_proxy_async_smem();  // the dump was written by generic stores
             if (tail->valid > 0)
@@ -626,15 +554,9 @@ __global__ void __launch_bounds__(256, 1)
             bulk_commit();
             bulk_wait<0>();
             __threadfence();
-            if ((args.dbg & 2) && blockIdx.x < 296) g_du_ts[blockIdx.x][11] = gtimer();
         }
         tc_fence_before();
         cluster_sync();
-        const bool ts = (args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296;
-        if (ts) {
-            g_du_ts[blockIdx.x][3] = gtimer();
-            g_du_ts[blockIdx.x][5] = (unsigned long long)clock64();
-        }
         const DuTail d = *tail;  // registers: the output stores must not force reloads
         const int S = d.S, rows = max(0, min(d.rows, d.valid - d.r0));  // slice rows inside M
         float* cs = cr_part + 136 * kDuBN;  // past S * ceil(128 / S) <= 135 slice rows (S <= 8)
@@ -648,9 +570,7 @@ __global__ void __launch_bounds__(256, 1)
                 if (d.colsum) bulk_load_1d(cs + q2 * 128, d.c0 + q2 * kDuBN, 512, rbar);
             }
         }
-        if (ts) g_du_ts[blockIdx.x][6] = gtimer();
         mbar_wait(rbar, 0);
-        if (ts) g_du_ts[blockIdx.x][7] = gtimer();
         // element (slice row r, column c) of split q2: row q2 * rows + r, chunk (c/4) ^ ((r0 + r) & 7)
         if (d.ns == 1) {
             // row-contiguous output (dU1): lanes over 4-column chunks, float4 stores
@@ -718,9 +638,6 @@ __global__ void __launch_bounds__(256, 1)
                 d.db[n] = sum;
             }
         }
-        if (ts) g_du_ts[blockIdx.x][8] = gtimer();
-        if ((args.dbg & 2) && lane == 0 && blockIdx.x < 296) g_du_wend[blockIdx.x][warp] = gtimer();
-        if (ts) g_du_ts[blockIdx.x][4] = (unsigned long long)clock64() - g_du_ts[blockIdx.x][5];
     } else {
         tc_fence_before();
         cluster_sync();  // the pair's MMAs into this CTA's TMEM are done before it is freed
@@ -729,8 +646,6 @@ __global__ void __launch_bounds__(256, 1)
         tc_fence_after();
         tmem_dealloc<2>(tmem_base, 512);
     }
-    if ((args.dbg & 2) && lane == 0 && blockIdx.x < 296) g_du_wend[blockIdx.x][8 + warp] = gtimer();
-    if ((args.dbg & 2) && threadIdx.x == 0 && blockIdx.x < 296) g_du_ts[blockIdx.x][1] = gtimer();
 }
 
 }  // namespace dev

@@ -219,9 +219,9 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode, int kKind, int kPost = 0>
+template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1>;
+    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS>;
     constexpr int eb = C::kElem, bk = C::kBK;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
@@ -234,12 +234,8 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
         SKL_TRY(make_tmap(&tb1, src.b1, 2, a.k, srows, a.k, 64, 64));
         SKL_TRY(make_tmap(&tb1b, src.b1b, 2, a.k, srows, a.k, 64, 64));
-        const int tall = 64 * C::kKbPerStage2;
-        // Measured slower than per-k-block boxes for the c2 forward; opt-in only.
-        static const bool tall_on = getenv("SKL_B2B_TALL") && atoi(getenv("SKL_B2B_TALL")) != 0;
-        a.b2tall = (tall_on && kCG == 2 && a.Lk % tall == 0 && a.R_pad % tall == 0 && tall <= 256) ? 1 : 0;
-        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.N2, a.Lk, a.N2, 64, a.b2tall ? tall : 64));
-        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.N2, a.Lk, a.N2, 64, a.b2tall ? tall : 64));
+        SKL_TRY(make_tmap(&tb2, src.b2, 2, a.N2, a.Lk, a.N2, 64, 64));
+        SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.N2, a.Lk, a.N2, 64, 64));
     } else {
         const int64_t srows = (int64_t)(a.Lk / a.k) * a.dS;
         SKL_TRY(make_tmap(&tb1, src.b1, 2, a.K1, a.Lk, a.K1, 64, a.b1rows));
@@ -251,26 +247,30 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     tm = ty;
     if (C::kMaskStage && a.mask) SKL_TRY(make_tmap(&tm, a.mask, eb, a.N2, a.T, a.ld_mask, bk, 128));  // output-tile boxes
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
-    static const int grid_cap = [] {  // SKL_B2B_GRID: cap on CTAs (experiments)
-        const char* e = getenv("SKL_B2B_GRID");
-        return e ? atoi(e) : 0;
-    }();
-    if (grid_cap > 0) sms = std::min(sms, grid_cap);
-    int grid = std::max(1, std::min(sms / kCG, tiles)) * kCG;
-    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost>;
+    const int csize = kCG * (kRS ? a.nsplit : 1);  // CTAs per cluster
+    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS>;
     static std::atomic<uint64_t> attr_done{0};
-    SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done));
+    SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done, /*clusters of 8 for 4 R-split pairs*/ kRS));
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(384);  // 4 control warps + 2 epilogue warpgroups
     cfg.dynamicSmemBytes = C::kSmem;
     cfg.stream = st;
     cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = kCG;
+    attr[0].val.clusterDim.x = csize;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
+    int clusters = std::max(1, std::min(sms / csize, tiles));
+    if (kRS) {  // clusters of 2*nsplit CTAs must each fit one GPC: persistent grid = what is co-resident
+        cfg.gridDim = dim3(clusters * csize);
+        cfg.numAttrs = 1;
+        int maxc = 0;
+        if (cudaOccupancyMaxActiveClusters(&maxc, kern, &cfg) == cudaSuccess && maxc > 0)
+            clusters = std::min(clusters, maxc);
+        (void)cudaGetLastError();
+    }
+    cfg.gridDim = dim3(clusters * csize);
     unsigned nattr = 1;
     add_pdl(attr, nattr);
     cfg.numAttrs = nattr;
@@ -317,27 +317,34 @@ int g_b2b_direct = 1;   // read the ABI stacks directly when k % 64 == 0 (SKL_B2
 
 skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     if (kind != 0 && mode != 0) return fail(SKL_ERR_UNSUPPORTED, "the TF32 fused kernel streams packed panels");
-    static const int dbg = [] {
-        const char* e = getenv("SKL_B2B_DEBUG");
-        return e ? atoi(e) : 0;
-    }();
-    a.dbg = dbg;
     // L2 hints: weight panels evict_last (every tile re-reads them); the streamed
     // activation evict_first only when it is far larger than L2 (126 MB) -- a
     // smaller one (c2's G, 201 MB) is partly still in L2 when du re-reads it.
     static const int l2hint = getenv("SKL_B2B_L2HINT") ? atoi(getenv("SKL_B2B_L2HINT")) : -1;
     const double act_bytes = (double)a.T * a.K1 * (kind == 0 ? 2 : 4);
     a.l2hint = l2hint >= 0 ? l2hint : (2 | (act_bytes > 256e6 ? 1 : 0));
-    {  // B1 box rows: largest power of two <= 128 dividing every chunk's per-CTA rows (and Lk in mode 2)
+    // R-split: R > 512 (bf16) runs on clusters of b2b_split(R) CTA pairs, r_loc rank columns each
+    const int split = kind == 0 ? b2b_split(a.R_pad) : 1;
+    a.nsplit = split;
+    a.r_loc = split > 1 ? (a.R_pad / split + 63) / 64 * 64 : a.R_pad;
+    {  // B1 box rows: largest power of two <= 128 dividing every chunk's per-CTA rows (and Lk, r_loc in mode 2)
         const int cg = g_b2b_cg;
         int r = 128;
         auto ok = [&](int v) {
-            for (int c = 0; c * 256 < a.R_pad; ++c)
-                if ((std::min(256, a.R_pad - 256 * c) / cg) % v) return false;
-            return mode != 2 || a.Lk % v == 0;
+            for (int c = 0; c * 256 < a.r_loc; ++c)
+                if ((std::min(256, a.r_loc - 256 * c) / cg) % v) return false;
+            return mode != 2 || (a.Lk % v == 0 && a.r_loc % v == 0);
         };
         while (r > 8 && !ok(r)) r /= 2;
         a.b1rows = r;
+    }
+    if (split > 1) {
+        if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "the R-split kernel needs CTA pairs");
+        if (a.relu || a.mask || a.relu_bits || a.mask_bits)
+            return fail(SKL_ERR_UNSUPPORTED, "fused ReLU with R > 512 runs on the unfused chain");
+        if (mode == 1) return run_b2b_cg<2, 1, 0, 0, true>(name, src, a, sms, st);
+        if (mode == 2) return run_b2b_cg<2, 2, 0, 0, true>(name, src, a, sms, st);
+        return run_b2b_cg<2, 0, 0, 0, true>(name, src, a, sms, st);
     }
     if (kind == 1 && b2b_tf32_wide_supported(a.R_pad)) {
         if (g_b2b_cg != 2) return fail(SKL_ERR_UNSUPPORTED, "the wide-rank TF32 kernel needs CTA pairs");
@@ -454,17 +461,24 @@ bool use_fused(const SklDims& d, skl_dtype t) {
         return e && atoi(e) != 0;
     }();
     static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
+    // SKL_B2B_RSPLIT=0: R > 512 (bf16) on the unfused GEMM chain instead of the R-split clusters
+    static const bool rsplit = !(getenv("SKL_B2B_RSPLIT") && atoi(getenv("SKL_B2B_RSPLIT")) == 0);
     if (force_unfused) return false;
     if (t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad)) return g_b2b_cg == 2;
+    if (t == SKL_BF16 && b2b_split(d.R_pad) > 1) return rsplit && g_b2b_cg == 2 && b2b_supported(d.R_pad, 0);
     return b2b_supported(d.R_pad, t == SKL_BF16 ? 0 : 1);
 }
+
+// R-split clusters (R > 512, bf16) run the plain layer; a fused ReLU / ReLU mask
+// there takes the unfused chain.
+bool rsplit_of(const SklDims& d, skl_dtype t) { return t == SKL_BF16 && b2b_split(d.R_pad) > 1; }
 
 // 1-bit ReLU masks are implemented in the CTA-pair b2b kernel only (not in the
 // wide-rank TF32 kernel or the unfused GEMM chain).
 bool relu_bits_ok(const SklDims& d, skl_dtype t) {
     read_b2b_env();
     static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
-    if (!use_fused(d, t) || g_b2b_cg != 2) return false;
+    if (!use_fused(d, t) || g_b2b_cg != 2 || rsplit_of(d, t)) return false;
     return !(t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad));
 }
 
@@ -586,8 +600,9 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
     p.bcatT = take((size_t)d.d_out * d.R_pad * e);
     p.bias32 = take((size_t)d.d_out * 4);
     const bool fused = use_fused(d, t);
-    // unfused only: H [T, R_pad] (fwd) / P [T, R_pad] (bwd) through HBM
-    p.inter = take(!fused ? (size_t)T * d.R_pad * e : 0);
+    // unfused only: H [T, R_pad] (fwd) / P [T, R_pad] (bwd) through HBM (also kept for
+    // R-split shapes: a fused ReLU there takes the unfused chain)
+    p.inter = take(!fused || rsplit_of(d, t) ? (size_t)T * d.R_pad * e : 0);
     p.saved = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);  // recomputed Savedᵀ when the caller kept none
     p.p2t = take(bwd ? (size_t)d.Lk * t8(T) * e : 0);    // P_S2ᵀ
     if (bwd) {
@@ -710,13 +725,6 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         // neither a cooperative launch nor co-residency of all units is needed
         a.cr = 1;
         a.coop = 0;
-        // which == 3 runs right after this backward's dX / P kernel: dU1 may start early
-        // on the SMs that kernel's last wave leaves idle.  Opt-in (SKL_DU_EARLY=1): only
-        // the clusters that fit there start early and the step time did not move.
-        static const bool early_on = getenv("SKL_DU_EARLY") && atoi(getenv("SKL_DU_EARLY")) != 0;
-        a.early = (early_on && which == 3 && pdl_enabled()) ? 1 : 0;
-        static const int du_dbg_cr = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;
-        a.dbg = du_dbg_cr;  // perf analysis: cycle accounting (bit 0), entry/exit timestamps (bit 1)
         const int S = u.t0 ? u.s0 : u.s1;
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(2 * units);
@@ -736,8 +744,6 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         SKL_CUDA(cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a));
         return SKL_OK;
     }
-    static const int du_dbg = getenv("SKL_DU_DEBUG") ? atoi(getenv("SKL_DU_DEBUG")) : 0;  // perf analysis
-    a.dbg = du_dbg;
     static const bool no_coop = getenv("SKL_DU_NOCOOP") && atoi(getenv("SKL_DU_NOCOOP")) != 0;  // profilers
     // one wave: cooperative launch, slice-parallel reduction; several waves:
     // persistent grid, the last CTA of each tile reduces it
@@ -927,7 +933,7 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
     void* acatT = at<void>(workspace, p.acatT);
     void* bcatT = at<void>(workspace, p.bcatT);
     float* bias32 = at<float>(workspace, p.bias32);
-    const bool fused = use_fused(d, s->dtype);
+    const bool fused = use_fused(d, s->dtype) && !(rsplit_of(d, s->dtype) && (fuse & SKL_FUSE_RELU_OUT));
     const bool direct = fused && direct_ok(d, s->dtype);
     if (!direct) SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, nullptr, nullptr, acatT, bcatT, bias, bias32, st));
 
@@ -1085,7 +1091,7 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
     void* acatT = at<void>(workspace, p.acatT);
     void* P = at<void>(workspace, p.inter);
     void* p2t = at<void>(workspace, p.p2t);
-    const bool fused = use_fused(d, s->dtype);
+    const bool fused = use_fused(d, s->dtype) && !(rsplit_of(d, s->dtype) && (fuse & SKL_FUSE_RELU_IN));
     const bool bwd_direct = fused && grad_x != nullptr && direct_ok(d, s->dtype);
     const bool need_saved = ph_u1 && !saved_proj;
     if ((ph_data && !bwd_direct) || need_saved)
@@ -1654,52 +1660,3 @@ skl_status skl_allreduce_grads(void* nccl_comm, float* grad_bucket, size_t count
 
 }  // extern "C"
 
-// Perf-analysis hook (not part of skl.h): per-CTA cycle counters of the last
-// fused-kernel launch run with SKL_B2B_DEBUG bit 32.
-extern "C" int skl_debug_b2b_prof(unsigned long long* out, int n) {
-    const int total = 296 * 8;
-    if (n > total) n = total;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_prof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-extern "C" int skl_debug_b2b_ts(unsigned long long* out, int n) {
-    if (n > 296 * 4) n = 296 * 4;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_ts, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-extern "C" int skl_debug_du_prof(unsigned long long* out, int n) {
-    const int total = 296 * 8;
-    if (n > total) n = total;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_prof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-extern "C" int skl_debug_du_ts(unsigned long long* out, int n) {
-    if (n > 296 * 12) n = 296 * 12;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_ts, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-
-extern "C" int skl_debug_du_wend(unsigned long long* out, int n) {
-    if (n > 296 * 16) n = 296 * 16;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_wend, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-
-extern "C" int skl_debug_du_wait(unsigned long long* out, int n) {
-    if (n > 296 * 4) n = 296 * 4;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_du_wait, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}
-extern "C" int skl_debug_b2b_eprof(unsigned long long* out, int n) {
-    const int total = 296 * 8;
-    if (n > total) n = total;
-    if (cudaMemcpyFromSymbol(out, skl::dev::g_b2b_eprof, (size_t)n * sizeof(unsigned long long)) != cudaSuccess)
-        return -1;
-    return n;
-}

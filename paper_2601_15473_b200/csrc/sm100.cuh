@@ -81,6 +81,27 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
         "r"(cta)
         : "memory");
 }
+// Arrive with RELEASE at cluster scope on the barrier at `bar`'s offset in CTA
+// `cta`: orders this thread's prior shared::cluster stores / shared loads before
+// the waiter's acquire (mbar_wait_cluster) -- the DSMEM hand-off protocol.
+__device__ __forceinline__ void mbar_arrive_remote_release(uint64_t* bar, uint32_t cta) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(smem_u32(bar)),
+        "r"(cta)
+        : "memory");
+}
+// 16-byte store into CTA `cta`'s shared memory at the offset `addr` (DSMEM).
+__device__ __forceinline__ void st_dsmem_v4(uint32_t addr, uint32_t cta, uint32_t a, uint32_t b, uint32_t c,
+                                            uint32_t d) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "st.shared::cluster.v4.b32 [ra], {%2, %3, %4, %5};\n\t}" ::"r"(addr),
+        "r"(cta), "r"(a), "r"(b), "r"(c), "r"(d)
+        : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %0;" ::"r"(bytes), "r"(smem_u32(bar))
                  : "memory");
@@ -115,6 +136,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
         if (t1 - t0 > 10000000000ull) {
             printf("skl: mbarrier wait timeout block %d thread %d bar %u phase %u\n", blockIdx.x, threadIdx.x,
                    addr, phase);
+            __trap();
+        }
+    }
+}
+
+// mbar_wait with ACQUIRE at cluster scope: the barrier completes on remote
+// arrivals (mbar_arrive_remote_release) whose DSMEM data this thread then reads.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
+    const uint32_t addr = smem_u32(bar);
+    uint64_t t0 = 0;
+    for (int it = 0;; ++it) {
+        uint32_t done = 0;
+        asm volatile(
+            "{\n\t.reg .pred P;\n\t"
+            "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P, [%1], %2, 0x989680;\n\t"
+            "selp.b32 %0, 1, 0, P;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(phase)
+            : "memory");
+        if (done) return;
+        uint64_t t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (it == 0) t0 = t1;
+        else if (t1 - t0 > 10000000000ull) {
+            printf("skl: cluster mbarrier wait timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
             __trap();
         }
     }

@@ -118,6 +118,11 @@ CASES = [
     (1024, 512, 1, 64, 20000),     # R = 128 ping-pong H: > 74 pair tiles, so CTAs alternate TMEM regions
     (4096, 4096, 1, 16, 300),      # c4 L1 k16 shape: R = 32 on d = 4096 (packed panels, 32 GEMM2 tiles)
     (4096, 4096, 4, 64, 257),      # c4 L4 k64 shape: R = 512, ragged T
+    # R > 512: R-split clusters of CTA pairs, partial sums chained over DSMEM
+    (512, 768, 3, 128, 1000),      # R = 768: 2 pairs x 384 (chunks 256 + 128), direct stacks
+    (1024, 1536, 3, 100, 700),     # R = 600 -> 640: 2 pairs x 320, packed panels (k % 64 != 0)
+    (2048, 1024, 4, 256, 2000),    # R = 2048: 4 pairs (cluster of 8 CTAs), several tiles per cluster
+    (4096, 4096, 3, 256, 3000),    # c3 shape: R = 1536, 3 pairs x 512
 ]
 
 
