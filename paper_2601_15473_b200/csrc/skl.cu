@@ -461,8 +461,11 @@ bool use_fused(const SklDims& d, skl_dtype t) {
         return e && atoi(e) != 0;
     }();
     static const bool tf32_wide = !(getenv("SKL_TF32_WIDE") && atoi(getenv("SKL_TF32_WIDE")) == 0);
-    // SKL_B2B_RSPLIT=0: R > 512 (bf16) on the unfused GEMM chain instead of the R-split clusters
-    static const bool rsplit = !(getenv("SKL_B2B_RSPLIT") && atoi(getenv("SKL_B2B_RSPLIT")) == 0);
+    // SKL_B2B_RSPLIT=1: R > 512 (bf16) on the R-split clusters (H on chip, GEMM2 partials
+    // chained over DSMEM) instead of the GEMM chain through HBM.  Opt-in: the fp32 partials
+    // need 64 KB per output tile per CTA against ~21 B/cycle of DSMEM bandwidth, so at c3
+    // (R = 1536) it measures 2.2x slower than the chain (R-split).
+    static const bool rsplit = getenv("SKL_B2B_RSPLIT") && atoi(getenv("SKL_B2B_RSPLIT")) != 0;
     if (force_unfused) return false;
     if (t != SKL_BF16 && tf32_wide && b2b_tf32_wide_supported(d.R_pad)) return g_b2b_cg == 2;
     if (t == SKL_BF16 && b2b_split(d.R_pad) > 1) return rsplit && g_b2b_cg == 2 && b2b_supported(d.R_pad, 0);

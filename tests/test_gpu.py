@@ -645,6 +645,38 @@ def test_unfused_path_parity_in_subprocess():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+def test_rsplit_path_parity_in_subprocess():
+    """The parity tests once more with SKL_B2B_RSPLIT=1: shapes with R > 512 (the
+    R = 768 / 640 / 2048 and c3 R = 1536 cases) run on the R-split clusters (H on
+    chip, GEMM2 partials chained over DSMEM in fixed pair order) against the same
+    oracle gates, and stay bitwise deterministic."""
+    import subprocess
+    import sys
+    if os.environ.get("SKL_B2B_RSPLIT") is not None:
+        pytest.skip("already the R-split process")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKL_B2B_RSPLIT="1")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu.py", "-k",
+                        "parity_bf16 or c3_shape or rsplit_is_deterministic"],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_rsplit_is_deterministic(skl):
+    """R > 512 backward twice: bitwise identical (both the default chain and, in
+    the SKL_B2B_RSPLIT=1 subprocess, the DSMEM partial chain)."""
+    d_in, d_out, L, k, T = 2048, 1024, 4, 256, 1500
+    lyr = skl.SkLinear(d_in, d_out, L, k, seed=5, dtype=skl.BF16)
+    X = torch.randn(T, d_in, device="cuda").to(torch.bfloat16)
+    G = torch.randn(T, d_out, device="cuda").to(torch.bfloat16)
+    y1, y2 = lyr.forward(X), lyr.forward(X)
+    a, b = lyr.backward(X, G), lyr.backward(X, G)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    for u, v in zip((a.grad_x, a.grad_u1, a.grad_u2, a.grad_b), (b.grad_x, b.grad_u1, b.grad_u2, b.grad_b)):
+        assert torch.equal(u, v)
+
+
 def test_graph_replay_is_bitwise_equal(skl):
     """A fixed-shape chain step (forward + backward through SkChain, 2 encoder
     layers of the c5 stack) recorded with graphs.capture replays to bitwise the
