@@ -27,6 +27,7 @@
 #include "b2b.cuh"
 #include "b2b_tf32.cuh"
 #include "du.cuh"
+#include "dut.cuh"
 #include "gemm.cuh"
 #include "prof.h"
 #include "skl_internal.h"
@@ -567,6 +568,34 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     return s;
 }
 
+// Small rank (L·k <= 128): the transposed dU problem (dut.cuh), M = d in
+// 256-row pair chunks grouped kDutGroup per unit, N = L·k padded to 16.
+// SKL_DUT=0 keeps du.cuh for every shape (A/B).
+struct DutShape {
+    int n_pad, g0, g1, splits, units, kb, max_chunks;
+};
+bool use_dut(const SklDims& d) {
+    static const bool on = !(getenv("SKL_DUT") && atoi(getenv("SKL_DUT")) == 0);
+    return on && d.Lk <= 128;
+}
+DutShape dut_shape(const SklDims& d, int64_t T, int sms, int kind, int which) {
+    DutShape s;
+    s.n_pad = (int)((d.Lk + 15) / 16 * 16);
+    const int rows_per_group = 256 * kDutGroup;
+    s.g0 = (which & 1) ? (int)((d.d_out + rows_per_group - 1) / rows_per_group) : 0;
+    s.g1 = (which & 2) ? (int)((d.d_in + rows_per_group - 1) / rows_per_group) : 0;
+    const int bkt = kind == 0 ? 64 : 32;
+    s.kb = (int)std::max<int64_t>(1, (T + bkt - 1) / bkt);
+    const int pairs = std::max(1, sms / 2), groups = std::max(1, s.g0 + s.g1);
+    s.splits = std::max(1, std::min(pairs / groups, s.kb / 4));  // one wave, >= 4 k-blocks per unit
+    s.units = (s.g0 + s.g1) * s.splits;
+    int mc = 0;
+    for (int dim : {(which & 1) ? (int)d.d_out : 0, (which & 2) ? (int)d.d_in : 0})
+        if (dim) mc = std::max(mc, std::min(kDutGroup, (dim + 255) / 256));
+    s.max_chunks = std::max(1, mc);
+    return s;
+}
+
 // du split partials / column-sum partials / tickets, sized for every phase's
 // split choice AND independently of the SM count the call will see
 // (skl_set_reserved_sms may change it after the size query): one-wave searches
@@ -584,6 +613,12 @@ void du_ws_sizes(const SklDims& d, skl_dtype t, int64_t T, int sms, size_t& part
         part = std::max(part, (size_t)u.units * 256 * 256 * 4);
         cpart = std::max(cpart, (size_t)u.n0t * u.s0 * 256 * 4);
         tickets = std::max(tickets, (size_t)u.tiles() * 4);
+    }
+    if (use_dut(d)) {  // dut: units <= max(pairs, groups) for any SM count
+        const DutShape u = dut_shape(d, T, 2 * full_pairs, t == SKL_BF16 ? 0 : 1, 3);
+        const size_t units = (size_t)std::max(full_pairs, u.g0 + u.g1);
+        part = std::max(part, units * 2 * kDutGroup * 128 * u.n_pad * 4);
+        cpart = std::max(cpart, units * 2 * kDutGroup * 128 * 4);
     }
 }
 
@@ -673,12 +708,97 @@ skl_status repad_in(const void* src, int eb, int64_t B, int64_t R, int64_t C, vo
 // dU1s = inv·Savedᵀ·G ([Lk, d_out] == [L][k][d_out]); dU2sᵀ = inv·P_S2ᵀ·X
 // ([Lk, d_in] scattered to [L][d_in][k]); db = column sums of G.  `which`:
 // bit 0 = dU1s (+ db), bit 1 = dU2s; one grouped persistent launch.
+// dut.cuh launch (L·k <= 128): problem 0 = dU1sᵀ (A = G, B = Savedᵀ, + db),
+// problem 1 = dU2s (A = X, B = P_S2ᵀ); a lone dU2 phase sits in slot 0.
+skl_status run_dut(const SklDims& d, int64_t T, int kind, int which, const void* saved, const void* grad_y,
+                   const void* p2t, const void* x, float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
+                   const Plan& p, int sms, cudaStream_t st, float inv) {
+    const int eb = kind == 0 ? 2 : 4;
+    const int64_t ldt = t8(T);
+    const DutShape u = dut_shape(d, T, sms, kind, which);
+    DutArgs a = {};
+    a.N = (int)d.Lk;
+    a.N_pad = u.n_pad;
+    a.k_blocks = u.kb;
+    a.splits = u.splits;
+    a.num_units = u.units;
+    a.alpha = inv;
+    a.b_bytes = (int)align_up((size_t)(u.n_pad / 2) * 128, 1024);
+    a.stage_bytes = a.b_bytes + u.max_chunks * 128 * 128;
+    const int csum_bytes = kDutGroup * 8 * 128 * 4;
+    a.stages = std::min(8, (225 * 1024 - csum_bytes - 2048) / a.stage_bytes);
+    if (a.stages < 2) return fail(SKL_ERR_UNSUPPORTED, "dut: stage does not fit shared memory");
+    const DutProblem pu1{(int)d.d_out, u.g0, 0, grad_bias ? 1 : 0, grad_U1s, (long long)1 << 40, 0,
+                         (long long)d.d_out, 1, grad_bias};
+    const DutProblem pu2{(int)d.d_in, u.g1, u.g0 * u.splits, 0, grad_U2s, (long long)d.k, (long long)(d.d_in * d.k),
+                         1, (long long)d.k, nullptr};
+    DutProblem none{};
+    none.unit0 = 1 << 30;
+    a.p[0] = (which & 1) ? pu1 : pu2;
+    if (!(which & 1)) a.p[0].unit0 = 0;
+    a.p[1] = (which & 1) && (which & 2) ? pu2 : none;
+    a.part = at<float>(workspace, p.du_part);
+    a.cpart = at<float>(workspace, p.du_cpart);
+    const int bkt = 128 / eb;
+    const CUtensorMapSwizzle mn_swz = kind == 0 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    CUtensorMap tu1a, tu1b, tu2a, tu2b;
+    if (which & 1) {
+        SKL_TRY(make_tmap(&tu1a, grad_y, eb, d.d_out, T, d.d_out, bkt, bkt, mn_swz));  // G, MN-major
+        SKL_TRY(make_tmap(&tu1b, saved, eb, T, d.Lk, ldt, bkt, u.n_pad / 2));            // Savedᵀ, K-major
+    }
+    if (which & 2) {
+        SKL_TRY(make_tmap(&tu2a, x, eb, d.d_in, T, d.d_in, bkt, bkt, mn_swz));           // X
+        SKL_TRY(make_tmap(&tu2b, p2t, eb, T, d.Lk, ldt, bkt, u.n_pad / 2));              // P_S2ᵀ
+    }
+    if (!(which & 1)) { tu1a = tu2a; tu1b = tu2b; }
+    if (!(which & 2)) { tu2a = tu1a; tu2b = tu1b; }
+    auto kern = kind == 0 ? dev::dut_kernel<0> : dev::dut_kernel<1>;
+    const int smem = a.stages * a.stage_bytes + 256 + csum_bytes + 1024;
+    static std::atomic<uint64_t> attr_done[2];
+    SKL_TRY(ensure_attrs(kern, 225 * 1024 + 1024, attr_done[kind]));
+    const int pairs = std::max(1, std::min(sms / 2, u.units));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2 * pairs);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    unsigned nattr = 1;
+    add_pdl(attr, nattr);
+    cfg.attrs = attr;
+    cfg.numAttrs = nattr;
+    {
+        ProfScope ps_("dut", st);
+        SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, (which & 1) ? tu1a : tu2a, (which & 1) ? tu1b : tu2b, tu2a, tu2b, a));
+    }
+    cudaLaunchConfig_t rc = {};
+    const int64_t outs = (int64_t)(d.d_out + d.d_in) * d.Lk;
+    rc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(sms * 4, (outs + 255) / 256)));
+    rc.blockDim = dim3(256);
+    rc.stream = st;
+    cudaLaunchAttribute rattr[1];
+    unsigned nr = 0;
+    add_pdl(rattr, nr);
+    rc.attrs = rattr;
+    rc.numAttrs = nr;
+    ProfScope ps2_("dut_reduce", st);
+    SKL_CUDA(cudaLaunchKernelEx(&rc, dev::dut_reduce_kernel, a));
+    return SKL_OK;
+}
+
 skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* saved, const void* grad_y,
                   const void* p2t, const void* x, float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
                   const Plan& p, int sms, cudaStream_t st, float alpha = 0.f) {
     const int eb = kind == 0 ? 2 : 4;
     const int64_t ldt = t8(T);
     const float inv = alpha != 0.f ? alpha : (float)(1.0 / (2.0 * (double)d.L));
+    if (use_dut(d))
+        return run_dut(d, T, kind, which, saved, grad_y, p2t, x, grad_U1s, grad_U2s, grad_bias, workspace, p, sms, st,
+                       inv);
     const DuShape u = du_shape(d, T, sms, kind, which);
     DuArgs a = {};
     a.k_blocks = u.kb;
