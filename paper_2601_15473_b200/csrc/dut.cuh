@@ -301,30 +301,44 @@ __global__ void __launch_bounds__(256, 1)
 // Split reduction of the dut partials: output (problem p, row m, rank column n)
 // = alpha * sum over splits s = 0..S-1 of part[unit(p, g, s)][...] -- in split
 // order, so bitwise reproducible -- scattered into the ABI layout; db likewise
-// from the column-sum partials (unscaled).  Threads run along m when the output
-// is m-contiguous (dU1s: ms == 1), else along n (dU2s: ns == 1).
+// from the column-sum partials (unscaled).  A block pass covers whole partial
+// rows: N_pad/4 threads per row, each reading one float4 per split (coalesced
+// 16-B loads along the row, up to 8 splits in flight before the ordered adds).
 __global__ void __launch_bounds__(256) dut_reduce_kernel(DutArgs args) {
     pdl_wait();
     pdl_launch_dependents();
     const int S = args.splits, Np = args.N_pad;
+    const int tpr = Np / 4;                 // threads per partial row
+    const int rows_per_pass = 256 / tpr;
+    const int tr = (int)threadIdx.x / tpr, n4 = ((int)threadIdx.x % tpr) * 4;
     for (int p = 0; p < 2; ++p) {
         const DutProblem& P = args.p[p];
         if (P.groups == 0) continue;
-        const long long total = (long long)P.M * args.N;
-        const bool along_m = P.ms == 1;
-        for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-             i += (long long)gridDim.x * blockDim.x) {
-            const int m = along_m ? (int)(i % P.M) : (int)(i / args.N);
-            const int n = along_m ? (int)(i / P.M) : (int)(i % args.N);
+        const int passes = (P.M + rows_per_pass - 1) / rows_per_pass;
+        for (int pass = blockIdx.x; pass < passes; pass += gridDim.x) {
+            const int m = pass * rows_per_pass + tr;
+            if (m >= P.M || (int)threadIdx.x >= tpr * rows_per_pass) continue;
             const int g = m / (256 * kDutGroup), mr = m % (256 * kDutGroup);
             const int c = mr / 256, r = (mr % 256) / 128, row = mr % 128;
-            const long long base = ((long long)r * kDutGroup + c) * 128 + row;
-            float acc = 0.f;
-            for (int s = 0; s < S; ++s) {
-                const long long u = P.unit0 + (long long)g * S + s;
-                acc += __ldcg(args.part + ((u * 2 * kDutGroup * 128) + base) * Np + n);
+            const long long rowoff = (((long long)r * kDutGroup + c) * 128 + row) * Np + n4;
+            const long long ustride = 2LL * kDutGroup * 128 * Np;
+            const float* base = args.part + (long long)(P.unit0 + g * S) * ustride + rowoff;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int s0 = 0; s0 < S; s0 += 8) {
+                float4 v[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (s0 + i < S) v[i] = __ldcg(reinterpret_cast<const float4*>(base + (long long)(s0 + i) * ustride));
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+                    if (s0 + i < S) { acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w; }
             }
-            P.out[(n / P.nb) * P.nbs + (n % P.nb) * P.ns + (long long)m * P.ms] = acc * args.alpha;
+            const float o[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int n = n4 + i;
+                if (n < args.N) P.out[(n / P.nb) * P.nbs + (n % P.nb) * P.ns + (long long)m * P.ms] = o[i] * args.alpha;
+            }
         }
         if (P.colsum && P.db) {
             for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < P.M;

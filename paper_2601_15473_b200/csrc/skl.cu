@@ -574,9 +574,14 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
 struct DutShape {
     int n_pad, g0, g1, splits, units, kb, max_chunks;
 };
+// Chosen where the padded du rows cost more than dut's partial round trip:
+// L·k <= 64, or L·k <= 128 on wide layers (measured: c4 L1 k16 / L2 k32 / TF32
+// L2 k64 -10 / -10 / -6.5 % per step; the 768x768 projections (L·k = 128) stay on
+// du, whose partials are a quarter of dut's there).
 bool use_dut(const SklDims& d) {
-    static const bool on = !(getenv("SKL_DUT") && atoi(getenv("SKL_DUT")) == 0);
-    return on && d.Lk <= 128;
+    static const int mode = getenv("SKL_DUT") ? atoi(getenv("SKL_DUT")) : -1;  // 0 off, 1 whenever L*k <= 128
+    if (mode == 0 || d.Lk > 128) return false;
+    return mode == 1 || d.Lk <= 64 || d.d_in + d.d_out >= 4096;
 }
 DutShape dut_shape(const SklDims& d, int64_t T, int sms, int kind, int which) {
     DutShape s;
@@ -777,7 +782,7 @@ skl_status run_dut(const SklDims& d, int64_t T, int kind, int which, const void*
     }
     cudaLaunchConfig_t rc = {};
     const int64_t outs = (int64_t)(d.d_out + d.d_in) * d.Lk;
-    rc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(sms * 4, (outs + 255) / 256)));
+    rc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(sms * 4, (outs * 4 / u.n_pad + 255) / 256)));
     rc.blockDim = dim3(256);
     rc.stream = st;
     cudaLaunchAttribute rattr[1];
