@@ -562,9 +562,22 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     // split partials summed over DSMEM -- needs one S for both problems and a
     // cluster of at most 8 CTAs.  Otherwise partials go through global memory.
     static const bool cr_on = !(getenv("SKL_DU_CR") && atoi(getenv("SKL_DU_CR")) == 0);
-    const int sc = s.t0 ? s.s0 : s.s1;
     static const int cr_max = getenv("SKL_DU_CR_MAX") ? atoi(getenv("SKL_DU_CR_MAX")) : 4;  // 8: clusters of 16
-    s.cr = cr_on && sc <= std::min(cr_max, 8) && (!s.t0 || !s.t1 || s.s0 == s.s1);
+    // Few tiles (the c5 768x768 projections: 6 tiles -> S = 12): the one-wave
+    // split is too deep for a cluster; S = 8 with clusters of 16 CTAs measures the
+    // same kernel time and, with no grid-wide barrier, lets the next kernel's
+    // CTAs start as this one's retire (projection backward 73.5 -> 68.5 us).
+    static const bool deep_cr = !(getenv("SKL_DU_DEEP_CR") && atoi(getenv("SKL_DU_DEEP_CR")) == 0);
+    if (cr_on && deep_cr && !getenv("SKL_DU_SPLITS") && (!s.t0 || !s.t1 || s.s0 == s.s1) &&
+        std::max(s.s0, s.s1) > 8 && smax >= 8 && 8 * (s.t0 + s.t1) <= pairs) {
+        const int S = 8;
+        if (s.t0) s.s0 = S;
+        if (s.t1) s.s1 = S;
+        s.units = s.t0 * s.s0 + s.t1 * s.s1;
+    }
+    const int sc = s.t0 ? s.s0 : s.s1;
+    const int lim = std::max(s.s0, s.s1) > 4 && deep_cr ? 8 : std::min(cr_max, 8);
+    s.cr = cr_on && sc <= lim && (!s.t0 || !s.t1 || s.s0 == s.s1);
     return s;
 }
 
