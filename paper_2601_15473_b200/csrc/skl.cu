@@ -1117,7 +1117,7 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
     g1.out2_c1 = (int)d.Lk;
     g1.out_f32 = eb == 4;
     g1.round_tf32 = eb == 4;  // H feeds a TF32 GEMM: round-to-nearest instead of hardware truncation
-        View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+    View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
     SKL_TRY(gemm_any(eb == 4, "gemm_H", vx, vat, (int)T, (int)d.R, (int)d.d_in, g1, di.sms, st));
     GemmArgs g2 = {};
     g2.alpha = inv;
@@ -1126,7 +1126,7 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
     g2.out = y;
     g2.ldo = d.d_out;
     g2.out_f32 = eb == 4;
-        View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
+    View vh{H, T, d.R, d.R_pad}, vbt{bcatT, d.d_out, d.R_pad, d.R_pad};
     SKL_TRY(gemm_any(eb == 4, "gemm_Y", vh, vbt, (int)T, (int)d.d_out, (int)d.R, g2, di.sms, st));
     return SKL_OK;
 }
@@ -1235,10 +1235,13 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
     const bool fused = use_fused(d, s->dtype) && !(rsplit_of(d, s->dtype) && (fuse & SKL_FUSE_RELU_IN));
     const bool bwd_direct = fused && grad_x != nullptr && direct_ok(d, s->dtype);
     const bool need_saved = ph_u1 && !saved_proj;
-    if ((ph_data && !bwd_direct) || need_saved)
-        SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, (ph_data && !bwd_direct) ? acat : nullptr,
-                              (ph_data && !bwd_direct) ? bcat : nullptr, need_saved ? acatT : nullptr, nullptr,
-                              nullptr, nullptr, st));
+    // no dX: only P_S2 = G·S2ᵀ, whose bf16 B operand is the S2s stack itself ([L*k][d_out], K-major)
+    const bool p2_only = ph_data && !grad_x;
+    const bool pack_data = ph_data && !bwd_direct && !(p2_only && kind == 0);
+    if (pack_data || need_saved)
+        SKL_CUDA(launch_pack2(d, elem, S1s, U2s, U1s, S2s, pack_data && !p2_only ? acat : nullptr,
+                              pack_data ? bcat : nullptr, need_saved ? acatT : nullptr, nullptr, nullptr, nullptr,
+                              st));
 
     // Savedᵀ = (x·S1)ᵀ, recomputed only when the caller did not keep it.
     const void* saved = saved_proj;
@@ -1252,7 +1255,7 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         g.out2_c1 = (int)d.Lk;
         g.out_f32 = eb == 4;
         g.round_tf32 = kind;
-                View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
+        View vx{x, T, d.d_in, d.d_in}, vat{acatT, d.R_pad, d.d_in, d.d_in};
         SKL_TRY(gemm_any(kind, "gemm_saved", vx, vat, (int)T, (int)d.Lk, (int)d.d_in, g, di.sms, st));
         saved = sv;
     }
@@ -1288,6 +1291,20 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
             SKL_TRY(run_b2b("b2b_bwd", 0, 2, B2BSrc{grad_y, U1s, S2s, S1s, U2s}, a, di.sms, st));
         else
             SKL_TRY(run_b2b("b2b_bwd", kind, 0, B2BSrc{grad_y, bcat, nullptr, acat, nullptr}, a, di.sms, st));
+    } else if (!grad_x) {
+        // no dX (e.g. the first layer of a chain): only P_S2 = G·S2ᵀ, the S2 rows of Bcat
+        GemmArgs g = {};
+        g.alpha = 1.f;
+        g.out2 = p2t;
+        g.ldo2 = ldt;
+        g.out2_c0 = 0;
+        g.out2_c1 = (int)d.Lk;
+        g.out_f32 = eb == 4;
+        g.round_tf32 = kind;
+        View vg{grad_y, T, d.d_out, d.d_out};
+        View vs2{kind == 0 ? S2s : static_cast<const void*>(static_cast<const uint8_t*>(bcat) + (size_t)d.Lk * d.d_out * eb),
+                 d.Lk, d.d_out, d.d_out};
+        SKL_TRY(gemm_any(kind, "gemm_P", vg, vs2, (int)T, (int)d.Lk, (int)d.d_out, g, di.sms, st));
     } else {
         GemmArgs g = {};
         g.alpha = 1.f;
@@ -1299,7 +1316,7 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         g.out2_c1 = (int)(2 * d.Lk);
         g.out_f32 = eb == 4;
         g.round_tf32 = kind;
-                View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
+        View vg{grad_y, T, d.d_out, d.d_out}, vb{bcat, d.R_pad, d.d_out, d.d_out};
         SKL_TRY(gemm_any(kind, "gemm_P", vg, vb, (int)T, (int)d.R, (int)d.d_out, g, di.sms, st));
         if (grad_x) {
             GemmArgs g2 = {};
@@ -1309,7 +1326,7 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
             g2.out = grad_x;
             g2.ldo = d.d_in;
             g2.out_f32 = eb == 4;
-                        View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
+            View vp{P, T, d.R, d.R_pad}, va{acat, d.d_in, d.R_pad, d.R_pad};
             SKL_TRY(gemm_any(kind, "gemm_dX", vp, va, (int)T, (int)d.d_in, (int)d.R, g2, di.sms, st));
         }
     }
