@@ -110,7 +110,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 
-template <int kCG, int kMode, int kKind = 0, bool kMask = false, bool kRS = false>
+template <int kCG, int kMode, int kKind = 0, bool kMask = false, bool kRS = false, bool kSP = false>
 struct B2BCfg {
     // kKind 1 (TF32, fp32 I/O): a k-block is 32 fp32 (still 128 B per row, so
     // every smem tile / descriptor has the bf16 byte geometry); the output
@@ -122,8 +122,11 @@ struct B2BCfg {
     static constexpr int kOutBytes = kKind == 0 ? 16384 : 32768;  // per epilogue group
     // The backward's GEMM1 (K = d_out, 80% of its MMAs) runs single-pass: one
     // A1 tile feeds both 256-wide chunks, so G is read once instead of twice;
-    // its stages therefore hold A1 + B1 for all of R (48 KB).
-    static constexpr bool kSinglePassG1 = kMode == 2 && kCG == 2;
+    // its stages therefore hold A1 + B1 for all of R (48 KB).  kSP does the same
+    // for a forward whose x is long (K1 = d_in >= 2048: the c5 FFN2 layer, c4),
+    // where the second pass would re-read a 1.5-2 MB x tile per pair that no
+    // longer fits L2 with every pair streaming.
+    static constexpr bool kSinglePassG1 = (kMode == 2 || kSP) && kCG == 2;
     static constexpr int kStageBytes = (kCG == 1 || kSinglePassG1) ? 48 * 1024 : 32 * 1024;
     // The forward keeps the whole bias (fp32, N2 <= kMaxBiasTab) resident in
     // smem and gives up one stage for it; its GEMM2 stages are 4 k-blocks deep.
@@ -138,7 +141,7 @@ struct B2BCfg {
     // kRS: one 16 KB receive slot per epilogue warpgroup ([128 rows][32 fp32],
     // chunk-swizzled) for the running GEMM2 partial of the previous pair.
     static constexpr int kRecvBytes = kRS ? 2 * 16384 : 0;
-    static constexpr int kStages = (kSinglePassG1 ? 4 : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind) -
+    static constexpr int kStages = (kSinglePassG1 ? (kBiasTab ? 3 : 4) : (kCG == 1 ? 4 : 6) - (kBiasTab ? 1 : 0) - kKind) -
                                    (kMaskBytes + kRecvBytes + kStageBytes - 1) / kStageBytes;
     static constexpr int kAOff = 16384;                      // B1 offset inside a GEMM1 stage
     static constexpr int kRingBytes = kStages * kStageBytes;
@@ -161,13 +164,13 @@ struct B2BCfg {
 // kPost: 1 = the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
 // mask), 2 = the same with 1-bit masks (relu_bits / mask_bits); separate
 // instantiations so the plain layer keeps its register budget.
-template <int kCG, int kMode, int kKind, int kPost, bool kRS = false>
+template <int kCG, int kMode, int kKind, int kPost, bool kRS = false, bool kSP = false>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
                const __grid_constant__ CUtensorMap tmM, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS>;
+    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));

@@ -220,9 +220,9 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false>
+template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false, bool kSP = false>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS>;
+    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     constexpr int eb = C::kElem, bk = C::kBK;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
@@ -249,7 +249,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     if (C::kMaskStage && a.mask) SKL_TRY(make_tmap(&tm, a.mask, eb, a.N2, a.T, a.ld_mask, bk, 128));  // output-tile boxes
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     const int csize = kCG * (kRS ? a.nsplit : 1);  // CTAs per cluster
-    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS>;
+    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS, kSP>;
     static std::atomic<uint64_t> attr_done{0};
     SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done, /*clusters of 8 for 4 R-split pairs*/ kRS));
     cudaLaunchConfig_t cfg = {};
@@ -372,6 +372,10 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         return run_b2b_cg<1, 0, 1>(name, src, a, sms, st);
     }
     if (g_b2b_cg == 2) {
+        // forward with a long x (K1 >= 2048) and two H chunks: single-pass GEMM1 (SKL_FWD_SP=0 off)
+        static const int fwd_sp = getenv("SKL_FWD_SP") ? atoi(getenv("SKL_FWD_SP")) : -1;
+        if (mode == 1 && a.R_pad > 256 && (fwd_sp == 1 || (fwd_sp < 0 && a.K1 >= 2048)))
+            return run_b2b_cg<2, 1, 0, 0, false, true>(name, src, a, sms, st);
         if (mode == 1) return run_b2b_cg<2, 1, 0>(name, src, a, sms, st);
         if (mode == 2) return run_b2b_cg<2, 2, 0>(name, src, a, sms, st);
         return run_b2b_cg<2, 0, 0>(name, src, a, sms, st);
