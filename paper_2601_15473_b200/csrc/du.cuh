@@ -55,8 +55,6 @@ struct DuArgs {
     int coop;        // 1: cooperative launch (all units co-resident) -> slice-parallel reduction
     int relay;       // 1: per-CTA TMA barriers + peer relay (needed when colsum reads both halves)
     int l2hint;      // L2 cache-hint policy bits for the operand loads (see the producer)
-    int rev;         // 1: every unit streams its token range last-to-first (the tokens the previous
-                     // kernel touched last -- still in L2 -- come first)
     int cr;          // cluster reduction: one cluster of 2S CTAs per tile (S splits = S pairs); each CTA
                      // bulk-stores its partial, the cluster barrier publishes it, each CTA bulk-loads its slice
 };
@@ -223,7 +221,7 @@ __global__ void __launch_bounds__(256, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
-                    const int k0 = (args.rev ? x.kb1 - 1 - (kb - x.kb0) : kb) * KT::kBK;
+                    const int k0 = kb * KT::kBK;
                     if (!args.relay) {
                         // no colsum anywhere: pair-signalled TMA straight onto the leader's barrier
                         if (leader) mbar_arrive_expect_tx(&full[stage], 2 * kDuStageBytes);

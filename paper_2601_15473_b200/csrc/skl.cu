@@ -829,8 +829,6 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     static const int du_l2hint = getenv("SKL_DU_L2HINT") ? atoi(getenv("SKL_DU_L2HINT")) : 2;
     a.l2hint = du_l2hint;
     a.num_tiles = u.tiles();
-    static const bool du_rev = !(getenv("SKL_DU_REVERSE") && atoi(getenv("SKL_DU_REVERSE")) == 0);
-    a.rev = du_rev ? 1 : 0;
     const int u1_units = (which & 1) ? u.t0 * u.s0 : 0;
     const DuProblem pu1{(int)d.Lk, (int)d.d_out, u.m0, u.n0t, 0, u.s0, 0, 0, grad_bias ? 1 : 0, inv, grad_U1s,
                         (long long)1 << 40, 0, (long long)d.d_out, 1, grad_bias};
