@@ -273,8 +273,7 @@ __global__ void __launch_bounds__(384, 1)
     // ---- tile queue: CTA 0 of the cluster claims tiles from the global counter
     // (first come, first served: clusters that start early -- args.early -- take
     // more) and publishes each to every CTA of its cluster; -1 ends the loop.
-    unsigned int* sched = g_b2b_sched[args.sched < 0 ? 0 : args.sched];
-    const int cluster_id = blockIdx.x / csize, num_clusters = gridDim.x / csize;
+    unsigned int* sched = g_b2b_sched[args.sched];
     auto publish = [&](int k, int t) {  // CTA 0, producer thread
         const int slot = k & 1;
         mbar_wait_cluster(&qempty[slot], ((k >> 1) & 1) ^ 1);
@@ -287,8 +286,7 @@ __global__ void __launch_bounds__(384, 1)
         }
     };
     auto claim = [&](int k) -> int {  // CTA 0, producer thread
-        // args.sched < 0: the static round-robin order (A/B)
-        int t = args.sched < 0 ? cluster_id + k * num_clusters : (int)atomicAdd(&sched[0], 1u);
+        int t = (int)atomicAdd(&sched[0], 1u);
         if (t >= num_tiles) t = -1;
         publish(k, t);
         return t;
@@ -923,7 +921,7 @@ __global__ void __launch_bounds__(384, 1)
         tc_fence_after();
         tmem_dealloc<kCG>(tmem_base, 512);
     }
-    if (threadIdx.x == 0 && args.sched >= 0) {  // the last CTA to finish resets this launch's scheduler slot
+    if (threadIdx.x == 0) {  // the last CTA to finish resets this launch's scheduler slot
         __threadfence();
         if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
             atomicExch(&sched[0], 0u);

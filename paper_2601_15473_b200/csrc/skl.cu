@@ -318,8 +318,6 @@ skl_status run_b2b_tf32_wide(const char* name, const B2BSrc& src, B2BArgs a, int
 // workspace are stream-ordered, so one slot per workspace never has two live
 // launches.  Slots are handed out round-robin.
 int sched_slot(const void* ws) {
-    static const bool stat = getenv("SKL_B2B_STATIC") && atoi(getenv("SKL_B2B_STATIC")) != 0;
-    if (stat) return -1;
     static std::mutex mu;
     static std::unordered_map<const void*, int> slots;
     static int next = 0;
