@@ -73,7 +73,6 @@ struct B2BArgs {
     long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
     int l2hint;                  // L2 cache-hint policy bits for the producer's TMA loads
     int early;                   // start before the previous kernel completes (SKL_FUSE_EARLY_START)
-    int sched;                   // tile-scheduler slot (g_b2b_sched), one per caller workspace
 };
 
 namespace dev {
@@ -111,14 +110,6 @@ __device__ __forceinline__ void mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_
             "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
             "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-
-// Dynamic tile scheduler: [slot][0] tiles claimed, [slot][1] CTAs finished.
-// Zero at module load; the last CTA of every launch resets its slot, so the
-// state is zero between launches (CUDA-graph replays included).  The host gives
-// every caller workspace its own slot (two launches on one workspace are
-// stream-ordered).
-constexpr int kSchedSlots = 1024;
-__device__ unsigned int g_b2b_sched[kSchedSlots][2];
 
 template <int kCG, int kMode, int kKind = 0, bool kMask = false, bool kRS = false, bool kSP = false>
 struct B2BCfg {
@@ -199,10 +190,7 @@ __global__ void __launch_bounds__(384, 1)
     uint64_t* mfull = tempty2 + 2;                    // [2] kMask: this group's mask tile landed
     uint64_t* rfull = mfull + 2;                      // [2] kRS: this group's receive slot holds a partial
     uint64_t* sfree = rfull + 2;                      // [2] kRS: the next pair's receive slot is free
-    uint64_t* qfull = sfree + 2;                      // [2] tile queue entry published
-    uint64_t* qempty = qfull + 2;                     // [2] tile queue entry read by every consumer (CTA 0)
-    int* q_tile = reinterpret_cast<int*>(qempty + 2);  // [2] tile queue
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_tile + 2);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfree + 2);
 
     const uint32_t warp = warp_id();
     // Cluster layout: pairs are CTA ranks (2p, 2p+1); kRS clusters hold nsplit pairs.
@@ -241,10 +229,6 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&mfull[i], 1);
             mbar_init(&rfull[i], 4);          // the 4 sender warps of the previous pair's group
             mbar_init(&sfree[i], 4);          // the 4 receiver warps of the next pair's group
-            mbar_init(&qfull[i], 1);          // CTA 0's producer publishes
-            // consumers in the cluster: every producer but CTA 0's, every pair leader's MMA
-            // issuer, every epilogue warp
-            mbar_init(&qempty[i], (kCG * nsplit - 1) + nsplit + 8 * kCG * nsplit);
         }
         if constexpr (C::kMaskStage) prefetch_tmap(&tmM);
         fence_barrier_init();
@@ -269,39 +253,8 @@ __global__ void __launch_bounds__(384, 1)
 
     const int tile_rows = 128 * kCG;
     const int num_tiles = (args.T + tile_rows - 1) / tile_rows;
-    const int csize = kCG * nsplit;  // CTAs per cluster
-    // ---- tile queue: CTA 0 of the cluster claims tiles from the global counter
-    // (first come, first served: clusters that start early -- args.early -- take
-    // more) and publishes each to every CTA of its cluster; -1 ends the loop.
-    unsigned int* sched = g_b2b_sched[args.sched];
-    auto publish = [&](int k, int t) {  // CTA 0, producer thread
-        const int slot = k & 1;
-        mbar_wait_cluster(&qempty[slot], ((k >> 1) & 1) ^ 1);
-        for (int c = 0; c < csize; ++c) {
-            asm volatile(
-                "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, %1;\n\t"
-                "st.shared::cluster.b32 [ra], %2;\n\t}" ::"r"(smem_u32(&q_tile[slot])), "r"(c), "r"(t)
-                : "memory");
-            mbar_arrive_remote_release(&qfull[slot], (uint32_t)c);
-        }
-    };
-    auto claim = [&](int k) -> int {  // CTA 0, producer thread
-        int t = (int)atomicAdd(&sched[0], 1u);
-        if (t >= num_tiles) t = -1;
-        publish(k, t);
-        return t;
-    };
-    auto get_tile = [&](int k) -> int {  // any consumer thread (a warp: every lane calls it)
-        mbar_wait_cluster(&qfull[k & 1], (k >> 1) & 1);
-        return *reinterpret_cast<volatile int*>(&q_tile[k & 1]);
-    };
-    auto release_tile = [&](int k) { mbar_arrive_remote_release(&qempty[k & 1], 0); };  // once per consumer
-    auto next_tile = [&](int k) -> int {  // the producer's view: claim (CTA 0) or read
-        if (crank == 0) return claim(k);
-        const int t = get_tile(k);
-        release_tile(k);
-        return t;
-    };
+    const int cluster_id = blockIdx.x / (kCG * nsplit);
+    const int num_clusters = gridDim.x / (kCG * nsplit);
     const int nch = (r_loc + 255) / 256;
     const int nkb1 = (args.K1 + C::kBK - 1) / C::kBK;
     const int nkb2 = r_loc / C::kBK;
@@ -397,20 +350,11 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             };
-            int k = 0;
-            int t = next_tile(k);
-            if (pp && t >= 0) load_g1(t);
-            while (t >= 0) {
-                if (!pp) {
-                    load_g1(t);
-                    load_g2();
-                    t = next_tile(++k);
-                } else {  // the next tile's GEMM1 operands before this tile's GEMM2 operands
-                    const int tn = next_tile(++k);
-                    if (tn >= 0) load_g1(tn);
-                    load_g2();
-                    t = tn;
-                }
+            if (pp && cluster_id < num_tiles) load_g1(cluster_id);
+            for (int t = cluster_id; t < num_tiles; t += num_clusters) {
+                if (!pp) load_g1(t);
+                else if (t + num_clusters < num_tiles) load_g1(t + num_clusters);
+                load_g2();
             }
         }
     } else if (warp == 1) {
@@ -483,31 +427,15 @@ __global__ void __launch_bounds__(384, 1)
                     commit(&tfull2[s]);
                 }
             };
-            int k = 0;
-            int t = get_tile(k);
-            release_tile(k);
-            if (pp && t >= 0) issue_g1(0, 0);
-            while (t >= 0) {
-                int tn = -1;
-                if (!pp) {
-                    issue_g1(0, 0);
-                } else {  // GEMM1 of the next tile before GEMM2 of this one (the producer's order)
-                    tn = get_tile(k + 1);
-                    release_tile(k + 1);
-                    if (tn >= 0) issue_g1(128u * ((it + 1) & 1), (it + 1) & 1);
-                }
+            if (pp && cluster_id < num_tiles) issue_g1(0, 0);
+            for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
+                if (!pp) issue_g1(0, 0);
+                else if (t + num_clusters < num_tiles) issue_g1(128u * ((it + 1) & 1), (it + 1) & 1);
                 // ---- wait for the bf16 H of this tile (both CTAs)
                 if (pp) mbar_wait(&hready[it & 1], (it >> 1) & 1);
                 else for (int c = 0; c < nch; ++c) mbar_wait(&hready[c], it & 1);
                 tc_fence_after();
                 issue_g2(pp ? 128u * (it & 1) : 0u);
-                ++k;
-                ++it;
-                if (!pp) {
-                    tn = get_tile(k);
-                    release_tile(k);
-                }
-                t = tn;
             }
         }
     } else if (warp >= 4) {
@@ -630,11 +558,7 @@ __global__ void __launch_bounds__(384, 1)
             ++xch;
         };
         int it = 0;
-        for (;; ++it) {
-            const int t = get_tile(it);
-            __syncwarp();
-            if (lane == 0) release_tile(it);
-            if (t < 0) break;
+        for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             cur_t = t;
             const int row = t * tile_rows + (int)rank * 128 + (int)srow;
             const bool row_ok = row < args.T;
@@ -920,14 +844,6 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kCG>(tmem_base, 512);
-    }
-    if (threadIdx.x == 0) {  // the last CTA to finish resets this launch's scheduler slot
-        __threadfence();
-        if (atomicAdd(&sched[1], 1u) == gridDim.x - 1) {
-            atomicExch(&sched[0], 0u);
-            atomicExch(&sched[1], 0u);
-            __threadfence();
-        }
     }
     if (args.early) {  // keep "a dependent starts only after every earlier kernel completed"
         pdl_wait();

@@ -22,7 +22,6 @@
 #include <cstring>
 #include <mutex>
 #include <string>
-#include <unordered_map>
 
 #include "../../include/skl.h"
 #include "b2b.cuh"
@@ -312,21 +311,6 @@ skl_status run_b2b_tf32_wide(const char* name, const B2BSrc& src, B2BArgs a, int
     ProfScope ps_(name, st);
     SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb2, ty, a));
     return SKL_OK;
-}
-
-// Tile-scheduler slot of a caller workspace (b2b.cuh g_b2b_sched): launches on one
-// workspace are stream-ordered, so one slot per workspace never has two live
-// launches.  Slots are handed out round-robin.
-int sched_slot(const void* ws) {
-    static std::mutex mu;
-    static std::unordered_map<const void*, int> slots;
-    static int next = 0;
-    std::lock_guard<std::mutex> lk(mu);
-    auto it = slots.find(ws);
-    if (it != slots.end()) return it->second;
-    const int s = next++ % dev::kSchedSlots;
-    slots.emplace(ws, s);
-    return s;
 }
 
 int g_b2b_cg = 2;       // CTA-group width of the fused kernel (SKL_B2B_CG=1 forces single-CTA MMAs)
@@ -1120,7 +1104,6 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
         a.Lk = (int)d.Lk;
         a.k = (int)d.k;
         a.dS = (int)d.d_in;
-        a.sched = sched_slot(workspace);
         if (direct) return run_b2b("b2b_fwd", 0, 1, B2BSrc{x, S1s, U2s, U1s, S2s}, a, di.sms, st);
         return run_b2b("b2b_fwd", s->dtype == SKL_BF16 ? 0 : 1, 0, B2BSrc{x, acatT, nullptr, bcatT, nullptr}, a,
                        di.sms, st);
@@ -1313,7 +1296,6 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         a.Lk = (int)d.Lk;
         a.k = (int)d.k;
         a.dS = (int)d.d_in;
-        a.sched = sched_slot(workspace);
         if (bwd_direct)
             SKL_TRY(run_b2b("b2b_bwd", 0, 2, B2BSrc{grad_y, U1s, S2s, S1s, U2s}, a, di.sms, st));
         else
