@@ -43,7 +43,7 @@ ABI_SYMBOLS = (
     "dense_linear_backward",
 )
 BWD_DU1_DB, BWD_DX_DU2, BWD_ALL = 1, 2, 3
-FUSE_RELU_OUT, FUSE_RELU_IN, FUSE_RELU_BITS, FUSE_EARLY_START = 1, 2, 4, 8
+FUSE_RELU_OUT, FUSE_RELU_IN, FUSE_RELU_BITS = 1, 2, 4
 
 
 class SklError(RuntimeError):

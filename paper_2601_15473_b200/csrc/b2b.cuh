@@ -72,7 +72,6 @@ struct B2BArgs {
     const uint32_t* mask_bits;   // backward: out *= bit, instead of reading `mask`
     long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
     int l2hint;                  // L2 cache-hint policy bits for the producer's TMA loads
-    int early;                   // start before the previous kernel completes (SKL_FUSE_EARLY_START)
 };
 
 namespace dev {
@@ -241,15 +240,8 @@ __global__ void __launch_bounds__(384, 1)
     if constexpr (kCG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    // inputs of this launch may come from the previous kernel in the stream; trigger
-    // dependents only after the wait, so when one starts our predecessor has completed.
-    // args.early (SKL_FUSE_EARLY_START): the caller guarantees the previous kernel
-    // writes nothing this launch reads and shares no workspace with it (the previous
-    // layer's dU kernel in a chain backward), so we start at once and wait at the end.
-    if (!args.early) {
-        pdl_wait();
-        pdl_launch_dependents();
-    }
+    pdl_wait();  // inputs of this launch may come from the previous kernel in the stream
+    pdl_launch_dependents();  // after the wait: a dependent starts only once our predecessor completed
 
     const int tile_rows = 128 * kCG;
     const int num_tiles = (args.T + tile_rows - 1) / tile_rows;
@@ -844,10 +836,6 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<kCG>(tmem_base, 512);
-    }
-    if (args.early) {  // keep "a dependent starts only after every earlier kernel completed"
-        pdl_wait();
-        pdl_launch_dependents();
     }
 }
 

@@ -1157,8 +1157,7 @@ skl_status sketched_linear_backward_ex(const skl_shape* s, int64_t T, unsigned p
                                        const void* S2s, const void* U1s, const void* U2s, void* grad_x,
                                        float* grad_U1s, float* grad_U2s, float* grad_bias, void* workspace,
                                        size_t ws_bytes, void* stream) {
-    if (fuse & ~(unsigned)(SKL_FUSE_RELU_IN | SKL_FUSE_EARLY_START))
-        return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
+    if (fuse & ~(unsigned)SKL_FUSE_RELU_IN) return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
     return sketched_linear_backward_bits(s, T, phases, fuse, grad_y, x, saved_proj, S1s, S2s, U1s, U2s, grad_x,
                                          grad_U1s, grad_U2s, grad_bias, nullptr, workspace, ws_bytes, stream);
 }
@@ -1168,7 +1167,7 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
                                          const void* S2s, const void* U1s, const void* U2s, void* grad_x,
                                          float* grad_U1s, float* grad_U2s, float* grad_bias, const uint32_t* relu_bits,
                                          void* workspace, size_t ws_bytes, void* stream) {
-    if (fuse & ~(unsigned)(SKL_FUSE_RELU_IN | SKL_FUSE_RELU_BITS | SKL_FUSE_EARLY_START))
+    if (fuse & ~(unsigned)(SKL_FUSE_RELU_IN | SKL_FUSE_RELU_BITS))
         return fail(SKL_ERR_PARAM, "backward: unsupported fuse flags %u", fuse);
     const bool bits = (fuse & SKL_FUSE_RELU_BITS) != 0;
     if (bits && (!(fuse & SKL_FUSE_RELU_IN) || (T > 0 && !relu_bits)))
@@ -1219,10 +1218,8 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         skl_shape sp = *s;
         sp.d_in = dp.d_in;
         sp.d_out = dp.d_out;
-        // the repad launches above precede the data-path kernel: no early start here
-        SKL_TRY(sketched_linear_backward_bits(&sp, T, phases, fuse & ~(unsigned)SKL_FUSE_EARLY_START, gp, xp,
-                                              saved_proj, s1p, s2p, u1p, u2p, gxp, du1p, du2p, dbp, relu_bits,
-                                              workspace, q.inner, stream));
+        SKL_TRY(sketched_linear_backward_bits(&sp, T, phases, fuse, gp, xp, saved_proj, s1p, s2p, u1p, u2p, gxp, du1p,
+                                              du2p, dbp, relu_bits, workspace, q.inner, stream));
         if (ph_u1 && du1p != grad_U1s) SKL_CUDA(launch_repad(du1p, 4, d.L, d.k, dp.d_out, grad_U1s, d.k, d.d_out, st));
         if (ph_u1 && dbp != grad_bias) SKL_CUDA(launch_repad(dbp, 4, 1, 1, dp.d_out, grad_bias, 1, d.d_out, st));
         if (ph_data && du2p != grad_U2s) SKL_CUDA(launch_repad(du2p, 4, d.L, dp.d_in, d.k, grad_U2s, d.d_in, d.k, st));
@@ -1283,8 +1280,6 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
         a.bias = nullptr;
         a.mask = (fuse & SKL_FUSE_RELU_IN) && !bits ? x : nullptr;  // grad_x *= (x > 0): the preceding ReLU's backward
         a.mask_bits = bits ? relu_bits : nullptr;                       // ... or its 1-bit form from the forward
-        // first kernel of this call, so its predecessor is the caller's previous launch
-        a.early = (fuse & SKL_FUSE_EARLY_START) && bwd_direct && !need_saved && pdl_enabled() ? 1 : 0;
         a.bits_ld = skl_relu_bits_row_words(d.d_in);
         a.ld_mask = d.d_in;
         a.out = grad_x;

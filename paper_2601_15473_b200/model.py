@@ -22,8 +22,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass, field
 
-from . import (BF16, BWD_ALL, BWD_DU1_DB, BWD_DX_DU2, FUSE_EARLY_START, FUSE_RELU_IN, FUSE_RELU_OUT, DenseLinear,
-               ShapeError,
+from . import (BF16, BWD_ALL, BWD_DU1_DB, BWD_DX_DU2, FUSE_RELU_IN, FUSE_RELU_OUT, DenseLinear, ShapeError,
                SkLinear, SklError, backward_phase, dense_backward, dense_forward, dense_workspace_size, forward,
                relu_bits_row_words, relu_bits_supported, torch_dtype, workspace_size)
 
@@ -85,7 +84,7 @@ class SkChain:
             self.steps.append(_Step(lyr, relu_out=False, relu_in=prev_relu))
             prev_relu = False
         self.dtype = self.steps[0].layer.dtype
-        self._ws = [None, None]  # alternating per layer in the backward (SKL_FUSE_EARLY_START)
+        self._ws = None
 
     def layers(self):
         """The chain's layer list as given (SkLinear / DenseLinear / Relu, repeated
@@ -100,13 +99,13 @@ class SkChain:
     def d_out(self):
         return self.steps[-1].layer.d_out
 
-    def _workspace(self, T, device, which=0):
+    def _workspace(self, T, device):
         import torch
         need = max(max(dense_workspace_size(st.layer.shape, T) if isinstance(st.layer, DenseLinear)
                        else workspace_size(st.layer.shape, T)) for st in self.steps)
-        if self._ws[which] is None or self._ws[which].numel() < need:
-            self._ws[which] = torch.empty(need, dtype=torch.uint8, device=device)
-        return self._ws[which]
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device)
+        return self._ws
 
     def forward(self, x, train=True):
         """model_forward (nn_model.cpp:111-122).  train=True keeps each layer's
@@ -174,26 +173,17 @@ class SkChain:
             overlap = dist.is_available() and dist.is_initialized()
         if buckets is None:
             buckets = self.allocate_grads(g.device)
-        wss = (self._workspace(T, g.device, 0), self._workspace(T, g.device, 1))
+        ws = self._workspace(T, g.device)
         td = torch_dtype(self.dtype)
         works = []
         cur = g
-        last = len(self.steps) - 1
-        # Every layer's G stays referenced until the backward returns: with early starts a
-        # layer's dX kernel runs alongside the layer above's dU kernel, which still reads that
-        # layer's G -- torch's stream-ordered allocator must not hand the block out again.
-        hold = []
-        for i in range(last, -1, -1):
+        for i in range(len(self.steps) - 1, -1, -1):
             st, b = self.steps[i], buckets[i]
             L = st.layer
-            ws = wss[i & 1]  # consecutive layers never share a workspace
             gx = torch.empty(T, L.d_in, dtype=td, device=g.device) if (i > 0 or need_grad_x) else None
             fuse = FUSE_RELU_IN if st.relu_in else 0
-            # below the top layer, the previous kernel is the layer above's dU launch, which reads
-            # only its own G / x / saved and writes dU / db: this layer's dX kernel starts under it
-            early = FUSE_EARLY_START if (i < last and not phased) else 0
             if isinstance(L, DenseLinear):
-                dense_backward(L.shape, cur, st.x, L.W, gx, b.dW, b.db, ws, fuse=fuse)  # (no early start)
+                dense_backward(L.shape, cur, st.x, L.W, gx, b.dW, b.db, ws, fuse=fuse)
                 if overlap:
                     w = b.allreduce_(group, async_op=True)
                     if w is not None:
@@ -214,16 +204,13 @@ class SkChain:
                 # NCCL's stream while the layers below run theirs (SURVEY §8e "in the
                 # stack"); the phased split would cost a second du launch per layer
                 backward_phase(L.shape, BWD_ALL, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
-                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse | early,
-                               relu_bits=st.bits if st.relu_in else None)
+                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
                 w = b.allreduce_(group, async_op=True)
                 if w is not None:
                     works.append(w)
             else:
                 backward_phase(L.shape, BWD_ALL, cur, st.x, st.saved, L.S1s, L.S2s, L.U1s, L.U2s, gx,
-                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse | early,
-                               relu_bits=st.bits if st.relu_in else None)
-            hold.append(cur)
+                               b.dU1s, b.dU2s, b.db, ws, fuse=fuse, relu_bits=st.bits if st.relu_in else None)
             cur = gx
         return ChainGrads(cur, buckets), works
 
