@@ -3,6 +3,8 @@
   python tools/make_profiles_r2.py sass      # profiles/r2_sass_summary.txt (cuobjdump of libskl.so, no GPU needed)
   python tools/make_profiles_r2.py ncu       # from gpurun_out/r2_launches.csv + gpurun_out/r2_c2_full.ncu-rep:
                                              #   profiles/r2_launches.txt, r2_ncu_c2_summary.txt, traffic.json
+  python tools/make_profiles_r2.py rep IN.ncu-rep OUT.txt "what was captured"
+                                             # key metrics of every launch in one capture
 """
 import csv
 import json
@@ -97,5 +99,36 @@ def ncu():
     print(traffic)
 
 
+KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+        "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+        "sm__pipe_tensor_cycles_active.max.pct_of_peak_sustained_elapsed",
+        "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+        "lts__t_sector_hit_rate.pct", "gpc__cycles_elapsed.avg.per_second", "launch__registers_per_thread",
+        "launch__grid_size", "launch__cluster_dim_x", "launch__shared_mem_per_block_dynamic"]
+
+
+def rep(path, out, what):
+    o = subprocess.run(["/usr/local/cuda/bin/ncu", "-i", path, "--page", "raw", "--csv"],
+                       capture_output=True, text=True).stdout
+    rows = list(csv.reader(o.splitlines()))
+    h, units = rows[0], rows[1]
+    ci = {k: i for i, k in enumerate(h)}
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    lines = ["# ncu --set full --clock-control none --import-source on: %s" % what,
+             "# (%s); dram_GBps = (dram read + write bytes) / gpu__time_duration" % path, ""]
+    for r in rows[2:]:
+        lines.append("[%s]" % r[ci["Kernel Name"]][:110])
+        for k in KEYS:
+            if k in ci:
+                lines.append("  %s = %s %s" % (k, r[ci[k]], units[ci[k]]))
+        val = lambda k: float(r[ci[k]].replace(",", "")) * scale.get(units[ci[k]], 1)
+        us = float(r[ci["gpu__time_duration.sum"]].replace(",", "")) * {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "ms": 1e3,
+                                                                         "msecond": 1e3}[units[ci["gpu__time_duration.sum"]]]
+        lines.append("  dram_GBps = %.0f" % ((val("dram__bytes_read.sum") + val("dram__bytes_write.sum")) / us / 1e3))
+        lines.append("")
+    open(out, "w").write("\n".join(lines))
+    print("\n".join(lines[:40]))
+
+
 if __name__ == "__main__":
-    {"sass": sass, "ncu": ncu}[sys.argv[1]]()
+    {"sass": sass, "ncu": ncu, "rep": rep}[sys.argv[1]](*sys.argv[2:])
