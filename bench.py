@@ -40,7 +40,13 @@ D_IN, D_OUT, L, K_RANK, T_GPU = 768, 3072, 2, 128, 32768
 SEED = 42
 WORKLOAD = (f"c2: SKLinear fwd+bwd d_in={D_IN} d_out={D_OUT} L={L} k={K_RANK}, "
             f"{T_GPU} tokens per GPU (BERT-base FFN shape)")
-RESERVED_SMS = 8     # SMs left to NCCL when N > 1 (NCCL_MAX_CTAS matches)
+# SMs libskl leaves free for NCCL when N > 1.  0: measured on one B200, 8
+# reserved SMs cost the phased step 28 us (312 vs 284 us) while the persistent
+# b2b_bwd kernel frees 40 SMs after its first wave anyway (128 tiles on 74
+# pairs), under which the head all-reduce runs -- its NCCL stream is created
+# high-priority so its CTAs take those SMs first.
+RESERVED_SMS = 0
+NCCL_CTAS = 8        # NCCL_MAX_CTAS for the ~3-4 MB gradient buckets
 
 
 def peaks():
@@ -413,8 +419,10 @@ def main():
 
     torch.cuda.set_device(local_rank)
     if world > 1:
-        os.environ.setdefault("NCCL_MAX_CTAS", str(RESERVED_SMS))
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        os.environ.setdefault("NCCL_MAX_CTAS", str(NCCL_CTAS))
+        opts = dist.ProcessGroupNCCL.Options()
+        opts.is_high_priority_stream = True
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank), pg_options=opts)
     dev = torch.device("cuda", local_rank)
     stream = torch.cuda.current_stream()
 
@@ -586,9 +594,10 @@ def main():
             workloads.append(measure_stack(skl, torch, dev, world))
         except Exception as e:
             workloads.append({"workload": "c5 stack", "error": str(e)[:200]})
-        try:  # the DP schedule's phased backward (two dU launches, 8 SMs left to NCCL), no collective
+        try:  # the DP schedule's phased backward (two dU launches, RESERVED_SMS left to NCCL), no collective
             skl.set_reserved_sms(RESERVED_SMS)
-            workloads.append(measure_workload(skl, torch, dev, "c2 bf16, DP-phased backward (8 SMs reserved)",
+            workloads.append(measure_workload(skl, torch, dev,
+                                              f"c2 bf16, DP-phased backward ({RESERVED_SMS} SMs reserved)",
                                               D_IN, D_OUT, L, K_RANK, T_GPU, "bf16", phased=True))
         finally:
             skl.set_reserved_sms(0)

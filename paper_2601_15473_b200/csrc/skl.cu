@@ -513,6 +513,39 @@ struct DuShape {
     bool cr;                                          // cluster (DSMEM) reduction of the split partials
     int tiles() const { return t0 + t1; }
 };
+// How many clusters of `csize` du CTAs the device runs at once
+// (cudaOccupancyMaxActiveClusters): a cluster must find csize free SMs inside
+// one GPC, so clusters of 12 or 16 CTAs fit only one per GPC.  Cached per
+// (device, kind, csize); without a device, the 8-GPC x 18-SM model.
+int du_cluster_cap(int kind, int csize) {
+    static std::atomic<int> cache[64][2][17];
+    int dev = 0;
+    if (csize < 1 || csize > 16 || cudaGetDevice(&dev) != cudaSuccess) return 8 * std::max(1, 18 / std::max(1, csize));
+    std::atomic<int>& c = cache[dev & 63][kind & 1][csize];
+    const int v = c.load(std::memory_order_relaxed);
+    if (v > 0) return v;
+    auto kern = kind == 0 ? dev::du_kernel<0> : dev::du_kernel<1>;
+    int n = 0;
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dev::kDuSmem) == cudaSuccess &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) == cudaSuccess) {
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(csize * 64);
+        cfg.blockDim = dim3(256);
+        cfg.dynamicSmemBytes = dev::kDuSmem;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = csize;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) n = 0;
+    }
+    (void)cudaGetLastError();
+    if (n <= 0) n = 8 * std::max(1, 18 / csize);
+    c.store(n, std::memory_order_relaxed);
+    return n;
+}
 DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) {
     DuShape s;
     s.m0 = (int)((d.Lk + 255) / 256);
@@ -572,8 +605,11 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     // same kernel time and, with no grid-wide barrier, lets the next kernel's
     // CTAs start as this one's retire (projection backward 73.5 -> 68.5 us).
     static const bool deep_cr = !(getenv("SKL_DU_DEEP_CR") && atoi(getenv("SKL_DU_DEEP_CR")) == 0);
+    // It needs enough tiles to keep half the pairs busy: the DP-phased dU2-only
+    // launch at c2 has 3 tiles, and its 24 pairs took 40-47 us where the
+    // cooperative S = 24 split on 72 pairs takes 33 us.
     if (cr_on && deep_cr && !getenv("SKL_DU_SPLITS") && (!s.t0 || !s.t1 || s.s0 == s.s1) &&
-        std::max(s.s0, s.s1) > 8 && smax >= 8 && 8 * (s.t0 + s.t1) <= pairs) {
+        std::max(s.s0, s.s1) > 8 && smax >= 8 && 8 * (s.t0 + s.t1) <= pairs && 2 * 8 * (s.t0 + s.t1) >= pairs) {
         const int S = 8;
         if (s.t0) s.s0 = S;
         if (s.t1) s.s1 = S;
@@ -582,6 +618,13 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     const int sc = s.t0 ? s.s0 : s.s1;
     const int lim = std::max(s.s0, s.s1) > 4 && deep_cr ? 8 : std::min(cr_max, 8);
     s.cr = cr_on && sc <= lim && (!s.t0 || !s.t1 || s.s0 == s.s1);
+    // Clusters of 2S CTAs pack per GPC (cudaOccupancyMaxActiveClusters: 74 / 33 /
+    // 22 / 15 / 11 / 7 clusters of 2 / 4 / 6 / 8 / 10 / 12+ CTAs on a B200), so a
+    // one-wave split whose clusters do not all fit runs in two waves.  Those
+    // shapes take the cooperative reduction at the same split instead: c2's
+    // DP-phased dU1-only launch (12 tiles, S = 6) 80 us as clusters of 12,
+    // 71 us at S = 4 in clusters of 8, 55-66 us cooperative at S = 6.
+    if (s.cr && !getenv("SKL_DU_SPLITS") && s.tiles() > du_cluster_cap(kind, 2 * sc)) s.cr = false;
     return s;
 }
 
@@ -822,6 +865,10 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         return run_dut(d, T, kind, which, saved, grad_y, p2t, x, grad_U1s, grad_U2s, grad_bias, workspace, p, sms, st,
                        inv);
     const DuShape u = du_shape(d, T, sms, kind, which);
+    static const bool verbose = getenv("SKL_DU_VERBOSE") != nullptr;
+    if (verbose)
+        fprintf(stderr, "[skl du] which=%d tiles=%d+%d splits=%d,%d units=%d kb=%d cr=%d sms=%d cap(2S)=%d\n", which,
+                u.t0, u.t1, u.s0, u.s1, u.units, u.kb, (int)u.cr, sms, du_cluster_cap(kind, 2 * (u.t0 ? u.s0 : u.s1)));
     DuArgs a = {};
     a.k_blocks = u.kb;
     a.num_units = u.units;
@@ -885,7 +932,7 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
         add_pdl(attr, nattr);
         cfg.attrs = attr;
         cfg.numAttrs = nattr;
-        ProfScope ps_("du_fused", st);
+        ProfScope ps_(which == 3 ? "du_fused" : which == 1 ? "du_dU1db" : "du_dU2", st);
         SKL_CUDA(cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a));
         return SKL_OK;
     }
@@ -907,7 +954,7 @@ skl_status run_du(const SklDims& d, int64_t T, int kind, int which, const void* 
     attr[1].val.cooperative = a.coop;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    ProfScope ps_("du_fused", st);
+    ProfScope ps_(which == 3 ? "du_fused" : which == 1 ? "du_dU1db" : "du_dU2", st);
     cudaError_t le = cudaLaunchKernelEx(&cfg, du_kern, ta0, tb0, ta1, tb1, a);
     if (le != cudaSuccess && a.coop) {  // cooperative + cluster refused: last-CTA reduction instead
         (void)cudaGetLastError();

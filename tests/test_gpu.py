@@ -270,6 +270,55 @@ def test_phased_backward_matches_oracle(skl, port, dtype_name):
     check_close("db(phased)", _np(db), rgb, dtype_name)
 
 
+@pytest.mark.parametrize("reserved", [0, 8])
+def test_phased_backward_full_c2_matches_fused(skl, reserved):
+    """At the bench's full c2 size (T = 32768) the phased launches take other
+    dU tilings than the fused one (dU1-only: 12 tiles, cooperative reduction
+    when clusters of 2S CTAs do not all fit; dU2-only: 3 tiles, S = 23-24):
+    grad_x is the same kernel (bitwise), the fp32 gradients differ only by the
+    order of the split partial sums."""
+    d_in, d_out, L, k, T = 768, 3072, 2, 128, 32768
+    s = skl.shape(d_in, d_out, L, k, skl.BF16)
+    bf = torch.bfloat16
+    S1s = torch.empty(L, d_in, k, dtype=bf, device="cuda")
+    S2s = torch.empty(L, k, d_out, dtype=bf, device="cuda")
+    U1s = torch.empty(L, k, d_out, dtype=bf, device="cuda")
+    U2s = torch.empty(L, d_in, k, dtype=bf, device="cuda")
+    skl.generate_sketches(s, skl.GAUSSIAN, 5, S1s, S2s)
+    skl.init_params(s, 5, U1s, U2s)
+    gen = torch.Generator(device="cuda")
+    gen.manual_seed(3)
+    X = torch.randn(T, d_in, device="cuda", generator=gen).to(bf)
+    G = torch.randn(T, d_out, device="cuda", generator=gen).to(bf)
+    B = torch.zeros(d_out, dtype=bf, device="cuda")
+    y = torch.empty(T, d_out, dtype=bf, device="cuda")
+    saved = torch.empty(L * k, T, dtype=bf, device="cuda")
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, saved, ws)
+    outs = []
+    for phased in (False, True):
+        gx = torch.empty(T, d_in, dtype=bf, device="cuda")
+        du1 = torch.empty(L, k, d_out, device="cuda")
+        du2 = torch.empty(L, d_in, k, device="cuda")
+        db = torch.empty(d_out, device="cuda")
+        skl.set_reserved_sms(reserved if phased else 0)
+        try:
+            if phased:
+                skl.backward_phase(s, skl.BWD_DU1_DB, G, X, saved, S1s, S2s, U1s, U2s, None, du1, None, db, ws)
+                skl.backward_phase(s, skl.BWD_DX_DU2, G, X, saved, S1s, S2s, U1s, U2s, gx, None, du2, None, ws)
+            else:
+                skl.backward(s, G, X, saved, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+            torch.cuda.synchronize()
+        finally:
+            skl.set_reserved_sms(0)
+        outs.append((gx, du1, du2, db))
+    (gx0, a0, b0, c0), (gx1, a1, b1, c1) = outs
+    assert torch.equal(gx0, gx1)
+    for name, u, v in (("dU1s", a0, a1), ("dU2s", b0, b1), ("db", c0, c1)):
+        rel = float((u - v).norm() / v.norm())
+        assert rel <= 1e-5, f"{name}: phased vs fused rel_fro {rel:.2e}"
+
+
 def test_dp_overlapped_step_over_nccl(skl, port):
     """The DP schedule bench.py runs at N > 1 (dp.backward_overlapped: async
     NCCL all-reduce of dU1s|db issued before the dX kernel), on a world-1 NCCL
