@@ -624,7 +624,10 @@ DuShape du_shape(const SklDims& d, int64_t T, int sms, int kind, int which = 3) 
     // shapes take the cooperative reduction at the same split instead: c2's
     // DP-phased dU1-only launch (12 tiles, S = 6) 80 us as clusters of 12,
     // 71 us at S = 4 in clusters of 8, 55-66 us cooperative at S = 6.
-    if (s.cr && !getenv("SKL_DU_SPLITS") && s.tiles() > du_cluster_cap(kind, 2 * sc)) s.cr = false;
+    // (Several-wave shapes, more tiles than pairs, keep their clusters: they run
+    // in waves whatever the reduction.)
+    if (s.cr && !getenv("SKL_DU_SPLITS") && s.tiles() <= pairs && s.tiles() > du_cluster_cap(kind, 2 * sc))
+        s.cr = false;
     return s;
 }
 
