@@ -42,6 +42,7 @@
 #pragma once
 
 #include "sm100.cuh"
+#include "trace.cuh"
 
 #ifndef SKL_FWD_BIAS_TAB
 #define SKL_FWD_BIAS_TAB 1  // 0 measured: 96 -> 106 us at c2 (per-tile bias loads cost more than the 6th stage)
@@ -72,6 +73,7 @@ struct B2BArgs {
     const uint32_t* mask_bits;   // backward: out *= bit, instead of reading `mask`
     long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
     int l2hint;                  // L2 cache-hint policy bits for the producer's TMA loads
+    int save_tma;                // saved columns leave through TMA stores (tmS) in 64-column boxes
 };
 
 namespace dev {
@@ -169,7 +171,7 @@ __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
-               const __grid_constant__ CUtensorMap tmM, B2BArgs args) {
+               const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmS, B2BArgs args) {
     using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -230,6 +232,7 @@ __global__ void __launch_bounds__(384, 1)
             mbar_init(&sfree[i], 4);          // the 4 receiver warps of the next pair's group
         }
         if constexpr (C::kMaskStage) prefetch_tmap(&tmM);
+        if (args.save_tma) prefetch_tmap(&tmS);
         fence_barrier_init();
     }
     if (warp == 2) {
@@ -261,6 +264,7 @@ __global__ void __launch_bounds__(384, 1)
     if (warp == 0) {
         // ---------------------------------------------------------------- producer
         if (elect_one()) {
+            Tr tr(0);
             int stage = 0;
             uint32_t phase = 0;
             // activations (x / G) stream through L2 once; the weight panels are re-read by every tile
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(384, 1)
                     for (int c = c_lo; c < c_hi; ++c) bytes += (min(256, r_loc - 256 * c) / kCG) * 128;
                     for (int kb = 0; kb < nkb1; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
+                        tr(1);
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], bytes * kCG);
                         else mbar_arrive_cluster(&full[stage], lead);
@@ -320,6 +325,7 @@ __global__ void __launch_bounds__(384, 1)
                         const int kb0 = s * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
                         mbar_wait(&empty[stage], phase ^ 1);
+                        tr(2);
                         uint8_t* st = smem + stage * C::kStageBytes;
                         if (leader) mbar_arrive_expect_tx(&full[stage], (uint32_t)(nk * C::kB2KbBytes * kCG));
                         else mbar_arrive_cluster(&full[stage], lead);
@@ -352,6 +358,7 @@ __global__ void __launch_bounds__(384, 1)
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer
         if (leader && elect_one()) {
+            Tr tr(1);
             int stage = 0;
             uint32_t phase = 0;
             auto next = [&]() { if (++stage == C::kStages) { stage = 0; phase ^= 1; } };
@@ -367,9 +374,11 @@ __global__ void __launch_bounds__(384, 1)
                         for (int u = 0; u < 2; ++u, ++slot_seq)
                             mbar_wait(&tempty2[slot_seq & 1], ((slot_seq >> 1) & 1) ^ 1);
                         tc_fence_after();
+                        tr(10);
                     }
                     for (int kb = 0; kb < nkb1; ++kb) {
                         mbar_wait(&full[stage], phase);
+                        tr(11);
                         tc_fence_after();
                         const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int c = c_lo; c < c_hi; ++c) {
@@ -395,12 +404,14 @@ __global__ void __launch_bounds__(384, 1)
                 for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                     const uint32_t s = slot_seq & 1;
                     mbar_wait(&tempty2[s], ((slot_seq >> 1) & 1) ^ 1);
+                    tr(13);
                     tc_fence_after();
                     const uint32_t d = tmem_base + 256 + 128 * s;
                     for (int st2 = 0; st2 < nst2; ++st2) {
                         const int kb0 = st2 * C::kKbPerStage2;
                         const int nk = min(C::kKbPerStage2, nkb2 - kb0);
                         mbar_wait(&full[stage], phase);
+                        tr(14);
                         tc_fence_after();
                         const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
                         for (int q = 0; q < nk; ++q) {
@@ -426,6 +437,7 @@ __global__ void __launch_bounds__(384, 1)
                 // ---- wait for the bf16 H of this tile (both CTAs)
                 if (pp) mbar_wait(&hready[it & 1], (it >> 1) & 1);
                 else for (int c = 0; c < nch; ++c) mbar_wait(&hready[c], it & 1);
+                tr(12);
                 tc_fence_after();
                 issue_g2(pp ? 128u * (it & 1) : 0u);
             }
@@ -444,6 +456,7 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t slot_seq = 0;
         uint32_t tf_par0 = 0, tf_par1 = 0;
         uint32_t xch = 0;                     // kRS: partial hand-offs of this group so far
+        Tr tr((lane == 0 && wg == 0 && (q == 0 || q == 3)) ? 2 + (q == 3 ? 1 : 0) : -1);
         const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
         uint8_t* buf = stage_out + wg * C::kOutBytes;  // this group's output staging buffer
         uint8_t* mbuf = mask_s + wg * C::kOutBytes;    // kMask: this group's mask tile (same layout as buf)
@@ -493,13 +506,25 @@ __global__ void __launch_bounds__(384, 1)
         int cur_t = 0;
         // Saved columns go out TRANSPOSED, save[c - save_col0][t] (row stride
         // ld_save = round8(T)): the token-reduction GEMMs then read them K-major.
-        // The warp's [32 tokens x 16 cols] block is transposed through a 1 KB smem
-        // scratch so every lane writes two 16-B chunks (8 tokens of one column)
-        // instead of 16 scattered 2-B stores (8 % of the kernel).  `col` is the
-        // global rank index (r_off + the pair-local column).
+        // Each warp owns a 4 KB slice of the group's staging buffer (its 32
+        // tokens).  `col` is the global rank index (r_off + the pair-local column).
+        uint8_t* wbuf = buf + q * 4096;
+        bool save_pend = false;  // this warp's TMA save store may still be reading wbuf
+        auto reclaim_wbuf = [&]() {  // before wbuf is written again
+            if (save_pend) {
+                if (lane == 0) bulk_wait_read<0>();
+                __syncwarp();
+                save_pend = false;
+            }
+        };
+        // Fallback (columns straddling the save window, TF32-free shapes whose
+        // quarters are not 64 wide): the warp's [32 tokens x 16 cols] block is
+        // transposed through wbuf so every lane writes two 16-B chunks (8 tokens
+        // of one column) instead of 16 scattered 2-B stores.
         auto save_cols16 = [&](const uint32_t (&p)[8], int col) {
+            reclaim_wbuf();
             const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(p);
-            __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(buf + q * 1024);  // [16 cols][32 tokens]
+            __nv_bfloat16* scr = reinterpret_cast<__nv_bfloat16*>(wbuf);  // [16 cols][32 tokens]
 #pragma unroll
             for (int i = 0; i < 16; ++i) scr[i * 32 + lane] = pb[i];
             __syncwarp();
@@ -515,6 +540,37 @@ __global__ void __launch_bounds__(384, 1)
                 }
             }
             __syncwarp();
+        };
+        // TMA route (bf16, 64-column quarters inside the save window): the warp
+        // stages its [64 cols][32 tokens] block in wbuf (64-B rows; lane pairs
+        // swap halves so each lane stores two tokens of one column, even lanes
+        // filling one row and odd lanes the next: 128 B per store, no bank
+        // conflict) and lane 0 issues one TMA store of it.  The async engine then
+        // does the strided writes the threads did one 16-B chunk at a time
+        // (3.8k cycles per tile of the 768x768 projection, 7k of the c2 backward).
+        auto quarter_tma = [&](int col, int W) -> bool {
+            return kKind == 0 && args.save_tma && W == 64 && col >= args.save_col0 &&
+                   col + 64 <= args.save_col0 + args.save_cols;
+        };
+        auto stage16 = [&](const uint32_t (&p)[8], int j) {  // columns [16j, 16j + 16) of the quarter
+            const bool odd = lane & 1u;
+            const uint32_t a = smem_u32(wbuf) + (uint32_t)(16 * j + (odd ? 1 : 0)) * 64u + (lane & ~1u) * 2u;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const uint32_t x = __shfl_xor_sync(0xffffffffu, p[i], 1);
+                // even lane: column 2i of tokens (lane, lane+1); odd lane: column 2i+1 of (lane-1, lane)
+                const uint32_t w = odd ? ((x >> 16) | (p[i] & 0xFFFF0000u)) : ((p[i] & 0xFFFFu) | (x << 16));
+                asm volatile("st.shared.b32 [%0], %1;" ::"r"(a + (uint32_t)(2 * i) * 64u), "r"(w));
+            }
+        };
+        auto flush_quarter = [&](int col) {  // the warp staged its 32 rows of the quarter
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) {
+                tma_store_2d(&tmS, wbuf, cur_t * tile_rows + (int)rank * 128 + (int)q * 32, col - args.save_col0);
+                bulk_commit();
+            }
+            save_pend = true;
         };
         // kRS: add the running partial of the previous pair (if any) to this
         // group's 32 accumulator columns `r`, then pass the sum to the next pair
@@ -574,6 +630,7 @@ __global__ void __launch_bounds__(384, 1)
                 const int hb = pp ? (int)(it & 1) : c;            // tfull1 / hready index
                 const uint32_t hoff = pp ? 128u * (it & 1) : 0u;  // TMEM column of this tile's H
                 mbar_wait(&tfull1[hb], pp ? ((it >> 1) & 1) : (it & 1));
+                tr(21);
                 tc_fence_after();
                 if constexpr (kKind == 1) {
                     // TF32: H stays one fp32 word per column; round in place with
@@ -607,6 +664,8 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
                 for (int rd = 0; rd < 2; ++rd) {
                     const int qi = 2 * rd + (int)wg;
+                    const bool qt = args.save && !defer_save && quarter_tma(r_off + 256 * c + qi * W, W);
+                    if (qt) reclaim_wbuf();
                     uint32_t rr[4][16];
 #pragma unroll
                     for (int g = 0; g < 4; ++g)
@@ -628,16 +687,20 @@ __global__ void __launch_bounds__(384, 1)
                         const int cl = qi * W + 16 * g;  // chunk-local fp32 column
                         tmem_st8(tmem_base + lane_base + hoff + 128 * c + cl / 2, p);
                         const int col = r_off + 256 * c + cl;  // H column (global R order)
-                        if (args.save && !defer_save && col + 16 > args.save_col0 &&
-                            col < args.save_col0 + args.save_cols)
+                        if (qt)
+                            stage16(p, g);
+                        else if (args.save && !defer_save && col + 16 > args.save_col0 &&
+                                 col < args.save_col0 + args.save_cols)
                             save_cols16(p, col);
                     }
+                    if (qt) flush_quarter(r_off + 256 * c + qi * W);
                 }
                 }  // bf16 conversion
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
+                    tr(22);
                     arrive_leader(&hready[hb]);
                     if (c == 1) {  // release the two slots chunk 1 overlaid
                         arrive_leader(&tempty2[slot_seq & 1]);
@@ -654,6 +717,24 @@ __global__ void __launch_bounds__(384, 1)
 #pragma unroll 1
                     for (int rd = 0; rd < 2; ++rd) {
                         const int qi = 2 * rd + (int)wg;
+                        const int qcol = r_off + 256 * c + qi * W;
+                        if (!(qcol + W > args.save_col0 && qcol < args.save_col0 + args.save_cols)) continue;
+                        tr(27);
+                        if (quarter_tma(qcol, W)) {
+                            reclaim_wbuf();
+                            uint32_t pq[4][8];
+#pragma unroll
+                            for (int g = 0; g < 4; ++g)
+                                tmem_ld8(tmem_base + lane_base + (pp ? 128u * (it & 1) : 0u) + 128 * c + (qi * W + 16 * g) / 2, pq[g]);
+                            tmem_ld_wait();
+                            tr(28);
+#pragma unroll
+                            for (int g = 0; g < 4; ++g) stage16(pq[g], g);
+                            tr(29);
+                            flush_quarter(qcol);
+                            tr(30);
+                            continue;
+                        }
 #pragma unroll 1
                         for (int g = 0; g < 4 && 16 * g < W; ++g) {
                             const int cl = qi * W + 16 * g, col = r_off + 256 * c + cl;
@@ -666,6 +747,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             }
+            tr(23);
             // ---- GEMM2 output tiles: this group's 64 columns of every 128-wide tile
             for (int j = 0; j < n2_tiles; ++j, ++slot_seq) {
                 const uint32_t s = slot_seq & 1;
@@ -680,12 +762,14 @@ __global__ void __launch_bounds__(384, 1)
                 // acquisitions never commit it), so count its phases per slot.
                 mbar_wait(&tfull2[s], s ? tf_par1 : tf_par0);
                 if (s) tf_par1 ^= 1u; else tf_par0 ^= 1u;
+                tr(24);
                 tc_fence_after();
                 if (!C::kBiasTab && srow < 64) bias_g[s * 64 + srow] = bval;  // published by the barrier below
                 uint32_t ra[32], rb[32];
                 tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg, ra);
                 tmem_ld32(tmem_base + lane_base + 256 + 128 * s + 64 * wg + 32, rb);
                 tmem_ld_wait();
+                tr(31);
                 // every TMEM read of this slot by this warp has completed
                 tc_fence_before();
                 __syncwarp();
@@ -703,8 +787,11 @@ __global__ void __launch_bounds__(384, 1)
                     if (j + 1 < n2_tiles) mbits_next = load_bits(j + 1);
                 }
                 uint32_t bo0 = 0u, bo1 = 0u;  // use_bits_out: this row's bits of the group's 64 columns
-                if (issuer) bulk_wait_read<0>();  // our previous store has read `buf`
+                if (issuer || (save_pend && lane == 0)) bulk_wait_read<0>();  // our previous stores have read `buf`
+                save_pend = false;
+                tr(25);
                 named_bar_sync(1 + wg, 128);
+                tr(32);
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
                 const uint32_t mrow_addr = smem_u32(mbuf) + srow * 128;
                 if (use_mask) {
@@ -819,11 +906,14 @@ __global__ void __launch_bounds__(384, 1)
                 if (use_bits_out && row_ok && n0 < args.N2)
                     *reinterpret_cast<uint2*>(args.relu_bits + (long long)row * args.bits_ld + n0 / 32) =
                         make_uint2(bo0, bo1);
+                tr(33);
                 fence_proxy_async_smem();
                 named_bar_sync(1 + wg, 128);
+                tr(34);
                 if (issuer) {
                     tma_store_2d(&tmY, buf, n0, t * tile_rows + (int)rank * 128);
                     bulk_commit();
+                    tr(26);
                 }
                 if (use_mask && issuer && j + 1 < n2_tiles) issue_mask(t, j + 1);  // mbuf was read by all
             }

@@ -124,6 +124,12 @@ skl_status make_tmap(CUtensorMap* m, const void* ptr, int elem_bytes, int64_t in
     return SKL_OK;
 }
 
+// Saved columns of the fused kernels through TMA stores (SKL_SAVE_TMA=0: per-thread 16-B stores).
+bool save_tma_enabled() {
+    static const bool on = !(getenv("SKL_SAVE_TMA") && atoi(getenv("SKL_SAVE_TMA")) == 0);
+    return on;
+}
+
 // Programmatic dependent launch on the fused / GEMM kernels (SKL_PDL=0 disables).
 bool pdl_enabled() {
     static const bool on = !(getenv("SKL_PDL") && atoi(getenv("SKL_PDL")) == 0);
@@ -224,7 +230,7 @@ template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false, bool k
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     constexpr int eb = C::kElem, bk = C::kBK;
-    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm;
+    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm, ts;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
     if constexpr (kMode == 0) {
         SKL_TRY(make_tmap(&tb1, src.b1, eb, a.K1, a.R_pad, a.K1, bk, a.b1rows));
@@ -247,6 +253,14 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     SKL_TRY(make_tmap(&ty, a.out, eb, a.N2, a.T, a.ldo, bk, 128));
     tm = ty;
     if (C::kMaskStage && a.mask) SKL_TRY(make_tmap(&tm, a.mask, eb, a.N2, a.T, a.ld_mask, bk, 128));  // output-tile boxes
+    // saved columns (bf16): [save_cols][ld_save] tokens-contiguous, stored per warp in [64 cols][32 tokens] boxes
+    ts = ty;
+    a.save_tma = 0;
+    if (kKind == 0 && a.save && a.save_cols >= 64 && (reinterpret_cast<uintptr_t>(a.save) & 15) == 0 &&
+        ((a.ld_save * 2) & 15) == 0 && save_tma_enabled()) {
+        SKL_TRY(make_tmap(&ts, a.save, 2, a.ld_save, a.save_cols, a.ld_save, 32, 64, CU_TENSOR_MAP_SWIZZLE_NONE));
+        a.save_tma = 1;
+    }
     const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
     const int csize = kCG * (kRS ? a.nsplit : 1);  // CTAs per cluster
     auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS, kSP>;
@@ -276,7 +290,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     add_pdl(attr, nattr);
     cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, tm, a));
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, tm, ts, a));
     return SKL_OK;
 }
 
@@ -1845,6 +1859,21 @@ skl_status skl_profile_enable(int on) {
 }
 
 int skl_profile_collect(skl_profile_entry* out, int max_entries) { return skl::prof_collect(out, max_entries); }
+
+#ifdef SKL_TRACE
+// Trace builds only (-DSKL_TRACE=1, csrc/trace.cuh; not in include/skl.h): copy out / clear
+// the per-role event table [slot][role][event](clock64, code).
+static constexpr int kTraceWords = skl::dev::kTraceSlots * skl::dev::kTraceRoles * 2 * skl::dev::kTraceEvents;
+int skl_trace_dump(uint64_t* out, int max_words) {
+    if (max_words < kTraceWords) return -kTraceWords;
+    cudaDeviceSynchronize();
+    return cudaMemcpyFromSymbol(out, skl::dev::g_trace, kTraceWords * 8) == cudaSuccess ? kTraceWords : 0;
+}
+int skl_trace_reset(void) {
+    static unsigned long long zero[kTraceWords];
+    return cudaMemcpyToSymbol(skl::dev::g_trace, zero, kTraceWords * 8) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // ---------------------------------------------------------------- NCCL
 typedef int (*nccl_allreduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t);

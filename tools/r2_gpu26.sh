@@ -1,0 +1,7 @@
+# Traced timelines of the c5 projection layer (fwd, bwd) and the FFN1 (c2) layer forward.
+export PATH=/usr/local/cuda/bin:$PATH
+mkdir -p gpurun_out
+for a in "768 768 1 128 32768 fwd" "768 768 1 128 32768 bwd" "768 3072 2 128 32768 fwd" "768 3072 2 128 32768 bwd"; do
+  echo "=== $a"; SKL_LIB=scratch/libskl.so timeout 120 python tools/trace_b2b.py $a
+done > gpurun_out/trace26.txt 2>&1
+tail -c 1500 gpurun_out/trace26.txt
