@@ -74,6 +74,7 @@ struct B2BArgs {
     long long bits_ld;           // words per row (even: 64-column groups are 8-B aligned)
     int l2hint;                  // L2 cache-hint policy bits for the producer's TMA loads
     int save_tma;                // saved columns leave through TMA stores (tmS) in 64-column boxes
+    int wstore;                  // per-warp output stores allowed (tmYw)
 };
 
 namespace dev {
@@ -171,7 +172,8 @@ __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
-               const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmS, B2BArgs args) {
+               const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmS,
+               const __grid_constant__ CUtensorMap tmYw, B2BArgs args) {
     using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
@@ -218,6 +220,7 @@ __global__ void __launch_bounds__(384, 1)
             prefetch_tmap(&tmB2b);
         }
         prefetch_tmap(&tmY);
+        if constexpr (kKind == 0) prefetch_tmap(&tmYw);
         for (int s = 0; s < C::kStages; ++s) {
             mbar_init(&full[s], kCG);
             mbar_init(&empty[s], 1);
@@ -458,12 +461,20 @@ __global__ void __launch_bounds__(384, 1)
         uint32_t xch = 0;                     // kRS: partial hand-offs of this group so far
         Tr tr((lane == 0 && wg == 0 && (q == 0 || q == 3)) ? 2 + (q == 3 ? 1 : 0) : -1);
         const bool issuer = (q == 0 && lane == 0);  // per group: issues / waits its bulk stores
+        // Per-warp output stores (bf16, no fused mask, bias resident or absent): each
+        // warp writes its 32 rows of the output tile with its own TMA store and
+        // waits only for its own previous store, so the two group barriers per
+        // output tile go away (the 768x768 projection's GEMM2 is epilogue-bound).
+        // Otherwise the group shares one store per tile (staged bias / mask tiles
+        // are published by the group barrier).
         uint8_t* buf = stage_out + wg * C::kOutBytes;  // this group's output staging buffer
         uint8_t* mbuf = mask_s + wg * C::kOutBytes;    // kMask: this group's mask tile (same layout as buf)
         uint32_t mph = 0;
         const bool use_mask = C::kMaskStage && args.mask != nullptr;
         const bool use_bits_in = kPost == 2 && args.mask_bits != nullptr;
         const bool use_bits_out = kPost == 2 && args.relu_bits != nullptr;
+        const bool wstore = kKind == 0 && args.wstore && !use_mask && (C::kBiasTab || args.bias == nullptr);
+        const bool storer = wstore ? lane == 0 : issuer;  // threads that own bulk stores
         uint2 mbits = make_uint2(0u, 0u), mbits_next = make_uint2(0u, 0u);
         // mask tile of output tile (t, j) for this group's 64 columns -> mbuf (issuer only)
         auto issue_mask = [&](int t_, int j_) {
@@ -658,7 +669,7 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 } else {
                 if (args.save && !defer_save) {  // buf doubles as the transpose scratch: the last store must have left it
-                    if (issuer) bulk_wait_read<0>();
+                    if (storer) bulk_wait_read<0>();
                     named_bar_sync(1 + wg, 128);
                 }
 #pragma unroll 1
@@ -710,7 +721,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (c == 1) slot_seq += 2;
             }
             if (defer_save && args.save) {  // saved columns from the bf16 H, under the first GEMM2 MMAs
-                if (issuer) bulk_wait_read<0>();  // buf is the transpose scratch
+                if (storer) bulk_wait_read<0>();  // buf is the transpose scratch
                 named_bar_sync(1 + wg, 128);
                 for (int c = 0; c < nch; ++c) {
                     const int W = min(256, r_loc - 256 * c) / 4;
@@ -787,10 +798,11 @@ __global__ void __launch_bounds__(384, 1)
                     if (j + 1 < n2_tiles) mbits_next = load_bits(j + 1);
                 }
                 uint32_t bo0 = 0u, bo1 = 0u;  // use_bits_out: this row's bits of the group's 64 columns
-                if (issuer || (save_pend && lane == 0)) bulk_wait_read<0>();  // our previous stores have read `buf`
+                if (storer || (save_pend && lane == 0)) bulk_wait_read<0>();  // our previous stores have read `buf`
                 save_pend = false;
                 tr(25);
-                named_bar_sync(1 + wg, 128);
+                if (wstore) __syncwarp();
+                else named_bar_sync(1 + wg, 128);
                 tr(32);
                 const uint32_t row_addr = smem_u32(buf) + srow * 128;
                 const uint32_t mrow_addr = smem_u32(mbuf) + srow * 128;
@@ -861,9 +873,13 @@ __global__ void __launch_bounds__(384, 1)
                 }
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
+                    // (per-warp stores without the bias table means no bias: the group
+                    // barrier that publishes bias_g is gone, so it is not read)
                     const float4* bp = C::kBiasTab ? reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)
                                                   : reinterpret_cast<const float4*>(bias_g + s * 64 + 8 * c);
-                    const float4 b0 = bp[0], b1 = bp[1];
+                    const float4 zero4 = make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float4 b0 = (!C::kBiasTab && wstore) ? zero4 : bp[0];
+                    const float4 b1 = (!C::kBiasTab && wstore) ? zero4 : bp[1];
                     const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
                     const uint32_t* src = (c < 4) ? ra : rb;
                     const int o = (c & 3) * 8;
@@ -908,6 +924,15 @@ __global__ void __launch_bounds__(384, 1)
                         make_uint2(bo0, bo1);
                 tr(33);
                 fence_proxy_async_smem();
+                if (wstore) {
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmYw, buf + q * 4096, n0, t * tile_rows + (int)rank * 128 + (int)q * 32);
+                        bulk_commit();
+                    }
+                    tr(26);
+                    continue;
+                }
                 named_bar_sync(1 + wg, 128);
                 tr(34);
                 if (issuer) {
@@ -918,7 +943,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (use_mask && issuer && j + 1 < n2_tiles) issue_mask(t, j + 1);  // mbuf was read by all
             }
         }
-        if (issuer) bulk_wait<0>();
+        if (storer) bulk_wait<0>();
     }
 
     tc_fence_before();

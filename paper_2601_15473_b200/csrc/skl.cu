@@ -230,7 +230,7 @@ template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false, bool k
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
     using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
     constexpr int eb = C::kElem, bk = C::kBK;
-    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm, ts;
+    CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm, ts, tyw;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
     if constexpr (kMode == 0) {
         SKL_TRY(make_tmap(&tb1, src.b1, eb, a.K1, a.R_pad, a.K1, bk, a.b1rows));
@@ -251,6 +251,10 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         SKL_TRY(make_tmap(&tb2b, src.b2b, 2, a.k, srows, a.k, 64, C::kB2Rows));
     }
     SKL_TRY(make_tmap(&ty, a.out, eb, a.N2, a.T, a.ldo, bk, 128));
+    tyw = ty;
+    static const int wstore_env = getenv("SKL_B2B_WSTORE") ? atoi(getenv("SKL_B2B_WSTORE")) : 1;
+    a.wstore = kKind == 0 && wstore_env;
+    if (a.wstore) SKL_TRY(make_tmap(&tyw, a.out, eb, a.N2, a.T, a.ldo, bk, 32));  // per-warp output stores
     tm = ty;
     if (C::kMaskStage && a.mask) SKL_TRY(make_tmap(&tm, a.mask, eb, a.N2, a.T, a.ld_mask, bk, 128));  // output-tile boxes
     // saved columns (bf16): [save_cols][ld_save] tokens-contiguous, stored per warp in [64 cols][32 tokens] boxes
@@ -290,7 +294,7 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
     add_pdl(attr, nattr);
     cfg.numAttrs = nattr;
     ProfScope ps_(name, st);
-    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, tm, ts, a));
+    SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb1, tb1b, tb2, tb2b, ty, tm, ts, tyw, a));
     return SKL_OK;
 }
 
