@@ -30,6 +30,7 @@
 #pragma once
 
 #include "sm100.cuh"
+#include "trace.cuh"
 
 namespace skl {
 
@@ -205,6 +206,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0) {
         // ------------------------------------------------------------ producer (both CTAs, own half)
         if (elect_one()) {
+            Tr tr(0, 4);
             int stage = 0;
             uint32_t phase = 0;
             // A (Savedᵀ / P_S2ᵀ) is re-read by every N tile of the same split; B (G / X) once
@@ -219,6 +221,7 @@ __global__ void __launch_bounds__(256, 1)
                 const int m0 = x.mt * 256 + (int)rank * 128, n0 = x.nt * 256 + (int)rank * 128;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    tr(1);
                     uint8_t* a_dst = sA + stage * kDuABytes;
                     uint8_t* b_dst = sB + stage * kDuBBytes;
                     const int k0 = kb * KT::kBK;
@@ -245,6 +248,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ------------------------------------------------------------ MMA issuer (leader)
         if (leader && elect_one()) {
+            Tr tr(1, 4);
             constexpr uint32_t idesc = make_idesc(kKind, 256, kDuBN, 0, 1);
             int stage = 0;
             uint32_t phase = 0;
@@ -253,10 +257,12 @@ __global__ void __launch_bounds__(256, 1)
                 const Unit x = decode(u);
                 const int acc = iter & 1;
                 mbar_wait(&tempty[acc], ((iter >> 1) & 1) ^ 1);
+                tr(12);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * kDuBN;
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    tr(11);
                     tc_fence_after();
                     const uint32_t a_addr = smem_u32(sA + stage * kDuABytes);
                     const uint32_t b_addr = smem_u32(sB + stage * kDuBBytes);
@@ -292,6 +298,7 @@ __global__ void __launch_bounds__(256, 1)
         // ------------------------------------------------------------ epilogue warps (colsum + partials + reduce)
         const uint32_t q = warp & 3;
         const int t = (int)(q * 32 + lane);  // 0..127
+        Tr tr((lane == 0 && warp == 4) ? 2 : -1, 4);
         int stage = 0;
         uint32_t phase = 0;
         uint32_t red_phase = 0;
@@ -357,6 +364,7 @@ __global__ void __launch_bounds__(256, 1)
             // ---- accumulator -> fp32 partial [tile][split][256][256], our 128 rows
             const int acc = iter & 1;
             mbar_wait(&tfull[acc], (iter >> 1) & 1);
+            tr(21);
             tc_fence_after();
             if (args.cr) {
                 // accumulator -> this CTA's smem (the operand ring is idle now); the
@@ -382,6 +390,7 @@ __global__ void __launch_bounds__(256, 1)
                     if (leader) mbar_arrive(&tempty[acc]);
                     else mbar_arrive_cluster(&tempty[acc], lead_cta);
                 }
+                tr(22);
                 continue;
             }
             {
@@ -557,6 +566,8 @@ __global__ void __launch_bounds__(256, 1)
         }
         tc_fence_before();
         cluster_sync();
+        Tr trr((threadIdx.x == 128) ? 3 : -1, 4);
+        trr(23);
         const DuTail d = *tail;  // registers: the output stores must not force reloads
         const int S = d.S, rows = max(0, min(d.rows, d.valid - d.r0));  // slice rows inside M
         float* cs = cr_part + 136 * kDuBN;  // past S * ceil(128 / S) <= 135 slice rows (S <= 8)
@@ -571,6 +582,7 @@ __global__ void __launch_bounds__(256, 1)
             }
         }
         mbar_wait(rbar, 0);
+        trr(24);
         // element (slice row r, column c) of split q2: row q2 * rows + r, chunk (c/4) ^ ((r0 + r) & 7)
         if (d.ns == 1) {
             // row-contiguous output (dU1): lanes over 4-column chunks, float4 stores
@@ -580,19 +592,14 @@ __global__ void __launch_bounds__(256, 1)
                 const int m = d.m0 + r, n = d.n0 + j * 4;
                 if (m >= d.M || n >= d.N) continue;
                 const float* src = cr_part + r * kDuBN + ((j ^ ((d.r0 + r) & 7)) << 2);
-                float4 v[4];  // up to 4 partial loads in flight, then the ordered sum (split 0, 1, ...)
+                float4 v[8];  // up to 8 partial loads in flight, then the ordered sum (split 0, 1, ...)
 #pragma unroll
-                for (int q2 = 0; q2 < 4; ++q2)
+                for (int q2 = 0; q2 < 8; ++q2)
                     if (q2 < S) v[q2] = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
                 float4 a = v[0];
 #pragma unroll
-                for (int q2 = 1; q2 < 4; ++q2)
+                for (int q2 = 1; q2 < 8; ++q2)
                     if (q2 < S) { a.x += v[q2].x; a.y += v[q2].y; a.z += v[q2].z; a.w += v[q2].w; }
-#pragma unroll 1
-                for (int q2 = 4; q2 < S; ++q2) {  // SKL_DU_CR_MAX > 4
-                    const float4 w = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
-                    a.x += w.x; a.y += w.y; a.z += w.z; a.w += w.w;
-                }
                 const long long mo = d.mb >= d.M ? (long long)m * d.ms
                                                  : (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms;
                 float* o = d.out + mo + n;
@@ -615,12 +622,14 @@ __global__ void __launch_bounds__(256, 1)
                     const int m = d.m0 + r;
                     if (m >= d.M) break;
                     const float* src = cr_part + r * kDuBN + ((j ^ ((d.r0 + r) & 7)) << 2);
-                    float4 a = *reinterpret_cast<const float4*>(src);
-#pragma unroll 1
-                    for (int q2 = 1; q2 < S; ++q2) {
-                        const float4 v = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
-                        a.x += v.x; a.y += v.y; a.z += v.z; a.w += v.w;
-                    }
+                    float4 v[8];  // all partial loads in flight, then the ordered sum
+#pragma unroll
+                    for (int q2 = 0; q2 < 8; ++q2)
+                        if (q2 < S) v[q2] = *reinterpret_cast<const float4*>(src + q2 * rows * kDuBN);
+                    float4 a = v[0];
+#pragma unroll
+                    for (int q2 = 1; q2 < 8; ++q2)
+                        if (q2 < S) { a.x += v[q2].x; a.y += v[q2].y; a.z += v[q2].z; a.w += v[q2].w; }
                     float* o = d.out + (long long)(m / d.mb) * d.mbs + (long long)(m % d.mb) * d.ms + n * d.ns;
                     const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
@@ -629,6 +638,7 @@ __global__ void __launch_bounds__(256, 1)
                 }
             }
         }
+        trr(25);
         if (d.colsum) {
             for (int c = d.r0 + (int)threadIdx.x; c < d.r0 + d.rows; c += 256) {  // columns: not clamped by M
                 const int n = d.n0 + (int)rank * 128 + c;

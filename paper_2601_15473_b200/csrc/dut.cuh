@@ -20,6 +20,7 @@
 #pragma once
 
 #include "sm100.cuh"
+#include "trace.cuh"
 
 namespace skl {
 
@@ -122,6 +123,7 @@ __global__ void __launch_bounds__(256, 1)
     if (warp == 0) {
         // ---------------------------------------------------------------- producer (own half, own barrier)
         if (elect_one()) {
+            Tr tr(0, 4);
             int stage = 0;
             uint32_t phase = 0;
             const uint64_t pol_a = l2_evict_first();   // G / X: read once
@@ -133,6 +135,7 @@ __global__ void __launch_bounds__(256, 1)
                 const uint32_t bytes = (uint32_t)(x.chunks * kChunkBytes + (args.N_pad / 2) * 128);
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
+                    tr(1);
                     uint8_t* st = smem + stage * SB;
                     const int k0 = kb * kBK;
                     mbar_arrive_expect_tx(&full[stage], bytes);
@@ -165,6 +168,7 @@ __global__ void __launch_bounds__(256, 1)
     } else if (warp == 1) {
         // ---------------------------------------------------------------- MMA issuer (leader)
         if (leader && elect_one()) {
+            Tr tr(1, 4);
             const uint32_t idesc = make_idesc(kKind, 256, args.N_pad, 1, 0);
             int stage = 0;
             uint32_t phase = 0;
@@ -172,9 +176,11 @@ __global__ void __launch_bounds__(256, 1)
             for (int u = pair; u < units; u += npairs, ++iter) {
                 const Unit x = decode(u);
                 mbar_wait(tempty, (iter & 1) ^ 1);
+                tr(12);
                 tc_fence_after();
                 for (int kb = x.kb0; kb < x.kb1; ++kb) {
                     mbar_wait(&full[stage], phase);
+                    tr(11);
                     tc_fence_after();
                     const uint32_t st = smem_u32(smem + stage * SB);
                     const uint32_t b_addr = st;
@@ -200,6 +206,7 @@ __global__ void __launch_bounds__(256, 1)
         // ---------------------------------------------------------------- epilogue (colsum, partials)
         const uint32_t q = warp & 3;
         const int t = (int)(q * 32 + lane);  // 0..127: TMEM lane == A row of this CTA's chunk
+        Tr tr((lane == 0 && warp == 4) ? 2 : -1, 4);
         int stage = 0;
         uint32_t phase = 0;
         int iter = 0;
@@ -267,7 +274,45 @@ __global__ void __launch_bounds__(256, 1)
             }
             // ---- accumulators -> fp32 partials [u][rank][c][row t][N_pad]
             mbar_wait(tfull, iter & 1);
+            tr(21);
             tc_fence_after();
+            const int cbytes = 128 * args.N_pad * 4;  // one chunk's partial: 128 contiguous rows
+            if (u + npairs >= units && 2 * cbytes <= S * SB) {
+                // Last unit of this pair: the operand ring is idle, so each chunk is
+                // staged in smem (row t at t * N_pad, the row's 16-B chunks written
+                // in a lane-rotated order to spread banks) and leaves with ONE bulk
+                // store, double-buffered.  Per-thread 16-B global stores along
+                // 512-B rows ran at ~15 B/cycle (13k cycles for the 768x768
+                // projection's 3 chunks).
+                for (int c = 0; c < x.chunks; ++c) {
+                    uint8_t* buf = smem + (c & 1) * cbytes;
+                    if (c >= 2) {  // the store issued from this buffer two chunks ago has read it
+                        if (t == 0) bulk_wait_read<1>();
+                        named_bar_sync(2, 128);
+                    }
+                    const uint32_t row_s = smem_u32(buf) + (uint32_t)t * args.N_pad * 4;
+                    const uint32_t t_row = tmem_base + ((q * 32u) << 16) + c * args.N_pad;
+                    for (int n = 0; n < args.N_pad; n += 16) {
+                        uint32_t v[16];
+                        tmem_ld16(t_row + n, v);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int j = (i + t) & 3;
+                            st_shared_v4(row_s + (uint32_t)(n + 4 * j) * 4, v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                         v[4 * j + 3]);
+                        }
+                    }
+                    fence_proxy_async_smem();
+                    named_bar_sync(2, 128);
+                    if (t == 0) {
+                        bulk_store_1d(args.part + (((long long)u * 2 + rank) * kDutGroup + c) * 128 * args.N_pad, buf,
+                                      (uint32_t)cbytes);
+                        bulk_commit();
+                    }
+                }
+                if (t == 0) bulk_wait<0>();
+            } else
             for (int c = 0; c < x.chunks; ++c) {
                 float* prow = args.part + ((((long long)u * 2 + rank) * kDutGroup + c) * 128 + t) * args.N_pad;
                 const uint32_t t_row = tmem_base + ((q * 32u) << 16) + c * args.N_pad;
@@ -288,6 +333,7 @@ __global__ void __launch_bounds__(256, 1)
                 if (leader) mbar_arrive(tempty);
                 else mbar_arrive_cluster(tempty, 0);
             }
+            tr(22);
         }
     }
     tc_fence_before();
@@ -301,46 +347,64 @@ __global__ void __launch_bounds__(256, 1)
 // Split reduction of the dut partials: output (problem p, row m, rank column n)
 // = alpha * sum over splits s = 0..S-1 of part[unit(p, g, s)][...] -- in split
 // order, so bitwise reproducible -- scattered into the ABI layout; db likewise
-// from the column-sum partials (unscaled).  A block pass covers whole partial
-// rows: N_pad/4 threads per row, each reading one float4 per split (coalesced
-// 16-B loads along the row, up to 8 splits in flight before the ordered adds).
-__global__ void __launch_bounds__(256) dut_reduce_kernel(DutArgs args) {
+// from the column-sum partials (unscaled).  A block reduces a tile of kRedRows
+// consecutive partial rows: threads read float4s along the rows (coalesced,
+// 8 splits x kRedV float4s in flight), park the sums in smem, then write the
+// output with lanes along whichever index is contiguous in the ABI layout --
+// m for dU1s (out[n][m]), n for dU2s -- so every warp store is one segment.
+constexpr int kRedRows = 16, kRedCols = 32;  // block tile: 16 partial rows x 32 rank columns
+__global__ void __launch_bounds__(128) dut_reduce_kernel(DutArgs args) {
     pdl_wait();
     pdl_launch_dependents();
+    __shared__ float tile_s[kRedRows * (kRedCols + 1)];
+    constexpr int ld = kRedCols + 1;
     const int S = args.splits, Np = args.N_pad;
-    const int tpr = Np / 4;                 // threads per partial row
-    const int rows_per_pass = 256 / tpr;
-    const int tr = (int)threadIdx.x / tpr, n4 = ((int)threadIdx.x % tpr) * 4;
+    const long long ustride = 2LL * kDutGroup * 128 * Np;
+    const int n0 = (int)blockIdx.y * kRedCols;                 // this block's rank columns
+    const int ncols = min(kRedCols, args.N - n0);
+    const int rr_t = (int)threadIdx.x / (kRedCols / 4), c4 = ((int)threadIdx.x % (kRedCols / 4)) * 4;
     for (int p = 0; p < 2; ++p) {
         const DutProblem& P = args.p[p];
-        if (P.groups == 0) continue;
-        const int passes = (P.M + rows_per_pass - 1) / rows_per_pass;
-        for (int pass = blockIdx.x; pass < passes; pass += gridDim.x) {
-            const int m = pass * rows_per_pass + tr;
-            if (m >= P.M || (int)threadIdx.x >= tpr * rows_per_pass) continue;
-            const int g = m / (256 * kDutGroup), mr = m % (256 * kDutGroup);
-            const int c = mr / 256, r = (mr % 256) / 128, row = mr % 128;
-            const long long rowoff = (((long long)r * kDutGroup + c) * 128 + row) * Np + n4;
-            const long long ustride = 2LL * kDutGroup * 128 * Np;
-            const float* base = args.part + (long long)(P.unit0 + g * S) * ustride + rowoff;
-            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int s0 = 0; s0 < S; s0 += 8) {
-                float4 v[8];
+        if (P.groups == 0 || ncols <= 0) continue;
+        const int tiles = (P.M + kRedRows - 1) / kRedRows;
+        for (int tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+            const int m0 = tile * kRedRows;  // kRedRows divides 128: inside one partial half-chunk
+            const int g = m0 / (256 * kDutGroup), mr = m0 % (256 * kDutGroup);
+            const int c = mr / 256, r = (mr % 256) / 128, row0 = mr % 128;
+            // thread: partial row row0 + rr_t, columns n0 + c4 .. + 3 (one float4 per split)
+            if (n0 + c4 < Np) {
+                const float* src = args.part + (long long)(P.unit0 + g * S) * ustride +
+                                   (((long long)r * kDutGroup + c) * 128 + row0 + rr_t) * Np + n0 + c4;
+                float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int s0 = 0; s0 < S; s0 += 16) {
+                    float4 v[16];
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (s0 + i < S) v[i] = __ldcg(reinterpret_cast<const float4*>(base + (long long)(s0 + i) * ustride));
+                    for (int i = 0; i < 16; ++i)
+                        if (s0 + i < S) v[i] = __ldcg(reinterpret_cast<const float4*>(src + (long long)(s0 + i) * ustride));
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-                    if (s0 + i < S) { acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w; }
+                    for (int i = 0; i < 16; ++i)
+                        if (s0 + i < S) { acc.x += v[i].x; acc.y += v[i].y; acc.z += v[i].z; acc.w += v[i].w; }
+                }
+                float* d = tile_s + rr_t * ld + c4;
+                d[0] = acc.x * args.alpha; d[1] = acc.y * args.alpha;
+                d[2] = acc.z * args.alpha; d[3] = acc.w * args.alpha;
             }
-            const float o[4] = {acc.x, acc.y, acc.z, acc.w};
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const int n = n4 + i;
-                if (n < args.N) P.out[(n / P.nb) * P.nbs + (n % P.nb) * P.ns + (long long)m * P.ms] = o[i] * args.alpha;
+            __syncthreads();
+            const int rows = min(kRedRows, P.M - m0);
+            if (P.ms == 1) {  // out[n][m]: lanes along m, kRedRows consecutive floats per column
+                for (int i = (int)threadIdx.x; i < rows * ncols; i += 128) {
+                    const int nl = i / rows, rr = i % rows, n = n0 + nl;
+                    P.out[(n / P.nb) * P.nbs + (n % P.nb) * P.ns + (long long)(m0 + rr)] = tile_s[rr * ld + nl];
+                }
+            } else {          // lanes along n
+                for (int i = (int)threadIdx.x; i < rows * ncols; i += 128) {
+                    const int rr = i / ncols, nl = i % ncols, n = n0 + nl;
+                    P.out[(n / P.nb) * P.nbs + (n % P.nb) * P.ns + (long long)(m0 + rr) * P.ms] = tile_s[rr * ld + nl];
+                }
             }
+            __syncthreads();
         }
-        if (P.colsum && P.db) {
+        if (P.colsum && P.db && blockIdx.y == 0) {
             for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < P.M;
                  m += (long long)gridDim.x * blockDim.x) {
                 const int g = (int)(m / (256 * kDutGroup)), mr = (int)(m % (256 * kDutGroup));

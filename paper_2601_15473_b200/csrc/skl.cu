@@ -862,9 +862,12 @@ skl_status run_dut(const SklDims& d, int64_t T, int kind, int which, const void*
         SKL_CUDA(cudaLaunchKernelEx(&cfg, kern, (which & 1) ? tu1a : tu2a, (which & 1) ? tu1b : tu2b, tu2a, tu2b, a));
     }
     cudaLaunchConfig_t rc = {};
-    const int64_t threads = (int64_t)(d.d_out + d.d_in) * (u.n_pad / 4);  // N_pad/4 threads per partial row
-    rc.gridDim = dim3((unsigned)std::max<int64_t>(sms, std::min<int64_t>(sms * 8, (threads + 255) / 256)));
-    rc.blockDim = dim3(256);
+    // one block per (kRedRows-row tile of the larger problem, kRedCols rank columns); each block
+    // takes that tile of both problems
+    const int64_t red_tiles = (std::max(d.d_out, d.d_in) + dev::kRedRows - 1) / dev::kRedRows;
+    rc.gridDim = dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>(sms * 8, red_tiles)),
+                      (unsigned)((d.Lk + dev::kRedCols - 1) / dev::kRedCols));
+    rc.blockDim = dim3(128);
     rc.stream = st;
     cudaLaunchAttribute rattr[1];
     unsigned nr = 0;

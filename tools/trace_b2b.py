@@ -8,7 +8,10 @@ first event of the CTA).  Codes: producer 1 = G1 stage acquired, 2 = G2 stage;
 MMA 10 = G2 slots acquired for chunk 1, 11 = G1 stage full, 12 = H ready,
 13 = G2 slot free, 14 = G2 stage full; epilogue 21 = G1 chunk accumulated,
 22 = chunk converted, 23 = saves done, 24 = G2 tile accumulated,
-25 = staging buffer free, 26 = tile store issued."""
+25 = staging buffer free, 26 = tile store issued.  Slots 4-7 (SLOTS=4,6) are
+the du kernel: producer 1 = stage acquired; MMA 12 = unit start, 11 = stage
+full; epilogue 21 = accumulator ready, 22 = dumped to smem; tail 23 = after
+the cluster barrier, 24 = partial slices loaded, 25 = reduced and stored."""
 import ctypes
 import os
 import sys
@@ -41,9 +44,9 @@ if which == "fwd":
 else:
     lyr.backward(X, G, saved=sv)
 torch.cuda.synchronize()
-n = 4 * 4 * 2 * 1024
+n = 8 * 4 * 2 * 1024
 buf = (ctypes.c_uint64 * n)()
-assert lib.skl_trace_dump(buf, n) == n
+assert lib.skl_trace_dump(buf, n) == n, lib.skl_trace_dump(buf, n)
 slots = os.environ.get("SLOTS", "0,2").split(",")
 for s in (int(v) for v in slots):
     rows = []
