@@ -511,7 +511,20 @@ bool relu_bits_ok(const SklDims& d, skl_dtype t) {
 struct Plan {
     size_t acat, bcat, acatT, bcatT, bias32, inter, saved, p2t, colsum, total;
     size_t du_part, du_cpart, du_tickets;
+    size_t small_part, small_h;  // small-batch path (small.cu)
 };
+
+// Small-batch path (small.cu): T <= kSmallT tokens and at most ~0.5 GFLOP per
+// forward (2·R·D·T), where one tcgen05 tile on one CTA pair is weight-stream
+// bound (c1: 26 us per fused kernel) -- beyond that the tensor-core kernels win
+// even on a single tile.  SKL_SMALL=0 disables it, =1 forces it for T <= kSmallT;
+// SKL_FORCE_UNFUSED keeps it off so that run still exercises the GEMM chain.
+bool use_small(const SklDims& d, int64_t T) {
+    static const int mode = getenv("SKL_SMALL") ? atoi(getenv("SKL_SMALL")) : -1;
+    static const bool force_unfused = getenv("SKL_FORCE_UNFUSED") && atoi(getenv("SKL_FORCE_UNFUSED")) != 0;
+    if (mode == 0 || force_unfused || T < 1 || T > kSmallT) return false;
+    return mode == 1 || 2.0 * (double)d.R * (double)(d.d_in + d.d_out) * (double)T <= 0.5e9;
+}
 
 // Row stride (elements) of the transposed token-reduction operands Saved and
 // P_S2 ([L*k][T8]): T rounded up to 8 so every row starts 16-byte aligned.
@@ -735,6 +748,11 @@ Plan plan(const SklDims& d, skl_dtype t, int64_t T, bool bwd, int sms) {
         p.du_part = take(part);
         p.du_cpart = take(cpart);
         p.du_tickets = take(tickets);
+    }
+    if (use_small(d, T)) {
+        const int64_t splits = (std::max(d.d_in, d.d_out) + 63) / 64;
+        p.small_part = take((size_t)splits * T * d.R * 4);
+        p.small_h = take((size_t)T * d.R * 4);
     }
     p.colsum = take(0);
     p.total = off;
@@ -1146,6 +1164,31 @@ skl_status sketched_linear_forward_bits(const skl_shape* s, int64_t T, unsigned 
     const int elem = elem_of(s->dtype);
     const int eb = ebytes(s->dtype);
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
+    if (!bits && use_small(d, T)) {
+        SmallArgs a = {};
+        a.elem = elem;
+        a.T = (int)T;
+        a.d_in = (int)d.d_in;
+        a.d_out = (int)d.d_out;
+        a.k = (int)d.k;
+        a.Lk = (int)d.Lk;
+        a.R = (int)d.R;
+        a.alpha = inv;
+        a.x = x;
+        a.S1s = S1s;
+        a.S2s = S2s;
+        a.U1s = U1s;
+        a.U2s = U2s;
+        a.bias = bias;
+        a.relu = (fuse & SKL_FUSE_RELU_OUT) ? 1 : 0;
+        a.out = y;
+        a.save = saved_proj;
+        a.ld_save = t8(T);
+        a.part = at<float>(workspace, p.small_part);
+        a.H = at<float>(workspace, p.small_h);
+        SKL_CUDA(launch_small_forward(a, st));
+        return SKL_OK;
+    }
     void* acatT = at<void>(workspace, p.acatT);
     void* bcatT = at<void>(workspace, p.bcatT);
     float* bias32 = at<float>(workspace, p.bias32);
@@ -1302,6 +1345,39 @@ skl_status sketched_linear_backward_bits(const skl_shape* s, int64_t T, unsigned
     const int kind = s->dtype == SKL_BF16 ? 0 : 1;
     const float inv = (float)(1.0 / (2.0 * (double)d.L));
     const int64_t ldt = t8(T);
+    if (!bits && use_small(d, T)) {
+        SmallArgs a = {};
+        a.elem = elem;
+        a.T = (int)T;
+        a.d_in = (int)d.d_in;
+        a.d_out = (int)d.d_out;
+        a.k = (int)d.k;
+        a.Lk = (int)d.Lk;
+        a.R = (int)d.R;
+        a.alpha = inv;
+        a.x = x;
+        a.grad_y = grad_y;
+        a.S1s = S1s;
+        a.S2s = S2s;
+        a.U1s = U1s;
+        a.U2s = U2s;
+        a.mask = (fuse & SKL_FUSE_RELU_IN) ? x : nullptr;  // grad_x *= (x > 0): the preceding ReLU's backward
+        a.grad_x = grad_x;
+        a.need_saved = ph_u1 && !saved_proj;
+        a.save = at<void>(workspace, p.saved);
+        a.saved = saved_proj;
+        a.p2t = at<void>(workspace, p.p2t);
+        a.ld_save = ldt;
+        a.part = at<float>(workspace, p.small_part);
+        a.H = at<float>(workspace, p.small_h);
+        a.data = ph_data ? 1 : 0;
+        a.u1 = ph_u1 ? 1 : 0;
+        a.grad_U1s = grad_U1s;
+        a.grad_U2s = grad_U2s;
+        a.grad_bias = grad_bias;
+        SKL_CUDA(launch_small_backward(a, st));
+        return SKL_OK;
+    }
     void* acat = at<void>(workspace, p.acat);
     void* bcat = at<void>(workspace, p.bcat);
     void* acatT = at<void>(workspace, p.acatT);

@@ -44,4 +44,22 @@ cudaError_t launch_gaussian_scaled(int64_t rows, int64_t cols, uint64_t seed, do
                                    cudaStream_t st);
 // fp32 copy of an element-type vector (NULL in -> zeros), optionally TF32-rounded (cvt.rna).
 cudaError_t launch_to_f32(const void* in, int elem, int64_t n, float* out, int round_tf32, cudaStream_t st);
+// Small-batch path (small.cu): T <= kSmallT tokens, fp32 FMA over parameter slices.
+constexpr int kSmallT = 128;
+struct SmallArgs {
+    int elem, T, d_in, d_out, k, Lk, R;
+    float alpha;
+    const void *x, *grad_y, *S1s, *S2s, *U1s, *U2s, *bias, *mask;
+    int relu;
+    void *out, *grad_x;
+    void* save;         // forward: saved projection (nullable); backward: recomputed Saved^T target
+    const void* saved;  // backward: the caller's saved projection (when !need_saved)
+    void* p2t;          // backward: P_S2^T [Lk][ld_save]
+    long long ld_save;
+    float *part, *H;    // workspace: [splits][T][R] partials, [T][R] rank intermediate
+    int need_saved, data, u1;
+    float *grad_U1s, *grad_U2s, *grad_bias;
+};
+cudaError_t launch_small_forward(const SmallArgs& a, cudaStream_t st);
+cudaError_t launch_small_backward(const SmallArgs& a, cudaStream_t st);
 }  // namespace skl

@@ -694,6 +694,66 @@ def test_unfused_path_parity_in_subprocess():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+def test_fused_path_small_batches_in_subprocess():
+    """The parity tests once more with SKL_SMALL=0: batches of T <= 128 tokens (the
+    c1 shape, T = 64; ragged 50 / 77) take the fused tcgen05 kernels instead of the
+    small-batch path (small.cu), against the same oracle gates."""
+    import subprocess
+    import sys
+    if os.environ.get("SKL_SMALL") is not None:
+        pytest.skip("already the SKL_SMALL process")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SKL_SMALL="0")
+    # the parametrised cases with T <= 128 (ids end in the token count) and the small-shape tests
+    sel = ("(parity and (-64] or -50] or -77] or -20])) or c1 or gradcheck or identity or criterion or zero or "
+           "ragged or deterministic_small")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "tests/test_gpu.py", "tests/test_gpu_shapes.py",
+                        "-k", sel],
+                       env=env, cwd=root, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
+
+
+def test_small_batch_path_is_deterministic_and_matches_fused(skl, port):
+    """T <= 128: the small-batch path (fp32 FMA over parameter slices) against the
+    oracle at the c1 shape in both dtypes, bitwise reproducible, for every phase
+    split and a fused ReLU / x-mask."""
+    import oracle
+    from tests._util import check_close
+    for kind, name in ((skl.F32_TF32, "tf32"), (skl.BF16, "bf16")):
+        d_in, d_out, L, k, T = 1024, 1024, 1, 64, 64
+        s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, kind)
+        td = skl.torch_dtype(kind)
+        ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+        sv = torch.empty(L * k, (T + 7) // 8 * 8, dtype=td, device="cuda")
+        runs = []
+        for _ in range(2):
+            y = torch.empty(T, d_out, dtype=td, device="cuda")
+            skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, sv, ws)
+            gx = torch.empty(T, d_in, dtype=td, device="cuda")
+            du1 = torch.empty(L, k, d_out, device="cuda")
+            du2 = torch.empty(L, d_in, k, device="cuda")
+            db = torch.empty(d_out, device="cuda")
+            skl.backward(s, G, X, sv, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+            runs.append((y, gx, du1, du2, db))
+        torch.cuda.synchronize()
+        for a, b in zip(*runs):
+            assert torch.equal(a, b)
+        y, gx, du1, du2, db = runs[0]
+        check_close(f"small y {name}", _np(y), port.forward(P, b64, x64).T, name)
+        rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+        check_close(f"small grad_x {name}", _np(gx), rgx, name)
+        check_close(f"small dU1s {name}", _np(du1), rgu1, name)
+        check_close(f"small dU2s {name}", _np(du2), rgu2, name)
+        check_close(f"small db {name}", _np(db), rgb, name)
+        # the DP phases give the same gradients bitwise
+        du1p, du2p, dbp = torch.empty_like(du1), torch.empty_like(du2), torch.empty_like(db)
+        gxp = torch.empty_like(gx)
+        skl.backward_phase(s, skl.BWD_DU1_DB, G, X, sv, S1s, S2s, U1s, U2s, None, du1p, None, dbp, ws)
+        skl.backward_phase(s, skl.BWD_DX_DU2, G, X, sv, S1s, S2s, U1s, U2s, gxp, None, du2p, None, ws)
+        torch.cuda.synchronize()
+        assert torch.equal(du1p, du1) and torch.equal(du2p, du2) and torch.equal(dbp, db) and torch.equal(gxp, gx)
+
+
 def test_rsplit_path_parity_in_subprocess():
     """The parity tests once more with SKL_B2B_RSPLIT=1: shapes with R > 512 (the
     R = 768 / 640 / 2048 and c3 R = 1536 cases) run on the R-split clusters (H on
