@@ -276,6 +276,9 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
             "tflops": flops / (ms / 1e3) / 1e12, "hbm_gbs_alg": bytes_ / (ms / 1e3) / 1e9,
             # on-chip H: bf16 b2b kernel (R <= 512), TF32 b2b kernel (R <= 256) or wide-rank TF32 kernel (R <= 512)
             "fused": bool(r_pad <= 512),
+            "path": ("small-batch (small.cu: T <= 128, fp32 FMA over parameter slices)"
+                     if T <= 128 and 2.0 * 2 * l * k * (d_in + d_out) * T <= 0.5e9
+                     else "fused b2b (H on chip)" if r_pad <= 512 else "unfused tcgen05 GEMM chain (H through HBM)"),
             "peak_tflops_used": peak_tf, "peak_source": tf_src, "phased_backward": phased, "cuda_graph": graph,
             "ms_per_step_eager": ms_eager}
 
