@@ -575,6 +575,9 @@ def main():
     e2e = {"value": world * T / (ms_e2e / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": Xh.numel() * 2 + Gh.numel() * 2, "d2h_bytes_per_step": out_h.numel() * 4,
            "ms_per_step": ms_e2e,
+           # the binding resource end to end is the host link: achieved H2D rate over the step
+           "h2d_gbs": (Xh.numel() * 2 + Gh.numel() * 2) / (ms_e2e / 1e3) / 1e9,
+           "bound": "PCIe host->device copy of X and G (the device step is %.0f%% of it)" % (100 * ms / ms_e2e),
            "path": "pinned host X,G -(copy stream, double-buffered)-> sketched_linear_forward/backward -> "
                    "grad bucket to pinned host, every step"}
 
