@@ -394,9 +394,12 @@ __global__ void __launch_bounds__(256) col2im_gather_kernel(const T* __restrict_
     const int64_t d = (int64_t)g.c * g.kh * g.kw;
     const int64_t n = (int64_t)g.B * g.c * g.h * g.w;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const int ix = (int)(i % g.w), iy = (int)((i / g.w) % g.h);
-        const int ch = (int)((i / ((int64_t)g.w * g.h)) % g.c);
-        const int64_t b = i / ((int64_t)g.w * g.h * g.c);
+        // one 64-bit split into (image plane, pixel), then 32-bit arithmetic
+        const int64_t plane = i / ((int64_t)g.w * g.h);
+        const int pix = (int)(i - plane * g.w * g.h);
+        const int iy = pix / g.w, ix = pix - iy * g.w;
+        const int ch = (int)(plane % g.c);
+        const int64_t b = plane / g.c;
         float acc = 0.f;
         for (int kr = 0; kr < g.kh; ++kr) {
             const int ty = iy + g.pad - kr;
@@ -413,6 +416,39 @@ __global__ void __launch_bounds__(256) col2im_gather_kernel(const T* __restrict_
             }
         }
         img[i] = T(acc);
+    }
+}
+
+// Bandwidth-shaped im2col (round 2; the per-element kernel above spent 430 us
+// at a 64-channel 56x56 3x3 layer, B = 32, on 64-bit index arithmetic and
+// channel-strided reads; this one 80 us for the 116 MB patch matrix).  One warp per token, lanes along the lowered features (coalesced
+// row writes); the (channel plane offset, kr, kc) of every feature comes from
+// a shared-memory table built once per block, so the inner loop is a bounds
+// test, one L2 load and one store.  Same values, same layout.
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_warp_kernel(const T* __restrict__ img, T* __restrict__ cols,
+                                                          ConvGeom g) {
+    extern __shared__ int im_tab[];  // [d] channel plane offsets, then [d] (kr << 16 | kc)
+    const int d = g.c * g.kh * g.kw, khw = g.kh * g.kw;
+    int* ch_off = im_tab;
+    int* rc = im_tab + d;
+    for (int f = threadIdx.x; f < d; f += blockDim.x) {
+        const int ch = f / khw, r = f % khw;
+        ch_off[f] = ch * g.h * g.w;
+        rc[f] = ((r / g.kw) << 16) | (r % g.kw);
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warps = blockDim.x >> 5;
+    const long long tokens = (long long)g.B * g.oh * g.ow;
+    for (long long t = (long long)blockIdx.x * warps + (threadIdx.x >> 5); t < tokens; t += (long long)gridDim.x * warps) {
+        const int b = (int)(t / ((long long)g.oh * g.ow)), p = (int)(t % ((long long)g.oh * g.ow));
+        const int y0 = (p / g.ow) * g.stride - g.pad, x0 = (p % g.ow) * g.stride - g.pad;
+        const T* src = img + (long long)b * g.c * g.h * g.w;
+        T* dst = cols + t * d;
+        for (int f = lane; f < d; f += 32) {
+            const int iy = y0 + (rc[f] >> 16), ix = x0 + (rc[f] & 0xFFFF);
+            dst[f] = (iy >= 0 && iy < g.h && ix >= 0 && ix < g.w) ? src[ch_off[f] + iy * g.w + ix] : T(0.f);
+        }
     }
 }
 
@@ -458,6 +494,17 @@ __global__ void __launch_bounds__(256) tokens_planes_kernel(const T* __restrict_
 cudaError_t launch_im2col(const void* img, int elem, const ConvGeom& g, void* cols, cudaStream_t st) {
     ProfScope ps_("im2col", st);
     const uint64_t n = (uint64_t)g.B * g.oh * g.ow * g.c * g.kh * g.kw;
+    const int d = g.c * g.kh * g.kw;
+    const size_t tab = (size_t)d * 8;
+    if (tab <= 48 * 1024 && (uint64_t)g.c * g.h * g.w < (1ull << 31)) {  // table in static-limit smem, 32-bit offsets
+        const uint64_t tokens = (uint64_t)g.B * g.oh * g.ow;
+        const int grid = (int)std::min<uint64_t>((tokens + 7) / 8, 148 * 16);
+        if (elem == ELEM_BF16)
+            im2col_warp_kernel<__nv_bfloat16><<<grid, 256, tab, st>>>((const __nv_bfloat16*)img, (__nv_bfloat16*)cols, g);
+        else
+            im2col_warp_kernel<float><<<grid, 256, tab, st>>>((const float*)img, (float*)cols, g);
+        return cudaGetLastError();
+    }
     if (elem == ELEM_BF16)
         im2col_tokens_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)img, (__nv_bfloat16*)cols, g);
     else
