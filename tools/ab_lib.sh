@@ -2,6 +2,6 @@
 export PATH=/usr/local/cuda/bin:$PATH
 A=$1; B=$2; CMD=$3; N=${4:-3}
 for i in $(seq $N); do
-  echo "== A ($A)"; SKL_LIB=$A $CMD 2>&1 | grep -v "^\s*$" | tail -3
-  echo "== B ($B)"; SKL_LIB=$B $CMD 2>&1 | grep -v "^\s*$" | tail -3
+  echo "== A ($A)"; SKL_LIB=$A $CMD 2>&1 | grep -v "^\s*$" | tail -${LINES:-12}
+  echo "== B ($B)"; SKL_LIB=$B $CMD 2>&1 | grep -v "^\s*$" | tail -${LINES:-12}
 done
