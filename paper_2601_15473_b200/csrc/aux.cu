@@ -452,6 +452,59 @@ __global__ void __launch_bounds__(256) im2col_warp_kernel(const T* __restrict__ 
     }
 }
 
+// col2im, channel-parallel: a block owns 32 channels x 32 pixels of one image
+// row.  Lanes run along the channels, so each patch-matrix load of a warp
+// covers one token's 32 x (kh x kw) contiguous entries (the neighbours' (kr,
+// kc) entries of the same sectors are read by the neighbouring pixels of the
+// block, from L1); the sums (in (kr, kc) order, as the per-pixel gather above:
+// bitwise the same) are transposed through shared memory so the image row is
+// written 64 contiguous bytes per warp store.
+template <typename T>
+__global__ void __launch_bounds__(256) col2im_chan_kernel(const T* __restrict__ cols, T* __restrict__ img,
+                                                          ConvGeom g) {
+    __shared__ float tile[32][33];  // [channel][pixel]
+    const int khw = g.kh * g.kw;
+    const long long d = (long long)g.c * khw;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nxb = (g.w + 31) / 32, ncb = (g.c + 31) / 32;
+    const long long nblk = (long long)g.B * g.h * nxb * ncb;
+    for (long long blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const int cb = (int)(blk % ncb), xb = (int)((blk / ncb) % nxb);
+        const int iy = (int)((blk / ((long long)ncb * nxb)) % g.h);
+        const long long b = blk / ((long long)ncb * nxb * g.h);
+        const int ch = cb * 32 + lane, x0 = xb * 32;
+        __syncthreads();  // the previous tile's stores have read `tile`
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+            const int px = warp + 8 * j, ix = x0 + px;
+            float acc = 0.f;
+            if (ch < g.c && ix < g.w) {
+                const T* base = cols + (long long)ch * khw;
+                for (int kr = 0; kr < g.kh; ++kr) {
+                    const int ty = iy + g.pad - kr;
+                    if (ty < 0 || ty % g.stride) continue;
+                    const int oy = ty / g.stride;
+                    if (oy >= g.oh) continue;
+                    for (int kc = 0; kc < g.kw; ++kc) {
+                        const int tx = ix + g.pad - kc;
+                        if (tx < 0 || tx % g.stride) continue;
+                        const int ox = tx / g.stride;
+                        if (ox >= g.ow) continue;
+                        acc += (float)base[((b * g.oh + oy) * g.ow + ox) * d + kr * g.kw + kc];
+                    }
+                }
+            }
+            tile[lane][px] = acc;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {  // warp -> channel rows, lanes along the pixels
+            const int cl = warp + 8 * j, c = cb * 32 + cl, ix = x0 + lane;
+            if (c < g.c && ix < g.w) img[((b * g.c + c) * g.h + iy) * g.w + ix] = T(tile[cl][lane]);
+        }
+    }
+}
+
 // [B*P, C] token rows <-> [B, C, P] planes (P = oh*ow): 32x32 smem tiles per image.
 template <typename T>
 __global__ void __launch_bounds__(256) tokens_planes_kernel(const T* __restrict__ in, T* __restrict__ out, int64_t B,
@@ -515,6 +568,15 @@ cudaError_t launch_im2col(const void* img, int elem, const ConvGeom& g, void* co
 cudaError_t launch_col2im(const void* cols, int elem, const ConvGeom& g, void* img, cudaStream_t st) {
     ProfScope ps_("col2im", st);
     const uint64_t n = (uint64_t)g.B * g.c * g.h * g.w;
+    if (g.c >= 16) {  // channel-parallel tiles (fewer channels would leave most lanes idle)
+        const uint64_t blocks = (uint64_t)g.B * g.h * ((g.w + 31) / 32) * ((g.c + 31) / 32);
+        const int grid = (int)std::min<uint64_t>(blocks, 148 * 16);
+        if (elem == ELEM_BF16)
+            col2im_chan_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)cols, (__nv_bfloat16*)img, g);
+        else
+            col2im_chan_kernel<float><<<grid, 256, 0, st>>>((const float*)cols, (float*)img, g);
+        return cudaGetLastError();
+    }
     if (elem == ELEM_BF16)
         col2im_gather_kernel<__nv_bfloat16><<<grid_for(n), 256, 0, st>>>((const __nv_bfloat16*)cols, (__nv_bfloat16*)img, g);
     else
