@@ -58,6 +58,22 @@ def peaks():
     return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def sustained_tflops(dtype):
+    """The sustained (4 s back-to-back) dense peak for the long sweep workloads, reported
+    next to the burst-based fraction: bf16 from MEASURED_PEAKS.json, TF32 from
+    profiles/r2_tf32_peak.json."""
+    if dtype == "bf16":
+        p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+        if os.path.exists(p):
+            with open(p) as f:
+                d = json.load(f)
+            if "bf16_tflops_sustained" in d:
+                return float(d["bf16_tflops_sustained"])
+        return None
+    with open(os.path.join(ROOT, "profiles", "r2_tf32_peak.json")) as f:
+        return float(json.load(f)["tf32_tflops_sustained"])
+
+
 def tf32_peak():
     """Dense TF32 peak: MEASURED_PEAKS.json when the driver measured it, else the
     figure tools/measure_tf32_peak.py measured on a B200 (cuBLAS fp32 8192^3 with
@@ -271,13 +287,17 @@ def measure_workload(skl, torch, dev, name, d_in, d_out, l, k, T, dtype, steps=1
     peak_tf, tf_src = (peak_bf16, "bf16 burst") if dtype == "bf16" else tf32_peak()
     t_roof, bound, flops, bytes_ = roofline_time(d_in, d_out, l, k, T, 2 if dtype == "bf16" else 4, peak_tf, peak_bw)
     r_pad = (2 * l * k + 63) // 64 * 64
+    small = T <= 128 and 2.0 * 2 * l * k * (d_in + d_out) * T <= 0.5e9  # skl.cu use_small
+    sus = sustained_tflops(dtype)
+    t_roof_s = roofline_time(d_in, d_out, l, k, T, 2 if dtype == "bf16" else 4, sus, peak_bw)[0] if sus else None
     return {"workload": name, "dtype": dtype, "tokens": T, "ms_per_step": ms, "tokens_per_s": T / (ms / 1e3),
             "bound": bound, "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
+            "roofline_frac_sustained_peak": (t_roof_s / (ms / 1e3)) if t_roof_s else None,
             "tflops": flops / (ms / 1e3) / 1e12, "hbm_gbs_alg": bytes_ / (ms / 1e3) / 1e9,
-            # on-chip H: bf16 b2b kernel (R <= 512), TF32 b2b kernel (R <= 256) or wide-rank TF32 kernel (R <= 512)
-            "fused": bool(r_pad <= 512),
-            "path": ("small-batch (small.cu: T <= 128, fp32 FMA over parameter slices)"
-                     if T <= 128 and 2.0 * 2 * l * k * (d_in + d_out) * T <= 0.5e9
+            # on-chip H: bf16 b2b kernel (R <= 512), TF32 b2b kernel (R <= 256) or wide-rank TF32 kernel (R <= 512);
+            # T <= 128 takes the small-batch path (rank intermediate in a 32 KB fp32 buffer, L2-resident)
+            "fused": bool(r_pad <= 512) and not small,
+            "path": ("small-batch (small.cu: T <= 128, fp32 FMA over parameter slices)" if small
                      else "fused b2b (H on chip)" if r_pad <= 512 else "unfused tcgen05 GEMM chain (H through HBM)"),
             "peak_tflops_used": peak_tf, "peak_source": tf_src, "phased_backward": phased, "cuda_graph": graph,
             "ms_per_step_eager": ms_eager}
@@ -318,12 +338,15 @@ def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     peak_bf16, peak_bw, _ = peaks()
-    t_roof = 0.0
+    sus = sustained_tflops("bf16")
+    t_roof = t_roof_s = 0.0
     flops = 0
     for stp in chain.steps:
         L = stp.layer
         tr, _, f, _ = roofline_time(L.d_in, L.d_out, L.num_terms, L.low_rank, T, 2, peak_bf16, peak_bw)
         t_roof += tr
+        if sus:
+            t_roof_s += roofline_time(L.d_in, L.d_out, L.num_terms, L.low_rank, T, 2, sus, peak_bw)[0]
         flops += f
     del chain, buckets
     torch.cuda.empty_cache()
@@ -332,6 +355,7 @@ def measure_stack(skl, torch, dev, world, steps=5, warmup=2, T=T_GPU, num_layers
                                                                         if world > 1 else ""),
             "dtype": "bf16", "tokens": T * world, "ms_per_step": ms, "tokens_per_s": world * T / (ms / 1e3),
             "bound": "tensor", "roofline_ms": t_roof * 1e3, "roofline_frac": t_roof / (ms / 1e3),
+            "roofline_frac_sustained_peak": (t_roof_s / (ms / 1e3)) if sus else None,
             "tflops": flops / (ms / 1e3) / 1e12, "n_gpus": world, "cuda_graph": graph, "ms_per_step_eager": ms_eager}
 
 
