@@ -25,6 +25,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "prof.h"
 #include "skl_internal.h"
@@ -61,6 +62,35 @@ __device__ __forceinline__ float bcat(const Stacks& p, int r, int o) {
     return to_f(src[(long long)(u ? r : r - p.Lk) * p.d_out + o]);
 }
 
+// Programmatic dependent launch, as every other kernel of the library: the next
+// kernel's launch and prologue overlap this one's tail; each kernel waits for
+// its predecessor before touching data and only then lets its dependent start
+// (seven dependent launches per c1 step, each a few microseconds of work).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, cudaStream_t st, Args... args) {
+    static const bool pdl = !(getenv("SKL_PDL") && atoi(getenv("SKL_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
+#define SMALL_LAUNCH(kern, grid, st, ...)                                \
+    do {                                                                 \
+        const cudaError_t e_ = launch_pdl(kern, grid, st, __VA_ARGS__); \
+        if (e_ != cudaSuccess) return e_;                                \
+    } while (0)
+
 constexpr int kKS = 64;  // K slice per CTA (proj_part) / K chunk (out_gemm)
 constexpr int kNC = 32;  // output columns per CTA
 
@@ -91,6 +121,7 @@ __device__ __forceinline__ void micro_tile(const float (*A)[kTP], const float (*
 template <typename E, int kMode>
 __global__ void __launch_bounds__(256) proj_part_kernel(const E* __restrict__ in, Stacks p, int T, int r_end,
                                                         float* __restrict__ part) {
+    pdl_enter();
     __shared__ __align__(16) float in_s[kKS][kTP];  // transposed: [k][token]
     __shared__ __align__(16) float w_s[kKS][kWP];
     const int K = kMode == 0 ? p.d_in : p.d_out;
@@ -144,6 +175,7 @@ template <typename E>
 __global__ void __launch_bounds__(256) reduce_rank_kernel(const float* __restrict__ part, int S, int T, int R,
                                                           int r_end, float* __restrict__ H, E* __restrict__ save,
                                                           int c0, int Lk, long long ld_save) {
+    pdl_enter();
     const long long n = (long long)T * r_end;
     for (long long e = blockIdx.x * 256LL + threadIdx.x; e < n; e += (long long)gridDim.x * 256) {
         const int r = (int)(e % r_end), t = (int)(e / r_end);  // r fastest: coalesced partial loads
@@ -167,6 +199,7 @@ template <typename E, int kMode>
 __global__ void __launch_bounds__(256) out_gemm_kernel(const float* __restrict__ H, Stacks p, int T, float alpha,
                                                        const E* __restrict__ bias, int relu, const E* __restrict__ mask,
                                                        E* __restrict__ out) {
+    pdl_enter();
     __shared__ __align__(16) float h_s[kKS][kTP];  // transposed: [rank][token]
     __shared__ __align__(16) float w_s[kKS][kWP];
     const int N = kMode == 0 ? p.d_out : p.d_in;
@@ -239,6 +272,7 @@ __global__ void __launch_bounds__(256) grads_small_kernel(const E* __restrict__ 
                                                           long long ld, Stacks p, int T, float alpha, int g1,
                                                           float* __restrict__ dU1, float* __restrict__ dU2,
                                                           float* __restrict__ db) {
+    pdl_enter();
     __shared__ __align__(16) float a_s[kSmallT][kWP];  // activation columns: G (dU1) or X (dU2)
     __shared__ __align__(16) float r_s[kSmallT][kWP];  // rank columns: Saved (dU1) or P_S2 (dU2), token-major
     const bool u1 = (int)blockIdx.x < g1;
@@ -299,17 +333,17 @@ cudaError_t small_forward_t(const SmallArgs& a, cudaStream_t st) {
     const int S = (a.d_in + kKS - 1) / kKS;
     {
         ProfScope ps_("small_proj", st);
-        proj_part_kernel<E, 0><<<dim3((a.R + kNC - 1) / kNC, S), 256, 0, st>>>(static_cast<const E*>(a.x), p, a.T,
+        SMALL_LAUNCH((proj_part_kernel<E, 0>), dim3((a.R + kNC - 1) / kNC, S), st, static_cast<const E*>(a.x), p, a.T,
                                                                               a.R, a.part);
     }
     {
         ProfScope ps_("small_reduce", st);
         const long long n = (long long)a.T * a.R;
-        reduce_rank_kernel<E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a.part, S, a.T, a.R, a.R, a.H,
+        SMALL_LAUNCH(reduce_rank_kernel<E>, dim3((unsigned)((n + 255) / 256)), st, a.part, S, a.T, a.R, a.R, a.H,
                                                                              static_cast<E*>(a.save), 0, a.Lk, a.ld_save);
     }
     ProfScope ps_("small_out", st);
-    out_gemm_kernel<E, 0><<<(a.d_out + kNC - 1) / kNC, 256, 0, st>>>(a.H, p, a.T, a.alpha, static_cast<const E*>(a.bias),
+    SMALL_LAUNCH((out_gemm_kernel<E, 0>), dim3((a.d_out + kNC - 1) / kNC), st, a.H, p, a.T, a.alpha, static_cast<const E*>(a.bias),
                                                                     a.relu, nullptr, static_cast<E*>(a.out));
     return cudaGetLastError();
 }
@@ -322,12 +356,12 @@ cudaError_t small_backward_t(const SmallArgs& a, cudaStream_t st) {
         const int S = (a.d_in + kKS - 1) / kKS;
         {
             ProfScope ps_("small_proj", st);
-            proj_part_kernel<E, 0><<<dim3((a.Lk + kNC - 1) / kNC, S), 256, 0, st>>>(static_cast<const E*>(a.x), p, a.T,
+            SMALL_LAUNCH((proj_part_kernel<E, 0>), dim3((a.Lk + kNC - 1) / kNC, S), st, static_cast<const E*>(a.x), p, a.T,
                                                                                    a.Lk, a.part);
         }
         ProfScope ps_("small_reduce", st);
         const long long n = (long long)a.T * a.Lk;
-        reduce_rank_kernel<E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+        SMALL_LAUNCH(reduce_rank_kernel<E>, dim3((unsigned)((n + 255) / 256)), st, 
             a.part, S, a.T, a.R, a.Lk, nullptr, static_cast<E*>(a.save), 0, a.Lk, a.ld_save);
         saved = static_cast<const E*>(a.save);
     }
@@ -335,25 +369,25 @@ cudaError_t small_backward_t(const SmallArgs& a, cudaStream_t st) {
         const int S = (a.d_out + kKS - 1) / kKS;
         {
             ProfScope ps_("small_proj", st);
-            proj_part_kernel<E, 1><<<dim3((a.R + kNC - 1) / kNC, S), 256, 0, st>>>(static_cast<const E*>(a.grad_y), p,
+            SMALL_LAUNCH((proj_part_kernel<E, 1>), dim3((a.R + kNC - 1) / kNC, S), st, static_cast<const E*>(a.grad_y), p,
                                                                                   a.T, a.R, a.part);
         }
         {
             ProfScope ps_("small_reduce", st);
             const long long n = (long long)a.T * a.R;
-            reduce_rank_kernel<E><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            SMALL_LAUNCH(reduce_rank_kernel<E>, dim3((unsigned)((n + 255) / 256)), st, 
                 a.part, S, a.T, a.R, a.R, a.H, static_cast<E*>(a.p2t), a.Lk, a.Lk, a.ld_save);
         }
         if (a.grad_x) {
             ProfScope ps_("small_out", st);
-            out_gemm_kernel<E, 1><<<(a.d_in + kNC - 1) / kNC, 256, 0, st>>>(
+            SMALL_LAUNCH((out_gemm_kernel<E, 1>), dim3((a.d_in + kNC - 1) / kNC), st, 
                 a.H, p, a.T, a.alpha, nullptr, 0, static_cast<const E*>(a.mask), static_cast<E*>(a.grad_x));
         }
     }
     const int g1 = a.u1 ? (a.d_out + kNC - 1) / kNC : 0, g2 = a.data ? (a.d_in + kNC - 1) / kNC : 0;
     if (g1 + g2 == 0) return cudaGetLastError();
     ProfScope ps_("small_grads", st);
-    grads_small_kernel<E><<<dim3(g1 + g2, (a.Lk + kNC - 1) / kNC), 256, 0, st>>>(
+    SMALL_LAUNCH(grads_small_kernel<E>, dim3(g1 + g2, (a.Lk + kNC - 1) / kNC), st, 
         static_cast<const E*>(a.grad_y), static_cast<const E*>(a.x), saved, static_cast<const E*>(a.p2t), a.ld_save,
         p, a.T, a.alpha, g1, a.grad_U1s, a.grad_U2s, a.u1 ? a.grad_bias : nullptr);
     return cudaGetLastError();
