@@ -167,14 +167,14 @@ struct B2BCfg {
 // kPost: 1 = the epilogue also applies the fused ReLU / ReLU mask (B2BArgs::relu /
 // mask), 2 = the same with 1-bit masks (relu_bits / mask_bits); separate
 // instantiations so the plain layer keeps its register budget.
-template <int kCG, int kMode, int kKind, int kPost, bool kRS = false, bool kSP = false>
+template <int kCG, int kMode, int kKind, int kPost, bool kRS = false, bool kSP = false, bool kDT = false>
 __global__ void __launch_bounds__(384, 1)
     b2b_kernel(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmB1,
                const __grid_constant__ CUtensorMap tmB1b, const __grid_constant__ CUtensorMap tmB2,
                const __grid_constant__ CUtensorMap tmB2b, const __grid_constant__ CUtensorMap tmY,
                const __grid_constant__ CUtensorMap tmM, const __grid_constant__ CUtensorMap tmS,
                const __grid_constant__ CUtensorMap tmYw, B2BArgs args) {
-    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
+    using C = B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP || kDT>;
     extern __shared__ uint8_t smem_raw[];
     const uint32_t base_u32 = (smem_u32(smem_raw) + 1023u) & ~1023u;
     uint8_t* smem = smem_raw + (base_u32 - smem_u32(smem_raw));
@@ -351,11 +351,50 @@ __global__ void __launch_bounds__(384, 1)
                     }
                 }
             };
+            if constexpr (kDT) {
+                // Double tiles (R = 256): a GEMM1 stage holds the A tiles of two pair
+                // tiles (2u, 2u + 1) around one B1 k-block, so every weight byte
+                // brought in feeds twice the MMAs (the weight panels are two thirds of
+                // a 768x768 projection tile's operand traffic).
+                const int ndt = (num_tiles + 1) / 2;
+                for (int u = cluster_id; u < ndt; u += num_clusters) {
+                    for (int kb = 0; kb < nkb1; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        tr(1);
+                        uint8_t* st = smem + stage * C::kStageBytes;
+                        if (leader) mbar_arrive_expect_tx(&full[stage], 3u * 16384u * kCG);
+                        else mbar_arrive_cluster(&full[stage], lead);
+                        tma_load_2d_hint<kCG>(&tmA1, &full[stage], st, kb * C::kBK, 2 * u * tile_rows + (int)rank * 128,
+                                              pol_act);
+                        tma_load_2d_hint<kCG>(&tmA1, &full[stage], st + 32768, kb * C::kBK,
+                                              (2 * u + 1) * tile_rows + (int)rank * 128, pol_act);
+                        const int brows = 256 / kCG, b0 = (int)rank * brows;
+                        uint8_t* bst = st + C::kAOff;
+                        if constexpr (kMode == 2) {  // rows of [U1s ; S2s]
+                            for (int r = 0; r < brows; r += args.b1rows) {
+                                const int rg = b0 + r;
+                                tma_load_2d_hint<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + r * 128, kb * 64,
+                                                      rg < args.Lk ? rg : rg - args.Lk, pol_w);
+                            }
+                        } else {  // MN-major [64 d_in rows x 64 rank cols] blocks of S1s | U2s
+                            for (int jb = 0; jb < brows / 64; ++jb) {
+                                const int rg = b0 + 64 * jb;
+                                const int rr = rg < args.Lk ? rg : rg - args.Lk;
+                                tma_load_2d_hint<kCG>(rg < args.Lk ? &tmB1 : &tmB1b, &full[stage], bst + jb * 8192,
+                                                      rr % args.k, (rr / args.k) * args.dS + kb * 64, pol_w);
+                            }
+                        }
+                        next();
+                    }
+                    load_g2();
+                }
+            } else {
             if (pp && cluster_id < num_tiles) load_g1(cluster_id);
             for (int t = cluster_id; t < num_tiles; t += num_clusters) {
                 if (!pp) load_g1(t);
                 else if (t + num_clusters < num_tiles) load_g1(t + num_clusters);
                 load_g2();
+            }
             }
         }
     } else if (warp == 1) {
@@ -433,6 +472,83 @@ __global__ void __launch_bounds__(384, 1)
                     commit(&tfull2[s]);
                 }
             };
+            if constexpr (kDT) {
+                // Double tiles: TMEM [0, 256) and [256, 512) take tile a's and tile b's
+                // GEMM1 (fp32), compacted to H_a = [0, 128), H_b = [256, 384); GEMM2 of
+                // each output column tile accumulates a in [128, 256) and b in [384, 512)
+                // from the same B2 stage.  Each slot's drains are waited exactly once, in
+                // order: by the next output tile, the last one by the next double tile's
+                // GEMM1 (which overwrites the whole of TMEM).
+                const uint32_t idesc1 = make_idesc(kKind, 128 * kCG, 256, 0, kMode == 1 ? 1 : 0);
+                uint32_t dwait[2] = {0u, 0u};
+                auto wait_drain = [&](int h) {
+                    mbar_wait(&tempty2[h], dwait[h] & 1);
+                    ++dwait[h];
+                };
+                const int ndt = (num_tiles + 1) / 2;
+                for (int u = cluster_id; u < ndt; u += num_clusters, ++it) {
+                    if (it > 0) {
+                        wait_drain(0);
+                        wait_drain(1);
+                        tc_fence_after();
+                    }
+                    for (int kb = 0; kb < nkb1; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        tr(11);
+                        tc_fence_after();
+                        const uint32_t a_addr = smem_u32(smem + stage * C::kStageBytes);
+                        const uint32_t b_addr = a_addr + C::kAOff;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h)
+#pragma unroll
+                            for (int k = 0; k < 4; ++k)
+                                mma_ss<kCG, kKind>(tmem_base + 256u * h, make_sdesc(a_addr + 32768u * h + k * 32, 0, 1024),
+                                                   kMode == 1 ? make_sdesc(b_addr + k * 2048, 8192, 1024)
+                                                              : make_sdesc(b_addr + k * 32, 0, 1024),
+                                                   idesc1, (kb > 0 || k > 0) ? 1u : 0u);
+                        commit(&empty[stage]);
+                        next();
+                    }
+                    commit(&tfull1[0]);
+                    commit(&tfull1[1]);
+                    mbar_wait(&hready[0], it & 1);
+                    mbar_wait(&hready[1], it & 1);
+                    tr(12);
+                    tc_fence_after();
+                    for (int j = 0; j < n2_tiles; ++j) {
+                        if (j > 0) {
+                            wait_drain(0);
+                            wait_drain(1);
+                            tc_fence_after();
+                        }
+                        for (int st2 = 0; st2 < nst2; ++st2) {
+                            const int kb0 = st2 * C::kKbPerStage2;
+                            const int nk = min(C::kKbPerStage2, nkb2 - kb0);
+                            mbar_wait(&full[stage], phase);
+                            tr(14);
+                            tc_fence_after();
+                            const uint32_t b_addr = smem_u32(smem + stage * C::kStageBytes);
+#pragma unroll
+                            for (int h = 0; h < 2; ++h)
+                                for (int q = 0; q < nk; ++q) {
+#pragma unroll
+                                    for (int k = 0; k < 4; ++k) {
+                                        const uint32_t a_t = tmem_base + 256u * h + (uint32_t)((kb0 + q) * 32 + k * 8);
+                                        const uint64_t bdesc = kMode == 1
+                                            ? make_sdesc(b_addr + q * C::kB2KbBytes + k * 2048, 8192, 1024)
+                                            : make_sdesc(b_addr + q * C::kB2KbBytes + k * 32, 0, 1024);
+                                        mma_ts<kCG, kKind>(tmem_base + 256u * h + 128u, a_t, bdesc, idesc2,
+                                                           (st2 > 0 || q > 0 || k > 0) ? 1u : 0u);
+                                    }
+                                }
+                            commit(&empty[stage]);
+                            next();
+                        }
+                        commit(&tfull2[0]);
+                        commit(&tfull2[1]);
+                    }
+                }
+            } else {
             if (pp && cluster_id < num_tiles) issue_g1(0, 0);
             for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
                 if (!pp) issue_g1(0, 0);
@@ -443,6 +559,7 @@ __global__ void __launch_bounds__(384, 1)
                 tr(12);
                 tc_fence_after();
                 issue_g2(pp ? 128u * (it & 1) : 0u);
+            }
             }
         }
     } else if (warp >= 4) {
@@ -616,6 +733,134 @@ __global__ void __launch_bounds__(384, 1)
             }
             ++xch;
         };
+        if constexpr (kDT) {
+            // Double tiles (see the MMA issuer): convert both halves, save their
+            // columns (from the bf16 H), then per output column tile drain slot a and
+            // slot b.  Per-warp stores; the bias, when any, is the resident table.
+            int it = 0;
+            uint32_t tpar[2] = {0u, 0u};
+            const int ndt = (num_tiles + 1) / 2;
+            for (int u = cluster_id; u < ndt; u += num_clusters, ++it) {
+#pragma unroll 1
+                for (int h = 0; h < 2; ++h) {
+                    const uint32_t hoff = 256u * (uint32_t)h;
+                    mbar_wait(&tfull1[h], it & 1);
+                    tr(21);
+                    tc_fence_after();
+#pragma unroll 1
+                    for (int rd = 0; rd < 2; ++rd) {  // in-place compaction as in the one-tile path (W = 64)
+                        const int qi = 2 * rd + (int)wg;
+                        uint32_t rr[4][16];
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) tmem_ld16(tmem_base + lane_base + hoff + qi * 64 + 16 * g, rr[g]);
+                        tmem_ld_wait();
+                        if (rd == 0) {
+                            tc_fence_before();
+                            named_bar_sync(3, 256);
+                            tc_fence_after();
+                        }
+#pragma unroll
+                        for (int g = 0; g < 4; ++g) {
+                            uint32_t pk[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i)
+                                pk[i] = pack_bf16x2(__uint_as_float(rr[g][2 * i]), __uint_as_float(rr[g][2 * i + 1]));
+                            tmem_st8(tmem_base + lane_base + hoff + (qi * 64 + 16 * g) / 2, pk);
+                        }
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tr(22);
+                        arrive_leader(&hready[h]);
+                    }
+                }
+                if (args.save) {  // saved columns of both halves, under the first GEMM2 MMAs
+                    if (storer) bulk_wait_read<0>();
+                    named_bar_sync(1 + wg, 128);
+                    save_pend = false;
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {
+                        cur_t = 2 * u + h;
+#pragma unroll 1
+                        for (int rd = 0; rd < 2; ++rd) {
+                            const int qi = 2 * rd + (int)wg, qcol = qi * 64;
+                            if (!(qcol + 64 > args.save_col0 && qcol < args.save_col0 + args.save_cols)) continue;
+                            if (quarter_tma(qcol, 64)) {
+                                reclaim_wbuf();
+                                uint32_t pq[4][8];
+#pragma unroll
+                                for (int g = 0; g < 4; ++g)
+                                    tmem_ld8(tmem_base + lane_base + 256u * h + (qcol + 16 * g) / 2, pq[g]);
+                                tmem_ld_wait();
+#pragma unroll
+                                for (int g = 0; g < 4; ++g) stage16(pq[g], g);
+                                flush_quarter(qcol);
+                                continue;
+                            }
+#pragma unroll 1
+                            for (int g = 0; g < 4; ++g) {
+                                const int col = qcol + 16 * g;
+                                if (!(col + 16 > args.save_col0 && col < args.save_col0 + args.save_cols)) continue;
+                                uint32_t pk[8];
+                                tmem_ld8(tmem_base + lane_base + 256u * h + col / 2, pk);
+                                tmem_ld_wait();
+                                save_cols16(pk, col);
+                            }
+                        }
+                    }
+                }
+                tr(23);
+#pragma unroll 1
+                for (int j = 0; j < n2_tiles; ++j) {
+                    const int n0 = j * 128 + 64 * (int)wg;
+#pragma unroll 1
+                    for (int h = 0; h < 2; ++h) {
+                        mbar_wait(&tfull2[h], tpar[h]);
+                        tpar[h] ^= 1u;
+                        tr(24);
+                        tc_fence_after();
+                        uint32_t ra[32], rb[32];
+                        const uint32_t scol = 256u * h + 128u + 64u * wg;
+                        tmem_ld32(tmem_base + lane_base + scol, ra);
+                        tmem_ld32(tmem_base + lane_base + scol + 32, rb);
+                        tmem_ld_wait();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) arrive_leader(&tempty2[h]);
+                        if (lane == 0) bulk_wait_read<0>();  // this warp's previous stores have read `buf`
+                        save_pend = false;
+                        __syncwarp();
+                        const uint32_t row_addr = smem_u32(buf) + srow * 128;
+#pragma unroll
+                        for (int c = 0; c < 8; ++c) {
+                            float4 b0 = make_float4(0.f, 0.f, 0.f, 0.f), b1 = b0;
+                            if constexpr (C::kBiasTab) {
+                                b0 = reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)[0];
+                                b1 = reinterpret_cast<const float4*>(bias_tab + n0 + 8 * c)[1];
+                            }
+                            const float bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                            const uint32_t* src = (c < 4) ? ra : rb;
+                            const int o = (c & 3) * 8;
+                            uint32_t w[4];
+#pragma unroll
+                            for (int i = 0; i < 4; ++i)
+                                w[i] = pack_bf16x2(fmaf(__uint_as_float(src[o + 2 * i]), alpha, bv[2 * i]),
+                                                   fmaf(__uint_as_float(src[o + 2 * i + 1]), alpha, bv[2 * i + 1]));
+                            st_shared_v4(row_addr + ((uint32_t)(c ^ (srow & 7)) << 4), w[0], w[1], w[2], w[3]);
+                        }
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmYw, buf + q * 4096, n0, (2 * u + h) * tile_rows + (int)rank * 128 + (int)q * 32);
+                            bulk_commit();
+                        }
+                        tr(26);
+                    }
+                }
+            }
+        } else {
         int it = 0;
         for (int t = cluster_id; t < num_tiles; t += num_clusters, ++it) {
             cur_t = t;
@@ -943,6 +1188,7 @@ __global__ void __launch_bounds__(384, 1)
                 if (use_mask && issuer && j + 1 < n2_tiles) issue_mask(t, j + 1);  // mbuf was read by all
             }
         }
+        }  // kDT
         if (storer) bulk_wait<0>();
     }
 

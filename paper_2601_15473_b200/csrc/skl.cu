@@ -226,9 +226,9 @@ struct B2BSrc {
     const void *a1, *b1, *b1b, *b2, *b2b;
 };
 
-template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false, bool kSP = false>
+template <int kCG, int kMode, int kKind, int kPost = 0, bool kRS = false, bool kSP = false, bool kDT = false>
 skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, cudaStream_t st) {
-    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP>;
+    using C = dev::B2BCfg<kCG, kMode, kKind, kPost == 1 && kMode != 1, kRS, kSP || kDT>;
     constexpr int eb = C::kElem, bk = C::kBK;
     CUtensorMap ta, tb1, tb1b, tb2, tb2b, ty, tm, ts, tyw;
     SKL_TRY(make_tmap(&ta, src.a1, eb, a.K1, a.T, a.K1, bk, 128));
@@ -265,9 +265,10 @@ skl_status run_b2b_cg(const char* name, const B2BSrc& src, B2BArgs a, int sms, c
         SKL_TRY(make_tmap(&ts, a.save, 2, a.ld_save, a.save_cols, a.ld_save, 32, 64, CU_TENSOR_MAP_SWIZZLE_NONE));
         a.save_tma = 1;
     }
-    const int tiles = (a.T + 128 * kCG - 1) / (128 * kCG);
+    const int tiles = kDT ? ((a.T + 128 * kCG - 1) / (128 * kCG) + 1) / 2  // double tiles
+                          : (a.T + 128 * kCG - 1) / (128 * kCG);
     const int csize = kCG * (kRS ? a.nsplit : 1);  // CTAs per cluster
-    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS, kSP>;
+    auto kern = dev::b2b_kernel<kCG, kMode, kKind, kPost, kRS, kSP, kDT>;
     static std::atomic<uint64_t> attr_done{0};
     SKL_TRY(ensure_attrs(kern, C::kSmem, attr_done, /*clusters of 8 for 4 R-split pairs*/ kRS));
     cudaLaunchConfig_t cfg = {};
@@ -394,6 +395,15 @@ skl_status run_b2b(const char* name, int kind, int mode, const B2BSrc& src, B2BA
         static const int fwd_sp = getenv("SKL_FWD_SP") ? atoi(getenv("SKL_FWD_SP")) : -1;
         if (mode == 1 && a.R_pad > 256 && (fwd_sp == 1 || (fwd_sp < 0 && a.K1 >= 2048)))
             return run_b2b_cg<2, 1, 0, 0, false, true>(name, src, a, sms, st);
+        // R = 256 backward (the 768x768 projections): double tiles, one weight stream
+        // for two pair tiles (SKL_B2B_DT=0 off, =2 also the forward, measured slower:
+        // with the bias table it keeps only 3 of 48 KB stages; needs the per-warp stores)
+        static const int dt = getenv("SKL_B2B_DT") ? atoi(getenv("SKL_B2B_DT")) : 1;
+        static const int wst = getenv("SKL_B2B_WSTORE") ? atoi(getenv("SKL_B2B_WSTORE")) : 1;
+        if (dt && wst && a.R_pad == 256 && ((mode == 1 && dt == 2) || (mode == 2 && a.bias == nullptr))) {
+            if (mode == 1) return run_b2b_cg<2, 1, 0, 0, false, false, true>(name, src, a, sms, st);
+            return run_b2b_cg<2, 2, 0, 0, false, false, true>(name, src, a, sms, st);
+        }
         if (mode == 1) return run_b2b_cg<2, 1, 0>(name, src, a, sms, st);
         if (mode == 2) return run_b2b_cg<2, 2, 0>(name, src, a, sms, st);
         return run_b2b_cg<2, 0, 0>(name, src, a, sms, st);
