@@ -771,6 +771,30 @@ def test_rsplit_path_parity_in_subprocess():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+def test_store_and_tile_variants_are_bitwise_identical(tmp_path):
+    """The round-2 store and tiling variants change where bytes go, not the
+    arithmetic: the saved columns through per-warp TMA stores (SKL_SAVE_TMA) or
+    per-thread stores, per-warp or group output stores (SKL_B2B_WSTORE), and the
+    double-tile R = 256 backward (SKL_B2B_DT) or one tile per pair give bitwise
+    the same y, saved projection, dX, dU1s, dU2s and db."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    runs = {"default": {}, "no_tma_saves": {"SKL_SAVE_TMA": "0"}, "group_stores": {"SKL_B2B_WSTORE": "0"},
+            "single_tiles": {"SKL_B2B_DT": "0"}}
+    outs = {}
+    for name, extra in runs.items():
+        f = str(tmp_path / f"{name}.pt")
+        r = subprocess.run([sys.executable, "tests/store_paths_case.py", f], env=dict(os.environ, **extra), cwd=root,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        outs[name] = torch.load(f)
+    for name in runs:
+        for shape, tensors in outs["default"].items():
+            for key, t in tensors.items():
+                assert torch.equal(t, outs[name][shape][key]), f"{name}: {shape} {key} differs"
+
+
 def test_rsplit_is_deterministic(skl):
     """R > 512 backward twice: bitwise identical (both the default chain and, in
     the SKL_B2B_RSPLIT=1 subprocess, the DSMEM partial chain)."""
