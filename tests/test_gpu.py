@@ -771,6 +771,39 @@ def test_rsplit_path_parity_in_subprocess():
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("dtype_name", ["bf16", "tf32"])
+@pytest.mark.parametrize("d_in,d_out,L,k,T", [
+    (1024, 1024, 1, 64, 1),     # one token
+    (512, 768, 3, 48, 128),     # the largest small batch, L = 3, k % 64 != 0
+    (512, 768, 3, 48, 129),     # one past it: the fused kernels
+    (64, 4096, 2, 32, 17),      # wide output, ragged T
+])
+def test_small_batch_edges_match_oracle(skl, port, dtype_name, d_in, d_out, L, k, T):
+    """Edges of the small-batch path (T <= 128) and its hand-over to the fused
+    kernels at T = 129: forward and every gradient against the f64 oracle."""
+    import oracle
+    from tests._util import check_close
+    kind = skl.BF16 if dtype_name == "bf16" else skl.F32_TF32
+    s, (S1s, S2s, U1s, U2s), X, G, B, P, x64, g64, b64 = _make_case(skl, port, d_in, d_out, L, k, T, kind)
+    td = skl.torch_dtype(kind)
+    ws = torch.empty(max(skl.workspace_size(s, T)), dtype=torch.uint8, device="cuda")
+    sv = torch.empty(L * k, (T + 7) // 8 * 8, dtype=td, device="cuda")
+    y = torch.empty(T, d_out, dtype=td, device="cuda")
+    skl.forward(s, X, S1s, S2s, U1s, U2s, B, y, sv, ws)
+    gx = torch.empty(T, d_in, dtype=td, device="cuda")
+    du1 = torch.empty(L, k, d_out, device="cuda")
+    du2 = torch.empty(L, d_in, k, device="cuda")
+    db = torch.empty(d_out, device="cuda")
+    skl.backward(s, G, X, sv, S1s, S2s, U1s, U2s, gx, du1, du2, db, ws)
+    torch.cuda.synchronize()
+    check_close("y", _np(y), port.forward(P, b64, x64).T, dtype_name)
+    rgx, rgu1, rgu2, rgb = oracle.grads_to_abi(*port.backward(P, x64, g64))
+    check_close("grad_x", _np(gx), rgx, dtype_name)
+    check_close("dU1s", _np(du1), rgu1, dtype_name)
+    check_close("dU2s", _np(du2), rgu2, dtype_name)
+    check_close("db", _np(db), rgb, dtype_name)
+
+
 def test_store_and_tile_variants_are_bitwise_identical(tmp_path):
     """The round-2 store and tiling variants change where bytes go, not the
     arithmetic: the saved columns through per-warp TMA stores (SKL_SAVE_TMA) or
